@@ -1,0 +1,110 @@
+"""The CPU oracle against golden vectors produced by the real reference (scripts/make_golden.py)."""
+import numpy as np
+import pytest
+
+from oracle import colsolve, ext2d, geom, int3d, stepper
+from paper_2605_16082_b200.params import PhysParams
+
+P = PhysParams(f=1e-4, cd=2.5e-3, alpha=0.2, t_ref=12.5)
+
+
+def same(a, b, tol=0.0):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    if tol == 0.0:
+        assert np.array_equal(a, b), float(np.abs(a - b).max())
+    else:
+        assert np.abs(a - b).max() <= tol * max(np.abs(b).max(), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def mesh(golden):
+    g = golden("mesh")
+    raw = geom.make_mesh(g["vx"], g["vy"], g["vb"], g["raw_tri"])
+    return geom.hilbert_reorder(raw), raw, g
+
+
+def test_mesh_bitwise(mesh):
+    m, raw, g = mesh
+    same(raw.nbr, g["raw_nbr"]); same(raw.nbrk, g["raw_nbrk"])
+    for k in ["tri", "j2d", "dphx", "dphy", "elen", "enx", "eny", "nbr", "nbrk", "btag", "hilbert_perm", "b"]:
+        same(getattr(m, k), g[k])
+
+
+def test_ext2d(mesh, golden):
+    m = mesh[0]
+    g = golden("ext2d")
+    st = ext2d.S2(g["eta"], g["qx"], g["qy"])
+    same(ext2d.free_surface_residual(st, m, P, source=g["source"]), g["res_eta"])
+    same(ext2d.momentum_residual(st, m, P, f3d2d=g["f3d2d"], patm=g["patm"]), g["res_q"])
+    d = ext2d.tendencies(st, m, P, f3d2d=g["f3d2d"], source=g["source"], patm=g["patm"])
+    same(d[0], g["d_eta"]); same(d[1], g["d_qx"]); same(d[2], g["d_qy"])
+    d = ext2d.tendencies(st, m, P, els=g["els"], f3d2d=g["f3d2d"])
+    same(d[0], g["d_els_eta"]); same(d[1], g["d_els_qx"]); same(d[2], g["d_els_qy"])
+    s, qbx, qby, fx, fy = ext2d.subcycle(st, m, P, 10, 2.0, f3d2d=g["f3d2d"])
+    for a, k in [(s.eta, "sub_eta"), (s.qx, "sub_qx"), (s.qy, "sub_qy"), (qbx, "qbar_x"), (qby, "qbar_y"),
+                 (fx, "f2d_x"), (fy, "f2d_y")]:
+        same(a, g[k])
+    mo = geom.OMesh(**vars(m))
+    mo.btag = g["open_btag"]
+    d = ext2d.tendencies(st, mo, P, eta_bc=lambda t: 0.05 + 1e-3 * t)
+    same(d[0], g["open_d_eta"]); same(d[1], g["open_d_qx"]); same(d[2], g["open_d_qy"])
+
+
+def test_int3d(mesh, golden):
+    m = mesh[0]
+    g = golden("int3d")
+    L = int(g["L"])
+    G = geom.extrude(m, L, g["eta"])
+    G1 = geom.update_moving_mesh(G, g["eta1"], float(g["dt_mesh"]))
+    for k in ["z", "jz", "dzmid", "djz", "dztop", "dzbot"]:
+        same(getattr(G, k), g[k])
+    same(G1.w_m, g["w_m"])
+    same(ext2d.eos(g["T"], P), g["rho"])
+    M = int3d.prism_mass(G)
+    same(M, g["mass"])
+    q = int3d.project_transport(G, g["ux"], g["uy"], mass=M)
+    same(q, g["q"])
+    same(int3d.lateral_flux_factor(G, q, P), g["fac"])
+    same(int3d.compute_r(G, g["rho"], P), g["r"])
+    same(int3d.compute_w(G, q, g["ux"], g["uy"], P, g["fac"]), g["w"])
+    same(int3d.consistent_transport(G, q, g["qbx"], g["qby"]), g["qb"])
+    same(int3d.compute_wtilde(G, g["qb"], g["facb"]), g["wt"])
+    same(int3d.horizontal_rhs(G, g["ux"], g["uy"], g["qb"], g["facb"], g["r"], M, P), g["Fh"])
+    same(int3d.tracer_horizontal_rhs(G, g["T"], g["qb"], g["facb"], P), g["Ft"])
+    same(int3d.stress_rhs(G, 0.1 / 1025, -0.05 / 1025, 2.5e-3, g["ux"], g["uy"]), g["stress"])
+    A = int3d.assemble_vertical_operator(G, g["wt"], g["w_m"], 0.5, 1e-3)
+    same(A.d, g["A_d"]); same(A.u, g["A_u"]); same(A.w, g["A_w"])
+    Ai = int3d.build_implicit(int3d.prism_mass(G1), A, 20.0, G)
+    same(Ai.d, g["Ai_d"]); same(Ai.u, g["Ai_u"]); same(Ai.w, g["Ai_w"])
+    same(colsolve.block_thomas(Ai, g["rhs"]), g["xb"])
+    same(colsolve.banded_matvec(Ai, g["rhs"]), g["yb"])
+    same(int3d.mass_solve(M, g["rhs"].reshape(-1, 6, 2), G), g["ms"])
+    same(int3d.compute_r(G, g["rho"], P, els=g["els"]), g["r_els"])
+    same(int3d.horizontal_rhs(G, g["ux"], g["uy"], q, g["fac"], g["r"], M, P, els=g["els"]), g["Fh_els"])
+
+
+def test_columns(golden):
+    g = golden("columns")
+    same(colsolve.sweep_r(g["rhs"], g["j2d"]), g["r_out"])
+    same(colsolve.sweep_w(g["rhs"], g["j2d"]), g["w_out"])
+    same(ext2d.mh_apply(g["rhs"][:, 0, 0:3], g["j2d"]), g["mh"])
+    same(ext2d.mh_inv_apply(g["rhs"][:, 0, 0:3], g["j2d"]), g["mhinv"])
+    same(colsolve.thomas(g["lower"], g["diag"], g["upper"], g["trhs"]), g["tri_x"])
+    mh = 1.7 * np.array([[2.0, 1, 1], [1, 2, 1], [1, 1, 2]]) / 24.0
+    same(colsolve.dense_sweep_matrix("r", 3, mh), g["dense_r"])
+    same(colsolve.dense_sweep_matrix("w", 3, mh), g["dense_w"])
+
+
+def test_step(mesh, golden):
+    from types import SimpleNamespace
+    m = mesh[0]
+    g = golden("step")
+    L = int(g["L"])
+    p = PhysParams(f=1e-4, cd=2.5e-3, alpha=0.2, t_ref=12.5, tau_x=0.05, tau_y=-0.02)
+    s = SimpleNamespace(grid=geom.extrude(m, L, g["eta"]), ux=g["ux"], uy=g["uy"], T=g["T0"],
+                        s2d=ext2d.S2(g["eta"].copy(), g["qx"], g["qy"], 0.0))
+    for i in range(2):
+        s = stepper.imex_step(s, p, float(g["dt"]), int(g["m"]), float(g["kv"]), float(g["nu_v"]))
+        for n, a in [("ux", s.ux), ("uy", s.uy), ("T", s.T), ("eta", s.s2d.eta), ("qx", s.s2d.qx), ("qy", s.s2d.qy)]:
+            same(a, g[f"s{i}_{n}"])
