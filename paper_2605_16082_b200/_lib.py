@@ -1,0 +1,74 @@
+"""ctypes binding of libprismdg_b200.so (include/prismdg_b200.h).
+
+There is no fallback: if the library is missing or a CUDA device is absent,
+every compute entry raises.  The library is built in-tree by
+`python -m paper_2605_16082_b200.build` (or __graft_entry__.build()).
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprismdg_b200.so")
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+D = ctypes.c_double
+LL = ctypes.c_longlong
+
+
+class MeshDesc(ctypes.Structure):
+    _fields_ = [("nt", I), ("j2d", P), ("dphx", P), ("dphy", P), ("elen", P), ("enx", P), ("eny", P), ("b", P),
+                ("nbr", P), ("nbrk", P), ("btag", P), ("min_edge", D)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "pdg_ctx_create": (I, [ctypes.POINTER(MeshDesc), I, ctypes.POINTER(P)]),
+    "pdg_ctx_destroy": (I, [P]),
+    "pdg_ctx_set_layers": (I, [P, I, P]),
+    "pdg_last_error": (I, [P, P, ctypes.POINTER(I), ctypes.POINTER(LL), ctypes.POINTER(LL), ctypes.POINTER(D)]),
+    "pdg_cuda_error_string": (ctypes.c_char_p, []),
+    "pdg_launch_count": (LL, [P]),
+    "pdg_ext2d_eval": (I, [P, P, P, P, P, P, P, I, D, D, D, P, I, I, P, P, P, P]),
+    "pdg_ext2d_subcycle": (I, [P, P, I, D, D, D, P, P, P, P, P, P, I, P]),
+    "pdg_ext2d_cfl": (I, [P, P, D, D, P, P]),
+    "pdg_apply_mh": (I, [P, P, I, I, I, P, P, P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the CDLL; raises if the extension is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA extension not built: {LIB_PATH} missing "
+                               "(run `python -m paper_2605_16082_b200.build`); there is no CPU fallback")
+        l = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name, None)
+            if fn is None:
+                continue
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def declare(name, res, args):
+    _SIGS[name] = (res, args)
+    if _lib is not None:
+        fn = getattr(_lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def check(rc, what=""):
+    if rc != 0:
+        msg = lib().pdg_cuda_error_string().decode(errors="replace")
+        raise RuntimeError(f"{what}: CUDA error ({rc}) {msg}")

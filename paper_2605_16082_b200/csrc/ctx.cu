@@ -1,0 +1,126 @@
+// Context lifetime, mesh upload (reference (nt,3) host layout -> device SoA), error word.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ctx.cuh"
+
+static thread_local char g_errbuf[512] = "";
+static long long g_noctx_launches = 0;
+
+namespace pdg {
+int check_launch(pdg_ctx* ctx) {
+  if (ctx) ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_errbuf, sizeof(g_errbuf), "%s", cudaGetErrorString(e));
+    return PDG_ERR_CUDA;
+  }
+  return PDG_OK;
+}
+int check_launch_noctx() {
+  g_noctx_launches++;
+  return check_launch(nullptr);
+}
+}  // namespace pdg
+
+template <typename T>
+static int upload_soa3(const T* host_nt3, int nt, T** dev) {
+  // (nt,3) -> [3][nt]
+  std::vector<T> tmp((size_t)3 * nt);
+  for (int c = 0; c < nt; ++c)
+    for (int k = 0; k < 3; ++k) tmp[(size_t)k * nt + c] = host_nt3[(size_t)c * 3 + k];
+  if (cudaMalloc(dev, tmp.size() * sizeof(T)) != cudaSuccess) return PDG_ERR_CUDA;
+  if (cudaMemcpy(*dev, tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+    return PDG_ERR_CUDA;
+  return PDG_OK;
+}
+
+static int upload_int3(const int64_t* host_nt3, int nt, int** dev) {
+  std::vector<int> tmp((size_t)3 * nt);
+  for (int c = 0; c < nt; ++c)
+    for (int k = 0; k < 3; ++k) tmp[(size_t)k * nt + c] = (int)host_nt3[(size_t)c * 3 + k];
+  if (cudaMalloc(dev, tmp.size() * sizeof(int)) != cudaSuccess) return PDG_ERR_CUDA;
+  if (cudaMemcpy(*dev, tmp.data(), tmp.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+    return PDG_ERR_CUDA;
+  return PDG_OK;
+}
+
+extern "C" {
+
+int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return pdg::check_launch(nullptr), PDG_ERR_CUDA;
+  pdg_ctx* c = new pdg_ctx();
+  c->device = device;
+  c->nt = d->nt;
+  c->min_edge = d->min_edge;
+  int nt = d->nt;
+  int rc = PDG_OK;
+  rc |= cudaMalloc(&c->j2d, nt * sizeof(double)) != cudaSuccess;
+  rc |= cudaMemcpy(c->j2d, d->j2d, nt * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess;
+  rc |= upload_soa3(d->dphx, nt, &c->dphx);
+  rc |= upload_soa3(d->dphy, nt, &c->dphy);
+  rc |= upload_soa3(d->elen, nt, &c->elen);
+  rc |= upload_soa3(d->enx, nt, &c->enx);
+  rc |= upload_soa3(d->eny, nt, &c->eny);
+  rc |= upload_soa3(d->b, nt, &c->b);
+  rc |= upload_int3(d->nbr, nt, &c->nbr);
+  rc |= upload_int3(d->nbrk, nt, &c->nbrk);
+  rc |= upload_int3(d->btag, nt, &c->btag);
+  rc |= cudaMalloc(&c->err, sizeof(pdg_err)) != cudaSuccess;
+  rc |= cudaMemset(c->err, 0, sizeof(pdg_err)) != cudaSuccess;
+  rc |= cudaMalloc(&c->red, 4096 * sizeof(double)) != cudaSuccess;
+  rc |= cudaMalloc(&c->ws2d, (size_t)(9 + 9 + 6) * nt * sizeof(double)) != cudaSuccess;
+  if (rc) {
+    snprintf(g_errbuf, sizeof(g_errbuf), "pdg_ctx_create: %s", cudaGetErrorString(cudaGetLastError()));
+    pdg_ctx_destroy(c);
+    return PDG_ERR_CUDA;
+  }
+  *out = c;
+  return PDG_OK;
+}
+
+int pdg_ctx_destroy(pdg_ctx* c) {
+  if (!c) return PDG_OK;
+  void* ptrs[] = {c->j2d, c->dphx, c->dphy, c->elen, c->enx, c->eny, c->b, c->fracs,
+                  c->nbr, c->nbrk, c->btag, c->err, c->red, c->ws2d, c->ws3d};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+  return PDG_OK;
+}
+
+int pdg_ctx_set_layers(pdg_ctx* c, int L, const double* fracs) {
+  if (L < 1) return PDG_ERR_SHAPE;
+  if (c->fracs) cudaFree(c->fracs);
+  c->fracs = nullptr;
+  if (cudaMalloc(&c->fracs, (L + 1) * sizeof(double)) != cudaSuccess) return PDG_ERR_CUDA;
+  if (cudaMemcpy(c->fracs, fracs, (L + 1) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    return PDG_ERR_CUDA;
+  c->fracs_host.assign(fracs, fracs + L + 1);
+  c->L = L;
+  return PDG_OK;
+}
+
+int pdg_last_error(pdg_ctx* c, void* stream, int* code, long long* i0, long long* i1, double* val) {
+  pdg_err h;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(&h, c->err, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess) return PDG_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
+    snprintf(g_errbuf, sizeof(g_errbuf), "%s", cudaGetErrorString(cudaGetLastError()));
+    return PDG_ERR_CUDA;
+  }
+  if (h.code != 0) cudaMemsetAsync(c->err, 0, sizeof(pdg_err), s);
+  *code = h.code;
+  *i0 = h.i0;
+  *i1 = h.i1;
+  *val = h.val;
+  return PDG_OK;
+}
+
+const char* pdg_cuda_error_string(void) { return g_errbuf; }
+
+long long pdg_launch_count(pdg_ctx* c) { return c ? c->launches : g_noctx_launches; }
+
+}  // extern "C"

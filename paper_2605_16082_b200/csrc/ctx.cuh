@@ -1,0 +1,59 @@
+// Context object behind the opaque pdg_ctx handle (host side).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+struct pdg_ctx {
+  int device = 0;
+  int nt = 0;
+  int L = 0;
+  double min_edge = 0.0;
+  double *j2d = nullptr, *dphx = nullptr, *dphy = nullptr, *elen = nullptr, *enx = nullptr, *eny = nullptr,
+         *b = nullptr, *fracs = nullptr;
+  int *nbr = nullptr, *nbrk = nullptr, *btag = nullptr;
+  pdg_err* err = nullptr;     // device error word
+  double* red = nullptr;      // reduction scratch (device)
+  double* ws2d = nullptr;     // 2D subcycle workspace: 2 stage states + q0
+  double* ws3d = nullptr;     // 3D workspace (block-Thomas propagation tiles)
+  size_t ws3d_doubles = 0;
+  long long launches = 0;
+  std::vector<double> fracs_host;
+
+  pdg::DMesh view() const {
+    pdg::DMesh m;
+    m.nt = nt;
+    m.L = L;
+    m.j2d = j2d;
+    m.dphx = dphx;
+    m.dphy = dphy;
+    m.elen = elen;
+    m.enx = enx;
+    m.eny = eny;
+    m.b = b;
+    m.nbr = nbr;
+    m.nbrk = nbrk;
+    m.btag = btag;
+    m.fracs = fracs;
+    m.err = err;
+    return m;
+  }
+  // grows the 3D workspace (never on the hot path once sized)
+  double* ws3(size_t n) {
+    if (n > ws3d_doubles) {
+      if (ws3d) cudaFree(ws3d);
+      ws3d = nullptr;
+      if (cudaMalloc(&ws3d, n * sizeof(double)) != cudaSuccess) {
+        ws3d_doubles = 0;
+        return nullptr;
+      }
+      ws3d_doubles = n;
+    }
+    return ws3d;
+  }
+};
+
+namespace pdg {
+int check_launch(pdg_ctx* ctx);  // returns PDG_OK or PDG_ERR_CUDA and counts the launch
+int check_launch_noctx();
+}  // namespace pdg
