@@ -33,6 +33,32 @@ _SIGS = {
     "pdg_ext2d_subcycle": (I, [P, P, I, D, D, D, P, P, P, P, P, P, I, P]),
     "pdg_ext2d_cfl": (I, [P, P, D, D, P, P]),
     "pdg_apply_mh": (I, [P, P, I, I, I, P, P, P]),
+    "pdg_eos": (I, [P, P, LL, D, D, D, D, P, P]),
+    # internal3d (csrc/int3d.cu)
+    "pdg_prism_mass": (I, [P, P, P, I, P, P]),
+    "pdg_project_transport": (I, [P, P, P, P, P, P, I, P, P, P, P]),
+    "pdg_column_sum": (I, [I, I, I, P, P, P]),
+    "pdg_total_thickness": (I, [P, P, P, P]),
+    "pdg_mismatch": (I, [P, P, P, P, P, P]),
+    "pdg_consistent_transport": (I, [P, P, P, P, P, I, P, P]),
+    "pdg_lateral_flux_factor": (I, [P, P, P, D, P, I, P, P]),
+    "pdg_compute_r": (I, [P, P, P, I, D, D, D, P, I, P, P]),
+    "pdg_compute_w": (I, [P, P, P, P, P, P, P, I, P, P]),
+    "pdg_compute_wtilde": (I, [P, P, P, P, P, D, P, I, P, P]),
+    "pdg_horizontal_rhs": (I, [P, P, P, I, P, P, P, P, D, D, I, P, I, P, P]),
+    "pdg_mass_terms": (I, [I, I, P, P, P, D, D, P, P]),
+    "pdg_stress_rhs": (I, [P, P, P, D, D, D, P, I, P, P]),
+    "pdg_step_f3d2d": (I, [P, P, P, P, P, D, D, D, D, D, D, P, P]),
+    "pdg_step_rhs": (I, [P, I, P, P, P, P, P, P, P, P, P, D, D, D, D, D, D, D, P, P]),
+    # columns (csrc/columns.cu)
+    "pdg_solve_sweep": (I, [I, I, I, I, P, P, P, P, P, P]),
+    "pdg_solve_banded": (I, [I, I, I, P, P, P, P, P, P, P, P, P]),
+    "pdg_apply_banded": (I, [I, I, I, P, P, P, P, P, P]),
+    "pdg_build_implicit": (I, [LL, P, P, P, P, D, P, P, P, P]),
+    "pdg_mass_op": (I, [I, I, I, I, P, P, P, P, P]),
+    "pdg_solve_tridiagonal": (I, [I, I, P, P, P, P, P, P, P, P]),
+    "pdg_assemble_vertical": (I, [P, P, P, P, D, D, D, I, P, I, P, P, P, P]),
+    "pdg_step_vertical": (I, [P, I, I, P, P, P, D, P, D, D, D, I, D, P, P, P, P]),
 }
 
 _lib = None

@@ -1,0 +1,194 @@
+// Device building blocks shared by the 3D assemblies (internal3d.py) and the fused stepper.
+//
+// Execution model: ONE THREAD PER COLUMN looping over layers.  A warp covers 32 consecutive
+// (Hilbert-ordered) columns, so every per-layer load of a P6 plane is a coalesced 256-byte
+// run; per-column 2D data stays in registers across the whole layer loop; vertical sweeps
+// (r, w, w~, block Thomas) are carried in registers between layer iterations.
+#pragma once
+#include "common.cuh"
+
+namespace pdg {
+
+__device__ __forceinline__ void ld6(const double* __restrict__ f, int l, int c, int L, int nt, double v[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = f[((size_t)k * L + l) * nt + c];
+}
+__device__ __forceinline__ void st6(double* __restrict__ f, int l, int c, int L, int nt, const double v[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) f[((size_t)k * L + l) * nt + c] = v[k];
+}
+
+// the 4 lateral nodes (t0, t1, b0, b1) of the neighbour prism across local edge k2 of column e2
+__device__ __forceinline__ void ld_nb4(const double* __restrict__ f, int k2, int e2, int l, int L, int nt,
+                                       double n4[4]) {
+  const int a = EV0(k2), b = EV1(k2);
+  n4[0] = f[((size_t)a * L + l) * nt + e2];
+  n4[1] = f[((size_t)b * L + l) * nt + e2];
+  n4[2] = f[((size_t)(3 + a) * L + l) * nt + e2];
+  n4[3] = f[((size_t)(3 + b) * L + l) * nt + e2];
+}
+
+// own lateral trace on edge k at the 2v x 2h face points (internal3d.py:229-258, mirror=False)
+__device__ __forceinline__ void tr_own(const double v[6], int k, double t[2][2]) {
+  const int a = EV0(k), b = EV1(k);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double ht = v[a] * ES[h][0] + v[b] * ES[h][1];
+    const double hb = v[3 + a] * ES[h][0] + v[3 + b] * ES[h][1];
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv) t[vv][h] = VS[vv][0] * ht + VS[vv][1] * hb;
+  }
+}
+// neighbour trace at the same physical points (mirrored edge-point order)
+__device__ __forceinline__ void tr_nb(const double n4[4], double t[2][2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double ht = n4[0] * ES[h][1] + n4[1] * ES[h][0];
+    const double hb = n4[2] * ES[h][1] + n4[3] * ES[h][0];
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv) t[vv][h] = VS[vv][0] * ht + VS[vv][1] * hb;
+  }
+}
+// zeta-independent corner data on the two edge points
+__device__ __forceinline__ void tr2_own(const double c3[3], int k, double t[2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) t[h] = c3[EV0(k)] * ES[h][0] + c3[EV1(k)] * ES[h][1];
+}
+__device__ __forceinline__ void tr2_nb(double a, double b, double t[2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) t[h] = a * ES[h][1] + b * ES[h][0];
+}
+// corner data duplicated on both levels, traced like a prism field
+__device__ __forceinline__ void tr_dup(const double t2[2], double t[2][2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv) t[vv][h] = VS[vv][0] * t2[h] + VS[vv][1] * t2[h];
+}
+
+// acc[node] += s * sum_vh VS[v][lev] ES[h][hn] x[v][h] over the 4 lateral nodes of edge k
+// (internal3d.py:261-272; s = sign * Jedge)
+__device__ __forceinline__ void lat_add(double acc[6], int k, const double x[2][2], double s) {
+#pragma unroll
+  for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+    for (int hn = 0; hn < 2; ++hn) {
+      double t = 0.0;
+#pragma unroll
+      for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) t += VS[vv][lev] * ES[h][hn] * x[vv][h];
+      acc[3 * lev + (hn == 0 ? EV0(k) : EV1(k))] += s * t;
+    }
+}
+
+// per-column neighbour data of one interior edge, loaded once per column
+struct EdgeNb {
+  int e2, k2;
+  double eta0, eta1, b0, b1;  // neighbour free surface / bed at its edge corners (own traversal order)
+  double stab[2];             // 0.5 [[eta]] max(c) at the two edge points (internal3d.py:296-301)
+};
+
+__device__ __forceinline__ void edge_setup(const DMesh& m, const Col& C, const double eta[3],
+                                           const double* __restrict__ eta_g, int k, double g, EdgeNb& E) {
+  const int nt = m.nt;
+  E.e2 = C.nb[k];
+  E.k2 = C.nk[k];
+  if (C.tag[k] != 0) return;
+  const int i0 = EV0(E.k2) * nt + E.e2, i1 = EV1(E.k2) * nt + E.e2;
+  E.eta0 = eta_g[i0];
+  E.eta1 = eta_g[i1];
+  E.b0 = ldg(m.b + i0);
+  E.b1 = ldg(m.b + i1);
+  double ei[2], ee[2], bi[2], be[2];
+  tr2_own(eta, k, ei);
+  tr2_own(C.b, k, bi);
+  tr2_nb(E.eta0, E.eta1, ee);
+  tr2_nb(E.b0, E.b1, be);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double hi = ei[h] - bi[h], he = ee[h] - be[h];
+    E.stab[h] = 0.5 * (ei[h] - ee[h]) * fmax(sqrt(g * hi), sqrt(g * he));
+  }
+}
+
+// neighbour half thicknesses at its two edge corners for layer fractions (ft, fb)
+__device__ __forceinline__ void nb_jz(const EdgeNb& E, double ft, double fb, double& j0, double& j1) {
+  const double H0 = __dsub_rn(E.eta0, E.b0), H1 = __dsub_rn(E.eta1, E.b1);
+  j0 = __dmul_rn(0.5, __dsub_rn(__dsub_rn(E.eta0, __dmul_rn(ft, H0)), __dsub_rn(E.eta0, __dmul_rn(fb, H0))));
+  j1 = __dmul_rn(0.5, __dsub_rn(__dsub_rn(E.eta1, __dmul_rn(ft, H1)), __dsub_rn(E.eta1, __dmul_rn(fb, H1))));
+}
+
+// stabilised lateral flux factor n.{q} + {Jz/H} max(c) [[eta]] on interior edge k
+// (internal3d.py:275-314).  qo: own q (2 comps x 6 nodes), qn: neighbour lateral nodes (2 x 4)
+__device__ __forceinline__ void lat_factor(const Col& C, const EdgeNb& E, int k, const double jz[3],
+                                           const double eta[3], double ft, double fb, const double qo[2][6],
+                                           const double qn[2][4], double fac[2][2]) {
+  double ti[2][2][2], te[2][2][2];  // [comp][v][h]
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    tr_own(qo[cc], k, ti[cc]);
+    tr_nb(qn[cc], te[cc]);
+  }
+  double jo[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) jo[i] = jz[i] / (eta[i] - C.b[i]);
+  double j0, j1;
+  nb_jz(E, ft, fb, j0, j1);
+  j0 = j0 / (E.eta0 - E.b0);
+  j1 = j1 / (E.eta1 - E.b1);
+  double a2[2], b2[2], ja[2][2], jb[2][2];
+  tr2_own(jo, k, a2);
+  tr2_nb(j0, j1, b2);
+  tr_dup(a2, ja);
+  tr_dup(b2, jb);
+#pragma unroll
+  for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double qx = 0.5 * (ti[0][vv][h] + te[0][vv][h]);
+      const double qy = 0.5 * (ti[1][vv][h] + te[1][vv][h]);
+      const double jm = 0.5 * (ja[vv][h] + jb[vv][h]);
+      fac[vv][h] = C.nx[k] * qx + C.ny[k] * qy + jm * E.stab[h];
+    }
+}
+
+// iso-zeta divergence test term: acc[lev*3+i] += J2D (dphx_i S[lev][0] + dphy_i S[lev][1])
+__device__ __forceinline__ void iso_add(const Col& C, const double S[2][2], double acc[6]) {
+#pragma unroll
+  for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) acc[3 * lev + i] += C.j2d * (C.dx[i] * S[lev][0] + C.dy[i] * S[lev][1]);
+}
+
+// values of a prism nodal field at the 12 tensor points: out[v][q]
+__device__ __forceinline__ void at_pts(const double f[6], double out[2][6]) {
+  double t[6], b[6];
+  hq(f, t);
+  hq(f + 3, b);
+#pragma unroll
+  for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out[vv][q] = VS[vv][0] * t[q] + VS[vv][1] * b[q];
+}
+
+// S[m][d] = sum_vq QW VS[v][m] a[v][q] b_d[v][q]   (volume advection against phi_z grad_h phi_h)
+__device__ __forceinline__ void adv_moment(const double a[2][6], const double bx[2][6], const double by[2][6],
+                                           double S[2][2]) {
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    double sx = 0.0, sy = 0.0;
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double w = QW[q] * VS[vv][mm] * a[vv][q];
+        sx += w * bx[vv][q];
+        sy += w * by[vv][q];
+      }
+    S[mm][0] = sx;
+    S[mm][1] = sy;
+  }
+}
+
+}  // namespace pdg

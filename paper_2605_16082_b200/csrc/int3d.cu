@@ -1,0 +1,1197 @@
+// 3D internal-mode assemblies (internal3d.py), one thread per column, layer loop inside.
+//
+// Each kernel has an API flavour (inputs exactly as the reference passes them: explicit
+// factor / mass / q arrays) and, where the stepper needs it, a FUSED flavour that rebuilds
+// the flux factor, the consistent transport q~ and the prism masses on the fly, so those
+// 12-, 36- and 12-double-per-prism intermediates never touch HBM.
+#include "col3d.cuh"
+#include "ctx.cuh"
+
+namespace pdg {
+
+struct Cols {
+  const int* els;
+  int n;
+  __device__ __forceinline__ int col(int i) const { return els ? els[i] : i; }
+};
+
+__device__ __forceinline__ void load_eta(const double* __restrict__ e, int c, int nt, double eta[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) eta[i] = e[i * nt + c];
+}
+
+// ============================================================================ prism mass
+// internal3d.py:114-123.  M[i][j] = K[li][lj] J2D Mjz[ai][aj] (Kronecker form of the 12-point rule)
+__global__ void k_prism_mass(DMesh m, const double* __restrict__ eta_g, Cols cs, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const double j2d = ldg(m.j2d + c);
+  double eta[3], b[3];
+  load_eta(eta_g, c, nt, eta);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) b[k] = ldg(m.b + k * nt + c);
+  const double K[2][2] = {{VS[0][0] * VS[0][0] + VS[1][0] * VS[1][0], VS[0][0] * VS[0][1] + VS[1][0] * VS[1][1]},
+                          {VS[0][1] * VS[0][0] + VS[1][1] * VS[1][0], VS[0][1] * VS[0][1] + VS[1][1] * VS[1][1]}};
+  for (int l = 0; l < L; ++l) {
+    double jz[3], jzq[6], Mh[3][3];
+    layer_jz(b, eta, m.fracs[l], m.fracs[l + 1], jz);
+    hq(jz, jzq);
+    mass_h(jzq, Mh);
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int s = 0; s < 6; ++s) out[((size_t)(r * 6 + s) * L + l) * nt + c] = K[r / 3][s / 3] * (j2d * Mh[r % 3][s % 3]);
+  }
+}
+
+// ============================================================================ projection
+// internal3d.py:164-181: M q = <phi (Jz u) J2D Jz>.  Kronecker path: q_lev = Mjz^-1 R_lev,
+// R_lev[a] = sum_q QW BARY_a jzq^2 u_lev(q) (K and J2D cancel).  Optional outputs: the
+// vertical-DOF column sum of q (internal3d.py:184-187) and total thickness 2 sum Jz (mesh.py:422).
+template <bool MASS_GIVEN>
+__global__ void k_project(DMesh m, const double* __restrict__ eta_g, const double* __restrict__ ux,
+                          const double* __restrict__ uy, const double* __restrict__ mass, Cols cs,
+                          double* __restrict__ q, double* __restrict__ qsum, double* __restrict__ htot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  const double j2d = ldg(m.j2d + c);
+  double eta[3], b[3];
+  load_eta(eta_g, c, nt, eta);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) b[k] = ldg(m.b + k * nt + c);
+  double st[2][3] = {{0, 0, 0}, {0, 0, 0}}, sb[2][3] = {{0, 0, 0}, {0, 0, 0}}, hs[3] = {0, 0, 0};
+  for (int l = 0; l < L; ++l) {
+    double jz[3], jzq[6];
+    layer_jz(b, eta, m.fracs[l], m.fracs[l + 1], jz);
+    hq(jz, jzq);
+    double u[2][6];
+    ld6(ux, l, c, L, nt, u[0]);
+    ld6(uy, l, c, L, nt, u[1]);
+    double out[2][6];
+    if (MASS_GIVEN) {
+      double a[6][6], rhs[6][2];
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int s = 0; s < 6; ++s) a[r][s] = mass[((size_t)(r * 6 + s) * L + l) * nt + c];
+      double up[2][2][6];
+      at_pts(u[0], up[0]);
+      at_pts(u[1], up[1]);
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          double t = 0.0;
+#pragma unroll
+          for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+            for (int qq = 0; qq < 6; ++qq)
+              t += QW[qq] * (j2d * jzq[qq] * jzq[qq]) * up[cc][vv][qq] * (VS[vv][r / 3] * BARY[qq][r % 3]);
+          rhs[r][cc] = t;
+        }
+      const int bad = lu6(a);
+      if (bad >= 0) report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
+      lu6_solve<2>(a, rhs);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        out[0][r] = rhs[r][0];
+        out[1][r] = rhs[r][1];
+      }
+    } else {
+      double Mh[3][3];
+      mass_h(jzq, Mh);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev) {
+          double uq[6], R[3] = {0, 0, 0};
+          hq(u[cc] + 3 * lev, uq);
+#pragma unroll
+          for (int qq = 0; qq < 6; ++qq) {
+            const double w = QW[qq] * jzq[qq] * jzq[qq] * uq[qq];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) R[a] += w * BARY[qq][a];
+          }
+          double A[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) A[a][bb] = Mh[a][bb];
+          if (!solve3(A, R)) report(m.err, PDG_ERR_ZERO_PIVOT, l, 3 * lev, 0.0);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) out[cc][3 * lev + a] = R[a];
+        }
+    }
+    st6(q, l, c, L, nt, out[0]);
+    st6(q + P6, l, c, L, nt, out[1]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      st[0][a] += out[0][a];
+      st[1][a] += out[1][a];
+      sb[0][a] += out[0][3 + a];
+      sb[1][a] += out[1][3 + a];
+      hs[a] += jz[a];
+    }
+  }
+  if (qsum) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      qsum[a * nt + c] = st[0][a] + sb[0][a];
+      qsum[(3 + a) * nt + c] = st[1][a] + sb[1][a];
+    }
+  }
+  if (htot) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) htot[a * nt + c] = 2.0 * hs[a];
+  }
+}
+
+// vertical-DOF column sum of an N-component P6 field (internal3d.py:184-187) and total thickness
+__global__ void k_colsum(int nt, int L, int ncomp, const double* __restrict__ f, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nt) return;
+  for (int cc = 0; cc < ncomp; ++cc) {
+    const double* fc = f + (size_t)cc * 6 * L * nt;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double st = 0.0, sb = 0.0;
+      for (int l = 0; l < L; ++l) {
+        st += fc[((size_t)a * L + l) * nt + c];
+        sb += fc[((size_t)(3 + a) * L + l) * nt + c];
+      }
+      out[(cc * 3 + a) * nt + c] = st + sb;
+    }
+  }
+}
+
+__global__ void k_htot(DMesh m, const double* __restrict__ eta_g, double* __restrict__ htot) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = m.nt;
+  if (c >= nt) return;
+  double eta[3], b[3], hs[3] = {0, 0, 0};
+  load_eta(eta_g, c, nt, eta);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) b[k] = ldg(m.b + k * nt + c);
+  for (int l = 0; l < m.L; ++l) {
+    double jz[3];
+    layer_jz(b, eta, m.fracs[l], m.fracs[l + 1], jz);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) hs[a] += jz[a];
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) htot[a * nt + c] = 2.0 * hs[a];
+}
+
+// transport mismatch (Qbar - sum_col q) / H per column corner (internal3d.py:198-200)
+__global__ void k_mismatch(int nt, const double* __restrict__ qbar, const double* __restrict__ qsum,
+                           const double* __restrict__ htot, double* __restrict__ mis) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nt) return;
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int o = (cc * 3 + a) * nt + c;
+      mis[o] = (qbar[o] - qsum[o]) / htot[a * nt + c];
+    }
+}
+
+// consistent_transport (internal3d.py:190-208): qbar = q + Jz mis, both levels
+__global__ void k_consistent(DMesh m, const double* __restrict__ eta_g, const double* __restrict__ q,
+                             const double* __restrict__ mis, Cols cs, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  double eta[3], b[3], mi[2][3];
+  load_eta(eta_g, c, nt, eta);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    b[k] = ldg(m.b + k * nt + c);
+    mi[0][k] = mis[k * nt + c];
+    mi[1][k] = mis[(3 + k) * nt + c];
+  }
+  for (int l = 0; l < L; ++l) {
+    double jz[3];
+    layer_jz(b, eta, m.fracs[l], m.fracs[l + 1], jz);
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      double v[6];
+      ld6(q + cc * P6, l, c, L, nt, v);
+#pragma unroll
+      for (int n = 0; n < 6; ++n) v[n] = v[n] + jz[n % 3] * mi[cc][n % 3];
+      st6(out + cc * P6, l, c, L, nt, v);
+    }
+  }
+}
+
+// ============================================================================ flux factor (API)
+__global__ void k_factor(DMesh m, const double* __restrict__ eta_g, const double* __restrict__ q, double g, Cols cs,
+                         double* __restrict__ fac) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3];
+  load_eta(eta_g, c, nt, eta);
+  EdgeNb E[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) edge_setup(m, C, eta, eta_g, k, g, E[k]);
+  for (int l = 0; l < L; ++l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    double jz[3];
+    layer_jz(C.b, eta, ft, fb, jz);
+    double qo[2][6];
+    ld6(q, l, c, L, nt, qo[0]);
+    ld6(q + P6, l, c, L, nt, qo[1]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double f[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      if (C.tag[k] == 0) {
+        double qn[2][4];
+        ld_nb4(q, E[k].k2, E[k].e2, l, L, nt, qn[0]);
+        ld_nb4(q + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
+        lat_factor(C, E[k], k, jz, eta, ft, fb, qo, qn, f);
+      }
+#pragma unroll
+      for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) fac[((size_t)((k * 2 + vv) * 2 + h) * L + l) * nt + c] = f[vv][h];
+    }
+  }
+}
+
+__device__ __forceinline__ void ld_fac(const double* __restrict__ fac, int k, int l, int c, int L, int nt,
+                                       double f[2][2]) {
+#pragma unroll
+  for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) f[vv][h] = fac[((size_t)((k * 2 + vv) * 2 + h) * L + l) * nt + c];
+}
+
+// ============================================================================ baroclinic head r
+// internal3d.py:327-405 + columns.py:95-122.  FROM_T: rho' = -alpha (T - t_ref) inline.
+template <bool FROM_T>
+__global__ void __launch_bounds__(128) k_compute_r(DMesh m, const double* __restrict__ eta_g,
+                                                   const double* __restrict__ rhoT, double alpha, double tref,
+                                                   double g, Cols cs, double* __restrict__ r) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3];
+  load_eta(eta_g, c, nt, eta);
+  EdgeNb E[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) edge_setup(m, C, eta, eta_g, k, g, E[k]);
+  const double ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
+  const double ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
+  const double j2d = C.j2d;
+  double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  double prevb[3] = {0, 0, 0};
+  for (int l = 0; l < L; ++l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    LGeo G;
+    layer_geo(C, eta, ft, fb, G);
+    double rho[6];
+    ld6(rhoT, l, c, L, nt, rho);
+    if (FROM_T) {
+#pragma unroll
+      for (int n = 0; n < 6; ++n) rho[n] = -alpha * (rho[n] - tref);
+    }
+    double jzq[6];
+    hq(G.jz, jzq);
+    double acc[2][6] = {{0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}};
+    // volume: -g <phi grad_h(rho) J2D Jz>, grad_h = iso part + m_h d/dzeta  (meas * m_h = -J2D mid2)
+    {
+      double gi[2][2];
+#pragma unroll
+      for (int lev = 0; lev < 2; ++lev) {
+        gi[lev][0] = (rho[3 * lev] * C.dx[0] + rho[3 * lev + 1] * C.dx[1]) + rho[3 * lev + 2] * C.dx[2];
+        gi[lev][1] = (rho[3 * lev] * C.dy[0] + rho[3 * lev + 1] * C.dy[1]) + rho[3 * lev + 2] * C.dy[2];
+      }
+      double rt[6], rb[6];
+      hq(rho, rt);
+      hq(rho + 3, rb);
+#pragma unroll
+      for (int vv = 0; vv < 2; ++vv) {
+        double gv[2], mid2[2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          gv[d] = VS[vv][0] * gi[0][d] + VS[vv][1] * gi[1][d];
+          mid2[d] = G.dzmid[d] + ZQP[vv] * G.djz[d];
+        }
+#pragma unroll
+        for (int qq = 0; qq < 6; ++qq) {
+          const double dzr = 0.5 * (rt[qq] - rb[qq]);
+          const double wj = QW[qq] * j2d;
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const double t = g * (wj * jzq[qq] * gv[d] - wj * mid2[d] * dzr);
+#pragma unroll
+            for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+              for (int a = 0; a < 3; ++a) acc[d][3 * lev + a] -= VS[vv][lev] * BARY[qq][a] * t;
+          }
+        }
+      }
+    }
+    // interior horizontal face above this layer: 2g J2D (-grad z_face) . int phi [[rho]]
+    if (l > 0) {
+      double dr[3], fi[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) dr[a] = 0.5 * (rho[a] - prevb[a]);
+      const double sdr = (dr[0] + dr[1]) + dr[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) fi[a] = (dr[a] + sdr) / 24.0;
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) acc[d][a] += 2.0 * g * j2d * (-G.dztop[d]) * fi[a];
+    }
+    // interior lateral faces: g n [[rho]] {Jz} Jedge
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (C.tag[k] != 0) continue;
+      double n4[4], ti[2][2], te[2][2];
+      ld_nb4(rhoT, E[k].k2, E[k].e2, l, L, nt, n4);
+      if (FROM_T) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) n4[n] = -alpha * (n4[n] - tref);
+      }
+      tr_own(rho, k, ti);
+      tr_nb(n4, te);
+      double j0, j1, a2[2], b2[2], ja[2][2], jb[2][2];
+      nb_jz(E[k], ft, fb, j0, j1);
+      tr2_own(G.jz, k, a2);
+      tr2_nb(j0, j1, b2);
+      tr_dup(a2, ja);
+      tr_dup(b2, jb);
+      double xx[2][2], xy[2][2];
+#pragma unroll
+      for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double drh = 0.5 * (ti[vv][h] - te[vv][h]);
+          const double jm = 0.5 * (ja[vv][h] + jb[vv][h]);
+          xx[vv][h] = C.nx[k] * drh * jm;
+          xy[vv][h] = C.ny[k] * drh * jm;
+        }
+      const double je = 0.5 * C.el[k];
+      lat_add(acc[0], k, xx, g * je);
+      lat_add(acc[1], k, xy, g * je);
+    }
+    // surface fold: -Mh (g rho_s grad_h eta)
+    if (l == 0) {
+      double mr[3];
+      mh_apply3(rho, j2d, mr);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc[0][a] -= g * mr[a] * ex;
+        acc[1][a] -= g * mr[a] * ey;
+      }
+    }
+    // top-down sweep (columns.py:108-121)
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double gt[3], gb[3], out[6];
+      mh_inv3(acc[d], j2d, gt);
+      mh_inv3(acc[d] + 3, j2d, gb);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        s[d][a] = s[d][a] + (gt[a] + gb[a]);
+        out[a] = -s[d][a] + 2.0 * gb[a];
+        out[3 + a] = -s[d][a];
+      }
+      st6(r + d * P6, l, c, L, nt, out);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) prevb[a] = rho[3 + a];
+  }
+}
+
+// ============================================================================ w from continuity (API)
+// internal3d.py:434-502 + columns.py:125-151 (bed-anchored sweep, bottom-up)
+__global__ void __launch_bounds__(128) k_compute_w(DMesh m, const double* __restrict__ eta_g,
+                                                   const double* __restrict__ q, const double* __restrict__ ux,
+                                                   const double* __restrict__ uy, const double* __restrict__ fac,
+                                                   Cols cs, double* __restrict__ w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3];
+  load_eta(eta_g, c, nt, eta);
+  const double j2d = C.j2d;
+  double s[3] = {0, 0, 0};
+  double ut_below[6][2];  // top-face q/Jz of layer l+1 at the 6 horizontal points
+  for (int l = L - 1; l >= 0; --l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    LGeo G;
+    layer_geo(C, eta, ft, fb, G);
+    double jzq[6];
+    hq(G.jz, jzq);
+    double qv[2][6];
+    ld6(q, l, c, L, nt, qv[0]);
+    ld6(q + P6, l, c, L, nt, qv[1]);
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    double qp[2][2][6];
+    at_pts(qv[0], qp[0]);
+    at_pts(qv[1], qp[1]);
+    // volume: + <q . grad_h(phi) J2D> (iso part) + metric part J2D dphi_z/dzeta (q . m_h)
+    {
+      double S[2][2];
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+          for (int qq = 0; qq < 6; ++qq) {
+            sx += QW[qq] * VS[vv][mm] * qp[0][vv][qq];
+            sy += QW[qq] * VS[vv][mm] * qp[1][vv][qq];
+          }
+        S[mm][0] = sx;
+        S[mm][1] = sy;
+      }
+      iso_add(C, S, acc);
+      double met[3] = {0, 0, 0};
+#pragma unroll
+      for (int vv = 0; vv < 2; ++vv) {
+        const double m0 = G.dzmid[0] + ZQP[vv] * G.djz[0];
+        const double m1 = G.dzmid[1] + ZQP[vv] * G.djz[1];
+#pragma unroll
+        for (int qq = 0; qq < 6; ++qq) {
+          const double qm = qp[0][vv][qq] * (-m0 / jzq[qq]) + qp[1][vv][qq] * (-m1 / jzq[qq]);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) met[a] += QW[qq] * qm * BARY[qq][a];
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc[a] += j2d * DV[0] * met[a];
+        acc[3 + a] += j2d * DV[1] * met[a];
+      }
+    }
+    // horizontal faces: {q/Jz} . grad(z_face) with one-sided values at surface and bed
+    {
+      double ut[6][2], ub[6][2];
+      double t0[6], t1[6], b0[6], b1[6];
+      hq(qv[0], t0);
+      hq(qv[1], t1);
+      hq(qv[0] + 3, b0);
+      hq(qv[1] + 3, b1);
+#pragma unroll
+      for (int qq = 0; qq < 6; ++qq) {
+        ut[qq][0] = t0[qq] / jzq[qq];
+        ut[qq][1] = t1[qq] / jzq[qq];
+        ub[qq][0] = b0[qq] / jzq[qq];
+        ub[qq][1] = b1[qq] / jzq[qq];
+      }
+      double ubA[6][2];  // bottom-face q/Jz of the layer above (l-1)
+      if (l > 0) {
+        double jza[3], jzqa[6], qa0[6], qa1[6];
+        layer_jz(C.b, eta, m.fracs[l - 1], ft, jza);
+        hq(jza, jzqa);
+        double v0[6], v1[6];
+        ld6(q, l - 1, c, L, nt, v0);
+        ld6(q + P6, l - 1, c, L, nt, v1);
+        hq(v0 + 3, qa0);
+        hq(v1 + 3, qa1);
+#pragma unroll
+        for (int qq = 0; qq < 6; ++qq) {
+          ubA[qq][0] = qa0[qq] / jzqa[qq];
+          ubA[qq][1] = qa1[qq] / jzqa[qq];
+        }
+      }
+      double ftq[6], fbq[6];
+#pragma unroll
+      for (int qq = 0; qq < 6; ++qq) {
+        double mt0 = ut[qq][0], mt1 = ut[qq][1], mb0 = ub[qq][0], mb1 = ub[qq][1];
+        if (l > 0) {
+          mt0 = 0.5 * (ut[qq][0] + ubA[qq][0]);
+          mt1 = 0.5 * (ut[qq][1] + ubA[qq][1]);
+        }
+        if (l < L - 1) {
+          mb0 = 0.5 * (ub[qq][0] + ut_below[qq][0]);
+          mb1 = 0.5 * (ub[qq][1] + ut_below[qq][1]);
+        }
+        ftq[qq] = mt0 * G.dztop[0] + mt1 * G.dztop[1];
+        fbq[qq] = mb0 * G.dzbot[0] + mb1 * G.dzbot[1];
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double tt = 0.0, tb = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < 6; ++qq) {
+          tt += QW[qq] * ftq[qq] * BARY[qq][a];
+          tb += QW[qq] * fbq[qq] * BARY[qq][a];
+        }
+        acc[a] += j2d * tt;
+        acc[3 + a] -= j2d * tb;
+      }
+#pragma unroll
+      for (int qq = 0; qq < 6; ++qq) {
+        ut_below[qq][0] = ut[qq][0];
+        ut_below[qq][1] = ut[qq][1];
+      }
+    }
+    // lateral stabilised flux
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (C.tag[k] != 0) continue;
+      double f[2][2];
+      ld_fac(fac, k, l, c, L, nt, f);
+      lat_add(acc, k, f, -(0.5 * C.el[k]));
+    }
+    // bed kinematic fold w(bed) = u . grad_h(b)
+    if (l == L - 1) {
+      const double bx = (C.b[0] * C.dx[0] + C.b[1] * C.dx[1]) + C.b[2] * C.dx[2];
+      const double by = (C.b[0] * C.dy[0] + C.b[1] * C.dy[1]) + C.b[2] * C.dy[2];
+      double wb[3], mw[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        wb[a] = ux[((size_t)(3 + a) * L + l) * nt + c] * bx + uy[((size_t)(3 + a) * L + l) * nt + c] * by;
+      mh_apply3(wb, j2d, mw);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) acc[3 + a] += mw[a];
+    }
+    double gt[3], gb[3], out[6];
+    mh_inv3(acc, j2d, gt);
+    mh_inv3(acc + 3, j2d, gb);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      out[3 + a] = s[a] + gb[a] - gt[a];
+      out[a] = s[a] + gb[a] + gt[a];
+      s[a] = out[a];
+    }
+    st6(w, l, c, L, nt, out);
+  }
+}
+
+// ============================================================================ w~ (API + fused)
+// internal3d.py:505-541.  FUSED: qbar = q + Jz mis and its factor rebuilt on the fly.
+template <bool FUSED>
+__global__ void __launch_bounds__(128) k_compute_wtilde(DMesh m, const double* __restrict__ eta_g,
+                                                        const double* __restrict__ qb, const double* __restrict__ fac,
+                                                        const double* __restrict__ mis, double g, Cols cs,
+                                                        double* __restrict__ w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3];
+  load_eta(eta_g, c, nt, eta);
+  EdgeNb E[3];
+  double mo[2][3], mn[3][2][2];  // own mismatch, neighbour mismatch at its edge corners
+  if (FUSED) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      edge_setup(m, C, eta, eta_g, k, g, E[k]);
+      mo[0][k] = mis[k * nt + c];
+      mo[1][k] = mis[(3 + k) * nt + c];
+      if (C.tag[k] == 0) {
+        const int e2 = E[k].e2, k2 = E[k].k2;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          mn[k][cc][0] = mis[(cc * 3 + EV0(k2)) * nt + e2];
+          mn[k][cc][1] = mis[(cc * 3 + EV1(k2)) * nt + e2];
+        }
+      }
+    }
+  }
+  const double j2d = C.j2d;
+  double s[3] = {0, 0, 0};
+  for (int l = L - 1; l >= 0; --l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    double qv[2][6], jz[3];
+    ld6(qb, l, c, L, nt, qv[0]);
+    ld6(qb + P6, l, c, L, nt, qv[1]);
+    if (FUSED) {
+      layer_jz(C.b, eta, ft, fb, jz);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jz[n % 3] * mo[cc][n % 3];
+    }
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    {
+      double qp[2][2][6];
+      at_pts(qv[0], qp[0]);
+      at_pts(qv[1], qp[1]);
+      double S[2][2];
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+          for (int qq = 0; qq < 6; ++qq) {
+            sx += QW[qq] * VS[vv][mm] * qp[0][vv][qq];
+            sy += QW[qq] * VS[vv][mm] * qp[1][vv][qq];
+          }
+        S[mm][0] = sx;
+        S[mm][1] = sy;
+      }
+      iso_add(C, S, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (C.tag[k] != 0) continue;
+      double f[2][2];
+      if (FUSED) {
+        double qn[2][4], jn0, jn1;
+        ld_nb4(qb, E[k].k2, E[k].e2, l, L, nt, qn[0]);
+        ld_nb4(qb + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
+        nb_jz(E[k], ft, fb, jn0, jn1);
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          qn[cc][0] = qn[cc][0] + jn0 * mn[k][cc][0];
+          qn[cc][1] = qn[cc][1] + jn1 * mn[k][cc][1];
+          qn[cc][2] = qn[cc][2] + jn0 * mn[k][cc][0];
+          qn[cc][3] = qn[cc][3] + jn1 * mn[k][cc][1];
+        }
+        lat_factor(C, E[k], k, jz, eta, ft, fb, qv, qn, f);
+      } else {
+        ld_fac(fac, k, l, c, L, nt, f);
+      }
+      lat_add(acc, k, f, -(0.5 * C.el[k]));
+    }
+    double gt[3], gb[3], out[6];
+    mh_inv3(acc, j2d, gt);
+    mh_inv3(acc + 3, j2d, gb);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      out[3 + a] = s[a] + gb[a] - gt[a];
+      out[a] = s[a] + gb[a] + gt[a];
+      s[a] = out[a];
+    }
+    st6(w, l, c, L, nt, out);
+  }
+}
+
+// ============================================================================ horizontal RHS
+// internal3d.py:695-751 (momentum, NC=2) and :754-792 (tracer, NC=1), kappa = nu = 0.
+// MODE 0 (API):   explicit q_adv / factor / mass arrays; out = F (P6N); Coriolis and -M r/rho0
+//                 only if mass_terms (the host adds them over ALL rows when els is given, as the
+//                 reference does).
+// MODE 1 (PRED):  q from array, factor from q on the fly, Mu from geometry, + stresses;
+//                 out = vertical-DOF column sum of (F + stress) (the F3D->2D forcing).
+// MODE 2 (STAGE): qbar = q + Jz mis on the fly, factor from qbar, Mu/M0/M1 from geometry;
+//                 out = M0 u0 + dt (F + stress + M1 F2D/H1)  (momentum)  or  M0 T0 + dt F (tracer).
+struct HArgs {
+  const double* eta_u;   // grid of the stage values (C3)
+  const double* u;       // advected field (NC planes of P6)
+  const double* qa;      // q_adv (API, PRED) or q (STAGE), 2 x P6
+  const double* fac;     // FAC (API)
+  const double* r;       // 2 x P6 (momentum)
+  const double* mass;    // MASS (API)
+  const double* mis;     // [2][3][nt] (STAGE)
+  const double* eta0;    // STAGE: step-start grid
+  const double* eta1;    // STAGE: end-of-stage grid
+  const double* u0;      // STAGE: step-start field (NC x P6)
+  const double* f2d;     // STAGE momentum: [2][3][nt]
+  double g, f, rho0, tsx, tsy, cd, dt;
+  int mass_terms;
+};
+
+template <int NC, int MODE>
+__global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3];
+  load_eta(a.eta_u, c, nt, eta);
+  EdgeNb E[3];
+  double mo[2][3], mn[3][2][2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (MODE != 0) edge_setup(m, C, eta, a.eta_u, k, a.g, E[k]);
+    else {
+      E[k].e2 = C.nb[k];
+      E[k].k2 = C.nk[k];
+    }
+    if (MODE == 2) {
+      mo[0][k] = a.mis[k * nt + c];
+      mo[1][k] = a.mis[(3 + k) * nt + c];
+      if (C.tag[k] == 0) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          mn[k][cc][0] = a.mis[(cc * 3 + EV0(E[k].k2)) * nt + E[k].e2];
+          mn[k][cc][1] = a.mis[(cc * 3 + EV1(E[k].k2)) * nt + E[k].e2];
+        }
+      }
+    }
+  }
+  double eta0[3], eta1[3], F1[2][3];
+  if (MODE == 2) {
+    load_eta(a.eta0, c, nt, eta0);
+    load_eta(a.eta1, c, nt, eta1);
+    if constexpr (NC == 2) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double H1 = eta1[k] - C.b[k];
+        F1[0][k] = a.f2d[k * nt + c] / H1;
+        F1[1][k] = a.f2d[(3 + k) * nt + c] / H1;
+      }
+    }
+  }
+  const double j2d = C.j2d;
+  double csum[NC][3];
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
+  for (int l = 0; l < L; ++l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    double jz[3];
+    layer_jz(C.b, eta, ft, fb, jz);
+    double u[NC][6], qv[2][6];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) ld6(a.u + cc * P6, l, c, L, nt, u[cc]);
+    ld6(a.qa, l, c, L, nt, qv[0]);
+    ld6(a.qa + P6, l, c, L, nt, qv[1]);
+    if (MODE == 2) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jz[n % 3] * mo[cc][n % 3];
+    }
+    double acc[NC][6];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int n = 0; n < 6; ++n) acc[cc][n] = 0.0;
+    // volume advection: J2D grad_h(phi_h) . sum_vq W phi_z u (q . )
+    {
+      double qp[2][2][6];
+      at_pts(qv[0], qp[0]);
+      at_pts(qv[1], qp[1]);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double up[2][6], S[2][2];
+        at_pts(u[cc], up);
+        adv_moment(up, qp[0], qp[1], S);
+        iso_add(C, S, acc[cc]);
+      }
+    }
+    // lateral upwind flux on interior faces
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (C.tag[k] != 0) continue;
+      double f[2][2];
+      if (MODE == 0) {
+        ld_fac(a.fac, k, l, c, L, nt, f);
+      } else {
+        double qn[2][4];
+        ld_nb4(a.qa, E[k].k2, E[k].e2, l, L, nt, qn[0]);
+        ld_nb4(a.qa + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
+        if (MODE == 2) {
+          double jn0, jn1;
+          nb_jz(E[k], ft, fb, jn0, jn1);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            qn[cc][0] = qn[cc][0] + jn0 * mn[k][cc][0];
+            qn[cc][1] = qn[cc][1] + jn1 * mn[k][cc][1];
+            qn[cc][2] = qn[cc][2] + jn0 * mn[k][cc][0];
+            qn[cc][3] = qn[cc][3] + jn1 * mn[k][cc][1];
+          }
+        }
+        lat_factor(C, E[k], k, jz, eta, ft, fb, qv, qn, f);
+      }
+      const double je = -(0.5 * C.el[k]);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double n4[4], ti[2][2], te[2][2], x[2][2];
+        ld_nb4(a.u + cc * P6, E[k].k2, E[k].e2, l, L, nt, n4);
+        tr_own(u[cc], k, ti);
+        tr_nb(n4, te);
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) x[vv][h] = (f[vv][h] >= 0.0 ? ti[vv][h] : te[vv][h]) * f[vv][h];
+        lat_add(acc[cc], k, x, je);
+      }
+    }
+    // Coriolis f M (u_y, -u_x) and -M r / rho0   (momentum)
+    if constexpr (NC == 2) if (MODE != 0 || a.mass_terms) {
+      double mu[2][6], mr[2][6];
+      double rr[2][6];
+      ld6(a.r, l, c, L, nt, rr[0]);
+      ld6(a.r + P6, l, c, L, nt, rr[1]);
+      if (MODE == 0) {
+        double M[6][6];
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+#pragma unroll
+          for (int s = 0; s < 6; ++s) M[p][s] = a.mass[((size_t)(p * 6 + s) * L + l) * nt + c];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int p = 0; p < 6; ++p) {
+            double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+            for (int s = 0; s < 6; ++s) {
+              t0 += M[p][s] * u[cc][s];
+              t1 += M[p][s] * rr[cc][s];
+            }
+            mu[cc][p] = t0;
+            mr[cc][p] = t1;
+          }
+      } else {
+        double jzq[6], Mh[3][3];
+        hq(jz, jzq);
+        mass_h(jzq, Mh);
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          mass_apply_k(Mh, j2d, u[cc], mu[cc]);
+          mass_apply_k(Mh, j2d, rr[cc], mr[cc]);
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < 6; ++n) {
+        if (a.f != 0.0) {
+          acc[0][n] += a.f * mu[1][n];
+          acc[1][n] -= a.f * mu[0][n];
+        }
+        acc[0][n] -= mr[0][n] / a.rho0;
+        acc[1][n] -= mr[1][n] / a.rho0;
+      }
+    }
+    // surface wind and bottom drag (internal3d.py:919-934)
+    if constexpr (NC == 2 && MODE != 0) {
+      if (l == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          acc[0][k] += j2d / 6.0 * a.tsx;
+          acc[1][k] += j2d / 6.0 * a.tsy;
+        }
+      }
+      if (l == L - 1 && a.cd != 0.0) {
+        double dx3[3], dy3[3], mx[3], my[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double ubx = u[0][3 + k], uby = u[NC - 1][3 + k];
+          const double sp = sqrt(ubx * ubx + uby * uby);
+          dx3[k] = -a.cd * sp * ubx;
+          dy3[k] = -a.cd * sp * uby;
+        }
+        mh_apply3(dx3, j2d, mx);
+        mh_apply3(dy3, j2d, my);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          acc[0][3 + k] += mx[k];
+          acc[NC - 1][3 + k] += my[k];
+        }
+      }
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
+    } else if (MODE == 2) {
+      double j0[3], j1[3], q0[6], q1[6], M0h[3][3], M1h[3][3];
+      layer_jz(C.b, eta0, ft, fb, j0);
+      layer_jz(C.b, eta1, ft, fb, j1);
+      hq(j0, q0);
+      hq(j1, q1);
+      mass_h(q0, M0h);
+      mass_h(q1, M1h);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double x0[6], m0x[6], o[6];
+        ld6(a.u0 + cc * P6, l, c, L, nt, x0);
+        mass_apply_k(M0h, j2d, x0, m0x);
+        if constexpr (NC == 2) {
+          double F6[6], m1f[6];
+#pragma unroll
+          for (int n = 0; n < 6; ++n) F6[n] = F1[cc][n % 3];
+          mass_apply_k(M1h, j2d, F6, m1f);
+#pragma unroll
+          for (int n = 0; n < 6; ++n) o[n] = m0x[n] + a.dt * (acc[cc][n] + m1f[n]);
+        } else {
+#pragma unroll
+          for (int n = 0; n < 6; ++n) o[n] = m0x[n] + a.dt * acc[cc][n];
+        }
+        st6(out + cc * P6, l, c, L, nt, o);
+      }
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) st6(out + cc * P6, l, c, L, nt, acc[cc]);
+    }
+  }
+  if (MODE == 1) {
+    // (Fh + st) column sum -> [NC][3][nt]
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) out[(cc * 3 + k) * nt + c] = csum[cc][k];
+  }
+}
+
+// Coriolis and -M r / rho0 over all prisms (the reference applies them to every row even
+// when `els` restricts the advective part, internal3d.py:745-750)
+__global__ void k_mass_terms(int L, int nt, const double* __restrict__ mass, const double* __restrict__ u,
+                             const double* __restrict__ r, double f, double rho0, double* __restrict__ out) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long P = (long long)L * nt;
+  if (p >= P) return;
+  double M[6][6], uu[2][6], rr[2][6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) M[i][j] = mass[(i * 6 + j) * P + p];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      uu[cc][i] = u[(cc * 6 + i) * P + p];
+      rr[cc][i] = r[(cc * 6 + i) * P + p];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double mu0 = 0, mu1 = 0, mr0 = 0, mr1 = 0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      mu0 += M[i][j] * uu[0][j];
+      mu1 += M[i][j] * uu[1][j];
+      mr0 += M[i][j] * rr[0][j];
+      mr1 += M[i][j] * rr[1][j];
+    }
+    double o0 = out[i * P + p], o1 = out[(6 + i) * P + p];
+    if (f != 0.0) {
+      o0 += f * mu1;
+      o1 -= f * mu0;
+    }
+    out[i * P + p] = o0 - mr0 / rho0;
+    out[(6 + i) * P + p] = o1 - mr1 / rho0;
+  }
+}
+
+// stress_rhs (internal3d.py:919-934), API flavour
+__global__ void k_stress(DMesh m, const double* __restrict__ ux, const double* __restrict__ uy, double tsx,
+                         double tsy, double cd, Cols cs, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cs.n) return;
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  const double j2d = ldg(m.j2d + c);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    out[((size_t)k * L + 0) * nt + c] += j2d / 6.0 * tsx;
+    out[P6 + ((size_t)k * L + 0) * nt + c] += j2d / 6.0 * tsy;
+  }
+  if (cd != 0.0) {
+    double dx3[3], dy3[3], mx[3], my[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double bx = ux[((size_t)(3 + k) * L + L - 1) * nt + c], by = uy[((size_t)(3 + k) * L + L - 1) * nt + c];
+      const double sp = sqrt(bx * bx + by * by);
+      dx3[k] = -cd * sp * bx;
+      dy3[k] = -cd * sp * by;
+    }
+    mh_apply3(dx3, j2d, mx);
+    mh_apply3(dy3, j2d, my);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      out[((size_t)(3 + k) * L + L - 1) * nt + c] += mx[k];
+      out[P6 + ((size_t)(3 + k) * L + L - 1) * nt + c] += my[k];
+    }
+  }
+}
+
+}  // namespace pdg
+
+// ============================================================================ C ABI
+using namespace pdg;
+
+#define COLS(els, n) Cols{els, (els) ? (n) : ctx->nt}
+#define GRID1(nn) nblocks((nn), 128), 128, 0, (cudaStream_t)stream
+
+extern "C" {
+
+int pdg_prism_mass(pdg_ctx* ctx, const double* eta_g, const int* els, int n_els, double* out, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  k_prism_mass<<<GRID1(cs.n)>>>(ctx->view(), eta_g, cs, out);
+  return check_launch(ctx);
+}
+
+int pdg_project_transport(pdg_ctx* ctx, const double* eta_g, const double* ux, const double* uy,
+                          const double* mass, const int* els, int n_els, double* q, double* qsum, double* htot,
+                          void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  if (mass)
+    k_project<true><<<GRID1(cs.n)>>>(ctx->view(), eta_g, ux, uy, mass, cs, q, qsum, htot);
+  else
+    k_project<false><<<GRID1(cs.n)>>>(ctx->view(), eta_g, ux, uy, nullptr, cs, q, qsum, htot);
+  return check_launch(ctx);
+}
+
+int pdg_column_sum(int nt, int L, int ncomp, const double* f, double* out, void* stream) {
+  k_colsum<<<GRID1(nt)>>>(nt, L, ncomp, f, out);
+  return check_launch_noctx();
+}
+
+int pdg_total_thickness(pdg_ctx* ctx, const double* eta_g, double* htot, void* stream) {
+  k_htot<<<GRID1(ctx->nt)>>>(ctx->view(), eta_g, htot);
+  return check_launch(ctx);
+}
+
+int pdg_mismatch(pdg_ctx* ctx, const double* qbar, const double* qsum, const double* htot, double* mis,
+                 void* stream) {
+  k_mismatch<<<GRID1(ctx->nt)>>>(ctx->nt, qbar, qsum, htot, mis);
+  return check_launch(ctx);
+}
+
+int pdg_consistent_transport(pdg_ctx* ctx, const double* eta_g, const double* q, const double* mis,
+                             const int* els, int n_els, double* out, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  k_consistent<<<GRID1(cs.n)>>>(ctx->view(), eta_g, q, mis, cs, out);
+  return check_launch(ctx);
+}
+
+int pdg_lateral_flux_factor(pdg_ctx* ctx, const double* eta_g, const double* q, double g, const int* els,
+                            int n_els, double* fac, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  k_factor<<<GRID1(cs.n)>>>(ctx->view(), eta_g, q, g, cs, fac);
+  return check_launch(ctx);
+}
+
+int pdg_compute_r(pdg_ctx* ctx, const double* eta_g, const double* rho_or_T, int from_T, double alpha, double tref,
+                  double g, const int* els, int n_els, double* r, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  if (from_T)
+    k_compute_r<true><<<GRID1(cs.n)>>>(ctx->view(), eta_g, rho_or_T, alpha, tref, g, cs, r);
+  else
+    k_compute_r<false><<<GRID1(cs.n)>>>(ctx->view(), eta_g, rho_or_T, alpha, tref, g, cs, r);
+  return check_launch(ctx);
+}
+
+int pdg_compute_w(pdg_ctx* ctx, const double* eta_g, const double* q, const double* ux, const double* uy,
+                  const double* fac, const int* els, int n_els, double* w, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  k_compute_w<<<GRID1(cs.n)>>>(ctx->view(), eta_g, q, ux, uy, fac, cs, w);
+  return check_launch(ctx);
+}
+
+int pdg_compute_wtilde(pdg_ctx* ctx, const double* eta_g, const double* qb, const double* fac, const double* mis,
+                       double g, const int* els, int n_els, double* w, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  if (mis)
+    k_compute_wtilde<true><<<GRID1(cs.n)>>>(ctx->view(), eta_g, qb, nullptr, mis, g, cs, w);
+  else
+    k_compute_wtilde<false><<<GRID1(cs.n)>>>(ctx->view(), eta_g, qb, fac, nullptr, g, cs, w);
+  return check_launch(ctx);
+}
+
+// horizontal_rhs / tracer_horizontal_rhs, API flavour (internal3d.py:695-792)
+int pdg_horizontal_rhs(pdg_ctx* ctx, const double* eta_g, const double* u, int ncomp, const double* q_adv,
+                       const double* fac, const double* r, const double* mass, double f, double rho0, int mass_terms,
+                       const int* els, int n_els, double* out, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  HArgs a{};
+  a.eta_u = eta_g;
+  a.u = u;
+  a.qa = q_adv;
+  a.fac = fac;
+  a.r = r;
+  a.mass = mass;
+  a.f = f;
+  a.rho0 = rho0;
+  a.mass_terms = mass_terms;
+  if (ncomp == 2)
+    k_hrhs<2, 0><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+  else
+    k_hrhs<1, 0><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+  return check_launch(ctx);
+}
+
+int pdg_mass_terms(int L, int nt, const double* mass, const double* u, const double* r, double f, double rho0,
+                   double* out, void* stream) {
+  const long long P = (long long)L * nt;
+  k_mass_terms<<<nblocks(P, 128), 128, 0, (cudaStream_t)stream>>>(L, nt, mass, u, r, f, rho0, out);
+  return check_launch_noctx();
+}
+
+int pdg_stress_rhs(pdg_ctx* ctx, const double* ux, const double* uy, double tsx, double tsy, double cd,
+                   const int* els, int n_els, double* out, void* stream) {
+  Cols cs = COLS(els, n_els);
+  if (cs.n == 0) return PDG_OK;
+  k_stress<<<GRID1(cs.n)>>>(ctx->view(), ux, uy, tsx, tsy, cd, cs, out);
+  return check_launch(ctx);
+}
+
+// fused stepper entries ----------------------------------------------------------------
+// F3D->2D forcing: column sum of horizontal_rhs(u, q, fac(q)) + stresses  -> [2][3][nt]
+int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r, double g,
+                   double f, double rho0, double tsx, double tsy, double cd, double* f3d2d, void* stream) {
+  HArgs a{};
+  a.eta_u = eta_u;
+  a.u = u;
+  a.qa = q;
+  a.r = r;
+  a.g = g;
+  a.f = f;
+  a.rho0 = rho0;
+  a.tsx = tsx;
+  a.tsy = tsy;
+  a.cd = cd;
+  Cols cs{nullptr, ctx->nt};
+  k_hrhs<2, 1><<<GRID1(cs.n)>>>(ctx->view(), a, cs, f3d2d);
+  return check_launch(ctx);
+}
+
+// stage right-hand sides: momentum  M0 u0 + dt (F(u, qbar) + stress + M1 F2D/H1),
+// tracer M0 T0 + dt F(T, qbar)
+int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta0, const double* eta1,
+                 const double* u, const double* u0, const double* q, const double* mis, const double* r,
+                 const double* f2d, double g, double f, double rho0, double tsx, double tsy, double cd, double dt,
+                 double* out, void* stream) {
+  HArgs a{};
+  a.eta_u = eta_u;
+  a.eta0 = eta0;
+  a.eta1 = eta1;
+  a.u = u;
+  a.u0 = u0;
+  a.qa = q;
+  a.mis = mis;
+  a.r = r;
+  a.f2d = f2d;
+  a.g = g;
+  a.f = f;
+  a.rho0 = rho0;
+  a.tsx = tsx;
+  a.tsy = tsy;
+  a.cd = cd;
+  a.dt = dt;
+  Cols cs{nullptr, ctx->nt};
+  if (ncomp == 2)
+    k_hrhs<2, 2><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+  else
+    k_hrhs<1, 2><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+  return check_launch(ctx);
+}
+
+}  // extern "C"

@@ -22,10 +22,6 @@ from .params import ExternalResult, PhysParams, State2D
 __all__ = ["PhysParams", "State2D", "ExternalResult", "eos_density", "rhs_free_surface", "rhs_depth_momentum",
            "external_tendencies", "check_cfl", "subcycle_external", "integrate_nodal", "diagnostics_2d"]
 
-_lib.declare("pdg_eos", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_double,
-                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p,
-                                       ctypes.c_void_p])
-
 
 def eos_density(T, params: PhysParams, S=None):
     """rho' = -alpha (T - t_ref) + beta (S - s_ref)  (external2d.py:81-87), on device."""

@@ -1,0 +1,190 @@
+"""Fused 2-stage IMEX internal step (the hot path), every field resident in HBM.
+
+The reference ships no stepper.  The composition is the
+one defined in DESIGN.md section 3 and restated by the oracle
+(oracle/stepper.py): stage 1 over dt/2 with m/2 external substeps and an
+implicit vertical solve, stage 2 over dt with m substeps, explicit, from the
+stage-1 midpoint.  Per stage the device work is
+
+  1  compute_r with the EOS inline                    (k_compute_r<FROM_T>)
+  2  q = project(u) + column sum of q + total depth   (k_project<Kronecker>)
+  3  F3D->2D = column sum of (F_h(u, q, fac(q)) + stresses)     (k_hrhs<2, PRED>)
+  4  m_s SSP-RK3 substeps, one fused kernel per RK stage, + Qbar, F2D
+  5  mismatch (Qbar - sum q) / H                      (k_mismatch)
+  6  w~ with qbar = q + Jz mis and its factor on the fly         (k_compute_wtilde<FUSED>)
+  7  rhs_u = M0 u0 + dt (F_h(u, qbar) + stress + M1 F2D/H1)      (k_hrhs<2, STAGE>)
+     rhs_T = M0 T0 + dt F_T(T, qbar)                             (k_hrhs<1, STAGE>)
+  8  vertical: (M1 - dt A) x = rhs (block Thomas) or x = M1^-1 (rhs + dt A x)
+     with A assembled per layer in registers          (k_vstep<NC, IMPLICIT>)
+
+The flux factors, qbar, prism masses, mesh velocity and the banded matrices
+are never materialised.  The whole step is one CUDA graph.
+"""
+from __future__ import annotations
+
+from types import SimpleNamespace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import c3_in, c3_out, device_mesh, p6_in, p6_out, ptr, stream_ptr
+from .params import PenaltyParams, PhysParams
+
+F64 = torch.float64
+
+
+class ImexStepper:
+    """Device-resident internal+external stepper for one mesh / layer count."""
+
+    def __init__(self, mesh, L: int, params: PhysParams, dt: float, m: int, kv: float, nu_v: float,
+                 pen: PenaltyParams = PenaltyParams(), device=None):
+        if m % 2:
+            raise ValueError("m must be even (stage 1 uses m/2 substeps)")
+        for name in ("kappa_h", "kappa_v", "nu_h", "nu_v"):
+            if getattr(params, name) != 0.0 and name in ("kappa_v", "nu_v"):
+                raise NotImplementedError(f"params.{name} != 0: explicit split diffusion is not parity-pinned "
+                                          "(reference crash, internal3d.py:665)")
+        if params.kappa_h != 0.0 or params.nu_h != 0.0:
+            raise NotImplementedError("explicit horizontal diffusion is not parity-pinned (internal3d.py:665)")
+        self.mesh, self.L, self.p = mesh, L, params
+        self.dt, self.m, self.kv, self.nu_v, self.pen = float(dt), int(m), float(kv), float(nu_v), pen
+        self.dm = device_mesh(mesh, L)
+        self.dev = self.dm.device
+        nt = self.nt = mesh.nt
+        z = lambda *s: torch.zeros(s, dtype=F64, device=self.dev)  # noqa: E731
+        self.S = z(3, 3, nt)                     # 2D state (eta, qx, qy); eta is also the grid free surface
+        self.Sw = [z(3, 3, nt), z(3, 3, nt)]     # per-stage external working states
+        self.U = [z(2, 6, L, nt) for _ in range(3)]   # rotating: state / stage-1 result / stage-2 result
+        self.T = [z(6, L, nt) for _ in range(3)]
+        self.r = z(2, 6, L, nt)
+        self.q = z(2, 6, L, nt)
+        self.wt = z(6, L, nt)
+        self.qsum, self.htot, self.f3d2d = z(2, 3, nt), z(3, nt), z(2, 3, nt)
+        self.qbar, self.f2d, self.mis = z(2, 3, nt), z(2, 3, nt), z(2, 3, nt)
+        self.cur = 0
+        self.t = 0.0
+        self.graphs = {}
+        self.use_graph = True
+
+    # ------------------------------------------------------------------ state I/O (reference layouts)
+    def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
+        nt, L, dev = self.nt, self.L, self.dev
+
+        def d(a):
+            return (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
+        self.S[0].copy_(c3_in(d(eta), dev))
+        self.S[1].copy_(c3_in(d(qx), dev))
+        self.S[2].copy_(c3_in(d(qy), dev))
+        self.U[self.cur][0].copy_(p6_in(d(ux), nt, L))
+        self.U[self.cur][1].copy_(p6_in(d(uy), nt, L))
+        self.T[self.cur].copy_(p6_in(d(T), nt, L))
+        self.t = float(t)
+
+    def get_state(self, numpy=True):
+        nt, L = self.nt, self.L
+        u = self.U[self.cur]
+        out = dict(eta=c3_out(self.S[0]), qx=c3_out(self.S[1]), qy=c3_out(self.S[2]), ux=p6_out(u[0], nt, L),
+                   uy=p6_out(u[1], nt, L), T=p6_out(self.T[self.cur], nt, L), t=self.t)
+        if numpy:
+            out = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in out.items()}
+        return out
+
+    # ------------------------------------------------------------------ one stage
+    def _stage(self, s, eta_u, u, T, u0, T0, Sw, out_u, out_T, dt_s, m_s, implicit, t_wind):
+        lb, h, p = _lib.lib(), self.dm.h, self.p
+        chk = _lib.check
+        eta0 = self.S[0]
+        tsx, tsy = p.wind(t_wind)
+        chk(lb.pdg_compute_r(h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s), "r")
+        chk(lb.pdg_project_transport(h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
+                                     ptr(self.qsum), ptr(self.htot), s), "project")
+        chk(lb.pdg_step_f3d2d(h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy, p.cd,
+                              ptr(self.f3d2d), s), "f3d2d")
+        Sw.copy_(self.S)
+        chk(lb.pdg_ext2d_subcycle(h, ptr(Sw), m_s, dt_s / m_s, p.g, p.rho0, ptr(self.f3d2d), None, None, None,
+                                  ptr(self.qbar), ptr(self.f2d), 1, s), "subcycle")
+        eta1 = Sw[0]
+        chk(lb.pdg_mismatch(h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s), "mismatch")
+        chk(lb.pdg_compute_wtilde(h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0, ptr(self.wt), s),
+            "wtilde")
+        chk(lb.pdg_step_rhs(h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q), ptr(self.mis),
+                            ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s), "rhs_u")
+        chk(lb.pdg_step_rhs(h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q), ptr(self.mis),
+                            None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s), "rhs_T")
+        pe = self.pen
+        chk(lb.pdg_step_vertical(h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt), p.kappa_h,
+                                 self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s), "vertical_u")
+        chk(lb.pdg_step_vertical(h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt), p.nu_h,
+                                 self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s), "vertical_T")
+        return eta1
+
+    def _launch_step(self, t0):
+        s = stream_ptr()
+        a, b, c = self.cur, (self.cur + 1) % 3, (self.cur + 2) % 3
+        U, T = self.U, self.T
+        eta_h = self._stage(s, self.S[0], U[a], T[a], U[a], T[a], self.Sw[0], U[b], T[b], 0.5 * self.dt,
+                            self.m // 2, True, t0)
+        self._stage(s, eta_h, U[b], T[b], U[a], T[a], self.Sw[1], U[c], T[c], self.dt, self.m, False,
+                    t0 + 0.5 * self.dt)
+        self.S.copy_(self.Sw[1])
+
+    def step(self, n: int = 1):
+        """Advance n internal steps (stream ordered, no host sync)."""
+        with torch.cuda.device(self.dev):
+            for _ in range(n):
+                wind_varies = self.p.tau_x1 is not None
+                if self.use_graph and not wind_varies:
+                    g = self.graphs.get(self.cur)
+                    if g is None:
+                        g = self._capture()
+                    g.replay()
+                else:
+                    self._launch_step(self.t)
+                self.cur = (self.cur + 2) % 3
+                self.t = self.t + self.dt
+
+    def _capture(self):
+        # warm the workspace (block-Thomas scratch is sized on first use), then capture
+        side = torch.cuda.Stream(device=self.dev)
+        side.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            saved = [x.clone() for x in (self.S,)]
+            self._launch_step(self.t)                          # sizes workspaces (result discarded)
+            self.S.copy_(saved[0])
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(g):
+            self._launch_step(self.t)
+        self.graphs[self.cur] = g
+        return g
+
+    def check(self):
+        """Synchronise and raise the first device-side error (DryColumn, ZeroPivot, CflViolation ...)."""
+        self.dm.raise_errors("imex step")
+
+    def launches_per_step(self) -> int:
+        """Kernel launches issued by one step (counted by the library)."""
+        with torch.cuda.device(self.dev):
+            saved = (self.S.clone(), self.cur, self.t)
+            n0 = self.dm.launches()
+            self._launch_step(self.t)
+            n1 = self.dm.launches()
+            self.S.copy_(saved[0])
+            torch.cuda.synchronize(self.dev)
+        return n1 - n0
+
+
+def imex_step(state, params: PhysParams, dt: float, m: int, kv: float, nu_v: float):
+    """Drop-in one-step driver with the oracle-stepper interface (state.grid/ux/uy/T/s2d)."""
+    from .mesh import update_moving_mesh
+    from .params import State2D
+    grid = state.grid
+    st = ImexStepper(grid.mesh, grid.n_layers, params, dt, m, kv, nu_v)
+    st.use_graph = False
+    st.set_state(state.s2d.eta, state.s2d.qx, state.s2d.qy, state.ux, state.uy, state.T, state.s2d.t)
+    st.step(1)
+    st.check()
+    o = st.get_state()
+    return SimpleNamespace(grid=update_moving_mesh(grid, o["eta"], dt), ux=o["ux"], uy=o["uy"], T=o["T"],
+                           s2d=State2D(o["eta"], o["qx"], o["qy"], o["t"]))
