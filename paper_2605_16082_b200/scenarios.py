@@ -1,0 +1,140 @@
+"""Synthetic workloads of BASELINE.json `configs`.
+
+C1  2D seiche, 32x32 basin (2,048 tri), dt2d = 2 s, 100 SSP-RK3 steps
+C2  same basin, 10 sigma layers, barotropic, dt = 40 s, m = 20
+C3  lock exchange, 250x100 (50,000 tri) x 20 layers, dt2d = 1 s, m = 20
+C4  synthetic coastal mesh 1000x500 (1,000,000 tri) x 50 layers, dt2d = 0.5 s, m = 20  <- bench workload
+All meshes are Hilbert-reordered `generate_basin_mesh` meshes (mesh.py:150-228).
+Random fields are seeded.  `make_case(name)` returns the mesh (host setup) and
+numpy initial state in reference layouts; `device_state_c4` builds the C4 3D
+fields directly on the GPU (600 M random numbers are not worth a host round trip).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .mesh import generate_basin_mesh, hilbert_reorder
+from .params import PhysParams
+
+
+@dataclass
+class Case:
+    name: str
+    mesh: object
+    L: int
+    params: PhysParams
+    dt: float
+    m: int
+    kv: float
+    nu_v: float
+    dt2d: float
+    state: dict = field(default_factory=dict)
+
+    @property
+    def prisms(self):
+        return self.mesh.nt * self.L
+
+
+def coastal_bed(lx, ly, seed=42, nbump=8):
+    rng = np.random.default_rng(seed)
+    cx, cy = rng.uniform(0, lx, nbump), rng.uniform(0, ly, nbump)
+    amp, rad = rng.uniform(-3.0, 25.0, nbump), rng.uniform(0.03, 0.1, nbump) * lx
+
+    def bed(x, y):
+        b = -(5.0 + 195.0 * x / lx)
+        for i in range(nbump):
+            b = b - amp[i] * np.exp(-((x - cx[i]) ** 2 + (y - cy[i]) ** 2) / rad[i] ** 2)
+        return np.minimum(b, -2.0)
+    return bed
+
+
+def make_case(name: str, scale: float = 1.0, with_state: bool = True, L: int | None = None) -> Case:
+    """Build a config; `scale` < 1 shrinks nx, ny (used for bounded CPU samples)."""
+    name = name.lower()
+    if name in ("c1", "c2"):
+        lx = ly = 1e4
+        mesh = hilbert_reorder(generate_basin_mesh(32, 32, lx, ly, lambda x, y: -20.0 + 0.0 * x))
+        p = PhysParams(f=1e-4 if name == "c2" else 0.0, cd=2.5e-3 if name == "c2" else 0.0)
+        c = Case(name, mesh, L or (10 if name == "c2" else 1), p, 40.0, 20, 1e-3, 1e-4, 2.0)
+        if with_state:
+            nt, P = mesh.nt, mesh.nt * c.L
+            z = np.zeros((nt, 3))
+            c.state = dict(eta=0.1 * np.cos(np.pi * mesh.x / lx), qx=z.copy(), qy=z.copy(), ux=np.zeros((P, 6)),
+                           uy=np.zeros((P, 6)), T=np.full((P, 6), 12.5))
+        return c
+    if name == "c3":
+        nx, ny = max(2, int(250 * scale)), max(2, int(100 * scale))
+        lx, ly = 25e3 * nx / 250, 10e3 * ny / 100
+        mesh = hilbert_reorder(generate_basin_mesh(nx, ny, lx, ly, lambda x, y: -20.0 + 0.0 * x))
+        p = PhysParams(f=1e-4, cd=2.5e-3, alpha=0.2, t_ref=12.5)
+        c = Case(name, mesh, L or 20, p, 20.0, 20, 1e-4, 1e-5, 1.0)
+        if with_state:
+            nt, P = mesh.nt, mesh.nt * c.L
+            xc = np.repeat(mesh.x, c.L, axis=0)
+            xnode = np.concatenate([xc, xc], axis=1)
+            z = np.zeros((nt, 3))
+            c.state = dict(eta=z.copy(), qx=z.copy(), qy=z.copy(), ux=np.zeros((P, 6)), uy=np.zeros((P, 6)),
+                           T=np.where(xnode < lx / 2, 15.0, 10.0))
+        return c
+    if name == "c4":
+        nx, ny = max(2, int(1000 * scale)), max(2, int(500 * scale))
+        lx, ly = 1e5 * nx / 1000, 5e4 * ny / 500
+        mesh = hilbert_reorder(generate_basin_mesh(nx, ny, lx, ly, coastal_bed(lx, ly)))
+        p = PhysParams(f=1e-4, cd=2.5e-3, alpha=0.2, t_ref=12.5, tau_x=0.1, tau_y=0.02)
+        c = Case(name, mesh, L or 50, p, 10.0, 20, 1e-4, 1e-5, 0.5)
+        if with_state:
+            c.state = c4_host_state(c)
+        return c
+    raise ValueError(name)
+
+
+def _c4_eta(mesh, lx):
+    return 0.05 * np.exp(-((mesh.x - 0.3 * lx) ** 2) / (0.05 * lx) ** 2)
+
+
+def c4_host_state(c: Case, seed=42):
+    """Host numpy C4 initial state (used for bounded CPU samples and small-scale parity)."""
+    mesh, L = c.mesh, c.L
+    nt, P = mesh.nt, mesh.nt * L
+    lx = float(mesh.vx.max())
+    eta = _c4_eta(mesh, lx)
+    H = eta - mesh.b
+    fr = np.linspace(0.0, 1.0, L + 1)
+    zt = (eta[:, None, :] - fr[None, :-1, None] * H[:, None, :]).reshape(P, 3)
+    zb = (eta[:, None, :] - fr[None, 1:, None] * H[:, None, :]).reshape(P, 3)
+    z = np.concatenate([zt, zb], axis=1)
+    xc = np.repeat(mesh.x, L, axis=0)
+    x6 = np.concatenate([xc, xc], axis=1)
+    T = 12.0 + 3.0 * np.tanh((x6 - 0.5 * lx) / (0.05 * lx)) + 0.02 * z
+    rng = np.random.default_rng(seed)
+    z2 = np.zeros((nt, 3))
+    return dict(eta=eta, qx=z2.copy(), qy=z2.copy(), ux=0.05 * rng.standard_normal((P, 6)),
+                uy=0.05 * rng.standard_normal((P, 6)), T=T)
+
+
+def device_state_c4(c: Case, stepper, seed=42):
+    """Fill a stepper with the C4 initial state generated on device, in device layouts."""
+    import torch
+    mesh, L, nt = c.mesh, c.L, c.mesh.nt
+    dev = stepper.dev
+    lx = float(mesh.vx.max())
+    eta = _c4_eta(mesh, lx)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    S = stepper.S
+    S.zero_()
+    S[0].copy_(torch.as_tensor(eta.T.copy(), device=dev))
+    u = stepper.U[stepper.cur]
+    u.normal_(0.0, 0.05, generator=g)
+    fr = torch.as_tensor(np.linspace(0.0, 1.0, L + 1), device=dev, dtype=torch.float64)
+    e = S[0]                                    # [3][nt]
+    b = torch.as_tensor(mesh.b.T.copy(), device=dev)
+    H = e - b
+    x = torch.as_tensor(mesh.x.T.copy(), device=dev)
+    T = stepper.T[stepper.cur]
+    for lev, f in ((0, fr[:-1]), (1, fr[1:])):
+        z = e[:, None, :] - f[None, :, None] * H[:, None, :]      # [3][L][nt]
+        T[3 * lev:3 * lev + 3] = 12.0 + 3.0 * torch.tanh((x[:, None, :] - 0.5 * lx) / (0.05 * lx)) + 0.02 * z
+    stepper.t = 0.0
