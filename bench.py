@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: prism-DOF updates/s of the full FP64 internal+external IMEX step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Workload (N=1): config 4 of BASELINE.json -- synthetic coastal basin, 1,000,000 Hilbert-ordered
+triangles x 50 sigma layers (50 M prisms, 3e8 prism DOF), dt2d = 0.5 s, m = 20 external substeps
+(stage 1: m/2, stage 2: m), momentum (2 comps) + tracer, FP64.  A "step" is one full internal step:
+both IMEX stages, both external sub-cycles.  Inputs (~48 GB of fields) are far larger than L2.
+
+value     device-resident throughput: W warm-up steps, K timed steps (one CUDA graph each),
+          CUDA events on the launching stream, barrier + synchronize on both sides, max over ranks.
+e2e       same metric through the public API with HOST (pinned) buffers: every step uploads the
+          full state from host memory, steps, and downloads it again (copies inside the timed region).
+roofline  dominant kernel: algorithmic bytes / CUDA-event launch duration vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the CPU oracle (numpy restatement of the reference, oracle/) on a bounded sample.
+--impl reference  times that CPU path (the reference arm) with all host cores, same metric.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prism-DOF updates/s (FP64 RK step)"
+UNIT = "prism-DOF/s"
+
+# compulsory (algorithmic) HBM bytes per prism for each stepper launch
+KERNEL_BYTES = {
+    "r": 48 + 96,                       # read T, write r (2 comps)
+    "project": 96 + 96,                 # read u, write q
+    "f3d2d": 96 * 3,                    # read u, q, r -> 2D only
+    "wtilde": 96 + 48,                  # read q, write w~
+    "rhs_u": 96 * 4 + 96,               # read u, u0, q, r; write rhs
+    "rhs_T": 48 + 48 + 96 + 48,         # read T, T0, q; write rhs
+    "vertical_u_impl": 96 + 48 + 96,    # read rhs, w~; write u1
+    "vertical_T_impl": 48 + 48 + 48,
+    "vertical_u_expl": 96 + 48 + 96 + 96,   # + u for A u
+    "vertical_T_expl": 48 + 48 + 48 + 48,
+}
+# 2D RK stage per triangle: X 72 + S0 72 + geometry 188 + F3D->2D 48 + write 72 (+ Qbar 48 on stage 3)
+RK_STAGE_BYTES_PER_TRI = 72 + 72 + 188 + 48 + 72 + 16
+M2_BYTES_PER_PRISM = lambda L, m: 2736 + 1881.0 * m / L  # noqa: E731  (SURVEY.md section 8d model M2)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------- CPU (oracle)
+
+def _oracle_worker(args):
+    """One bounded oracle run: `steps` full IMEX steps on a patch of the workload (own process)."""
+    name, scale, L, steps, seed = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from types import SimpleNamespace
+
+    from oracle import ext2d as OE
+    from oracle import geom as OG
+    from oracle import stepper as OS
+    from paper_2605_16082_b200.scenarios import make_case
+    c = make_case(name, scale=scale, L=L)
+    om = OG.make_mesh(c.mesh.vx, c.mesh.vy, c.mesh.vb, c.mesh.tri)
+    s0 = c.state
+    s = SimpleNamespace(grid=OG.extrude(om, c.L, s0["eta"]), ux=s0["ux"], uy=s0["uy"], T=s0["T"],
+                        s2d=OE.S2(s0["eta"].copy(), s0["qx"], s0["qy"], 0.0))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        s = OS.imex_step(s, c.params, c.dt, c.m, c.kv, c.nu_v)
+        times.append(time.perf_counter() - t0)
+    return times, c.prisms
+
+
+def cpu_oracle_throughput(name, steps, procs, scale, skip=0):
+    """prism-DOF/s of the oracle: `procs` independent patches in parallel processes (all host cores).
+
+    Returns (value, seconds per step (max over processes, mean over the timed steps), prisms per process).
+    """
+    import multiprocessing as mp
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):   # one BLAS thread per process
+        os.environ[v] = "1"
+    L = 50 if name == "c4" else None
+    jobs = [(name, scale, L, steps, i) for i in range(procs)]
+    if procs == 1:
+        res = [_oracle_worker(jobs[0])]
+    else:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            res = pool.map(_oracle_worker, jobs)
+    per_step = np.max(np.array([r[0] for r in res]), axis=0)[skip:]
+    tstep = float(np.mean(per_step))
+    prisms = res[0][1]
+    return 6.0 * prisms * procs / tstep, tstep, prisms
+
+
+def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle (numpy restatement of the reference) on all host cores."""
+    if rank != 0:
+        return
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    scale = 0.02 if args.config == "c4" else 0.2   # c4 patch: 20 x 10 squares = 400 tri x 50 layers
+    value, tstep, prisms = cpu_oracle_throughput(args.config, args.warmup + args.steps, procs, scale,
+                                                 skip=args.warmup)
+    sample = (f"{procs} independent processes, each one full IMEX step (L=50, m=20) of a {prisms}-prism patch of the "
+              f"{args.config} workload per bench step (numpy oracle, oracle/stepper.py)")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": tstep * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{args.config} (bounded CPU sample: {prisms} prisms per process)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------------------- GPU
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2605_16082_b200 import stepper as S
+    from paper_2605_16082_b200.scenarios import device_state_c4, make_case
+
+    t_setup = time.perf_counter()
+    case = make_case(args.config, with_state=(args.config != "c4"))
+    st = S.ImexStepper(case.mesh, case.L, case.params, case.dt, case.m, case.kv, case.nu_v)
+    if args.config == "c4":
+        device_state_c4(case, st)
+    else:
+        st.set_state(**case.state)
+    setup_s = time.perf_counter() - t_setup
+    P = case.prisms
+    dof_per_step = 6.0 * P
+
+    # warm-up (graph capture happens on the first step)
+    st.step(args.warmup)
+    torch.cuda.synchronize()
+    st.check()
+
+    # ---- timed region: K graph replays
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record()
+        st.step(args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    st.check()
+    value = dof_per_step * world / (t_ms * 1e-3)
+
+    # ---- per-kernel breakdown (same K steps, unfused launches with CUDA events on the launching stream)
+    launches = st.launches_per_step()
+    st.use_graph = False
+    st.prof = {}
+    st.step(args.steps)
+    torch.cuda.synchronize()
+    prof = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in st.prof.items()}
+    counts = {k: len(v) / args.steps for k, v in st.prof.items()}
+    st.prof = None
+    st.use_graph = True
+    step_sum = sum(prof[k] * counts[k] for k in prof)
+    hbm, peak_kind = peaks()
+    per = {}
+    for k, ms in prof.items():
+        if k in KERNEL_BYTES:
+            b = KERNEL_BYTES[k] * P
+        elif k.startswith("subcycle"):
+            msub = int(k[len("subcycle"):])
+            b = RK_STAGE_BYTES_PER_TRI * case.mesh.nt * 3 * msub
+        else:
+            b = 0
+        per[k] = {"ms": ms, "share": ms * counts[k] / step_sum, "GBps": (b / (ms * 1e-3) / 1e9) if b else None,
+                  "bytes": b}
+    dom = max((k for k in per if per[k]["bytes"]), key=lambda k: per[k]["ms"] * counts[k])
+    ach = per[dom]["GBps"]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_kind": peak_kind, "traffic": None,
+                "bytes_per_launch": per[dom]["bytes"], "launch_ms": per[dom]["ms"],
+                "step_model_M2": {"bytes_per_prism": M2_BYTES_PER_PRISM(case.L, case.m),
+                                  "frac": M2_BYTES_PER_PRISM(case.L, case.m) * P / (t_ms * 1e-3) / 1e9 / hbm}}
+
+    # ---- e2e: public API, host pinned buffers, full state round trip every step
+    e2e = None
+    if not args.no_e2e:
+        host = st.get_state(numpy=False)
+        pin = {k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in host.items()}
+        h2d = sum(v.numel() * 8 for v in pin.values() if isinstance(v, torch.Tensor))
+        ke = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(ke):
+            dv = {k: (v.to("cuda", non_blocking=True) if isinstance(v, torch.Tensor) else v) for k, v in pin.items()}
+            st.set_state(dv["eta"], dv["qx"], dv["qy"], dv["ux"], dv["uy"], dv["T"], dv["t"])
+            st.step(1)
+            out = st.get_state(numpy=False)
+            for k, v in out.items():
+                if isinstance(v, torch.Tensor):
+                    pin[k].copy_(v, non_blocking=True)
+        f1.record()
+        torch.cuda.synchronize()
+        te = f0.elapsed_time(f1) / ke
+        if world > 1:
+            tt = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": dof_per_step * world / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": h2d, "ms_per_step": te, "steps": ke,
+               "path": "ImexStepper.set_state/step/get_state with pinned host buffers (full state round trip)"}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        procs = 1
+        v, tstep, prisms = cpu_oracle_throughput(args.config, 2, procs, 0.02 if args.config == "c4" else 0.2)
+        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+               "sample": f"2 full IMEX steps (L={case.L}, m={case.m}) of a {prisms}-prism patch of {args.config}, "
+                         f"numpy oracle (oracle/stepper.py), single process; {tstep:.2f} s/step"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+               "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded coastal basin; inputs larger than L2, no flush needed)",
+               "config": {"workload": f"{args.config}: {case.mesh.nt} tri x {case.L} layers = {P} prisms, "
+                                      f"m={case.m}, dt2d={case.dt2d} s, momentum+tracer, FP64",
+                          "nt": case.mesh.nt, "L": case.L, "m": case.m, "prism_dof_per_step": dof_per_step,
+                          "parallelism": f"replicas{world}" if world > 1 else "single GPU",
+                          "l2": "inputs larger than L2 (~48 GB resident fields)"},
+               "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
+               "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+               "kernels": {k: {"ms": round(v["ms"], 4), "share": round(v["share"], 4),
+                               "GBps": None if v["GBps"] is None else round(v["GBps"], 1)} for k, v in per.items()},
+               "setup_s": setup_s}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -79,33 +79,40 @@ def make_case(name: str, scale: float = 1.0, with_state: bool = True, L: int | N
                            T=np.where(xnode < lx / 2, 15.0, 10.0))
         return c
     if name == "c4":
+        # scale < 1: a window of the full C4 basin at the SAME resolution (100 m squares), centred
+        # on the shelf, so per-prism cost and dynamics match the full workload (bounded CPU samples)
         nx, ny = max(2, int(1000 * scale)), max(2, int(500 * scale))
-        lx, ly = 1e5 * nx / 1000, 5e4 * ny / 500
-        mesh = hilbert_reorder(generate_basin_mesh(nx, ny, lx, ly, coastal_bed(lx, ly)))
+        LX, LY = 1e5, 5e4
+        dx = LX / 1000
+        x0 = 0.0 if nx == 1000 else 0.45 * LX
+        y0 = 0.0 if ny == 500 else 0.45 * LY
+        full = coastal_bed(LX, LY)
+        mesh = hilbert_reorder(generate_basin_mesh(nx, ny, nx * dx, ny * dx, lambda x, y: full(x + x0, y + y0)))
         p = PhysParams(f=1e-4, cd=2.5e-3, alpha=0.2, t_ref=12.5, tau_x=0.1, tau_y=0.02)
         c = Case(name, mesh, L or 50, p, 10.0, 20, 1e-4, 1e-5, 0.5)
+        c.x0, c.lx = x0, LX
         if with_state:
             c.state = c4_host_state(c)
         return c
     raise ValueError(name)
 
 
-def _c4_eta(mesh, lx):
-    return 0.05 * np.exp(-((mesh.x - 0.3 * lx) ** 2) / (0.05 * lx) ** 2)
+def _c4_eta(x, lx):
+    return 0.05 * np.exp(-((x - 0.3 * lx) ** 2) / (0.05 * lx) ** 2)
 
 
 def c4_host_state(c: Case, seed=42):
     """Host numpy C4 initial state (used for bounded CPU samples and small-scale parity)."""
     mesh, L = c.mesh, c.L
     nt, P = mesh.nt, mesh.nt * L
-    lx = float(mesh.vx.max())
-    eta = _c4_eta(mesh, lx)
+    lx, x0 = c.lx, c.x0
+    eta = _c4_eta(mesh.x + x0, lx)
     H = eta - mesh.b
     fr = np.linspace(0.0, 1.0, L + 1)
     zt = (eta[:, None, :] - fr[None, :-1, None] * H[:, None, :]).reshape(P, 3)
     zb = (eta[:, None, :] - fr[None, 1:, None] * H[:, None, :]).reshape(P, 3)
     z = np.concatenate([zt, zb], axis=1)
-    xc = np.repeat(mesh.x, L, axis=0)
+    xc = np.repeat(mesh.x + x0, L, axis=0)
     x6 = np.concatenate([xc, xc], axis=1)
     T = 12.0 + 3.0 * np.tanh((x6 - 0.5 * lx) / (0.05 * lx)) + 0.02 * z
     rng = np.random.default_rng(seed)
@@ -119,8 +126,8 @@ def device_state_c4(c: Case, stepper, seed=42):
     import torch
     mesh, L, nt = c.mesh, c.L, c.mesh.nt
     dev = stepper.dev
-    lx = float(mesh.vx.max())
-    eta = _c4_eta(mesh, lx)
+    lx, x0 = c.lx, c.x0
+    eta = _c4_eta(mesh.x + x0, lx)
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     S = stepper.S
@@ -132,7 +139,7 @@ def device_state_c4(c: Case, stepper, seed=42):
     e = S[0]                                    # [3][nt]
     b = torch.as_tensor(mesh.b.T.copy(), device=dev)
     H = e - b
-    x = torch.as_tensor(mesh.x.T.copy(), device=dev)
+    x = torch.as_tensor((mesh.x + x0).T.copy(), device=dev)
     T = stepper.T[stepper.cur]
     for lev, f in ((0, fr[:-1]), (1, fr[1:])):
         z = e[:, None, :] - f[None, :, None] * H[:, None, :]      # [3][L][nt]

@@ -41,12 +41,10 @@ class ImexStepper:
                  pen: PenaltyParams = PenaltyParams(), device=None):
         if m % 2:
             raise ValueError("m must be even (stage 1 uses m/2 substeps)")
-        for name in ("kappa_h", "kappa_v", "nu_h", "nu_v"):
-            if getattr(params, name) != 0.0 and name in ("kappa_v", "nu_v"):
-                raise NotImplementedError(f"params.{name} != 0: explicit split diffusion is not parity-pinned "
-                                          "(reference crash, internal3d.py:665)")
-        if params.kappa_h != 0.0 or params.nu_h != 0.0:
-            raise NotImplementedError("explicit horizontal diffusion is not parity-pinned (internal3d.py:665)")
+        if params.kappa_h or params.kappa_v or params.nu_h or params.nu_v:
+            raise NotImplementedError("explicit horizontal viscosity/diffusion (PhysParams kappa_*, nu_*) is not "
+                                      "parity-pinned: the reference crashes there (internal3d.py:665); vertical "
+                                      "diffusion is set by kv / nu_v")
         self.mesh, self.L, self.p = mesh, L, params
         self.dt, self.m, self.kv, self.nu_v, self.pen = float(dt), int(m), float(kv), float(nu_v), pen
         self.dm = device_mesh(mesh, L)
@@ -66,6 +64,21 @@ class ImexStepper:
         self.t = 0.0
         self.graphs = {}
         self.use_graph = True
+        self.prof = None       # {name: [(start_event, end_event), ...]} when profiling
+
+    def _c(self, name, rc):
+        _lib.check(rc, name)
+
+    def _timed(self, name, fn, *args):
+        """Launch one library entry; record CUDA events around it on the current stream when profiling."""
+        if self.prof is None:
+            _lib.check(fn(*args), name)
+            return
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(fn(*args), name)
+        e1.record()
+        self.prof.setdefault(name, []).append((e0, e1))
 
     # ------------------------------------------------------------------ state I/O (reference layouts)
     def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
@@ -93,30 +106,31 @@ class ImexStepper:
     # ------------------------------------------------------------------ one stage
     def _stage(self, s, eta_u, u, T, u0, T0, Sw, out_u, out_T, dt_s, m_s, implicit, t_wind):
         lb, h, p = _lib.lib(), self.dm.h, self.p
-        chk = _lib.check
+        tm = self._timed
         eta0 = self.S[0]
         tsx, tsy = p.wind(t_wind)
-        chk(lb.pdg_compute_r(h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s), "r")
-        chk(lb.pdg_project_transport(h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
-                                     ptr(self.qsum), ptr(self.htot), s), "project")
-        chk(lb.pdg_step_f3d2d(h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy, p.cd,
-                              ptr(self.f3d2d), s), "f3d2d")
+        tag = "impl" if implicit else "expl"
+        tm("r", lb.pdg_compute_r, h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s)
+        tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
+           ptr(self.qsum), ptr(self.htot), s)
+        tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
+           p.cd, ptr(self.f3d2d), s)
         Sw.copy_(self.S)
-        chk(lb.pdg_ext2d_subcycle(h, ptr(Sw), m_s, dt_s / m_s, p.g, p.rho0, ptr(self.f3d2d), None, None, None,
-                                  ptr(self.qbar), ptr(self.f2d), 1, s), "subcycle")
+        tm(f"subcycle{m_s}", lb.pdg_ext2d_subcycle, h, ptr(Sw), m_s, dt_s / m_s, p.g, p.rho0, ptr(self.f3d2d), None,
+           None, None, ptr(self.qbar), ptr(self.f2d), 1, s)
         eta1 = Sw[0]
-        chk(lb.pdg_mismatch(h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s), "mismatch")
-        chk(lb.pdg_compute_wtilde(h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0, ptr(self.wt), s),
-            "wtilde")
-        chk(lb.pdg_step_rhs(h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q), ptr(self.mis),
-                            ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s), "rhs_u")
-        chk(lb.pdg_step_rhs(h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q), ptr(self.mis),
-                            None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s), "rhs_T")
+        tm("mismatch", lb.pdg_mismatch, h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s)
+        tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
+           ptr(self.wt), s)
+        tm("rhs_u", lb.pdg_step_rhs, h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q),
+           ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s)
+        tm("rhs_T", lb.pdg_step_rhs, h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q),
+           ptr(self.mis), None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s)
         pe = self.pen
-        chk(lb.pdg_step_vertical(h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt), p.kappa_h,
-                                 self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s), "vertical_u")
-        chk(lb.pdg_step_vertical(h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt), p.nu_h,
-                                 self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s), "vertical_T")
+        tm(f"vertical_u_{tag}", lb.pdg_step_vertical, h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
+           ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
+        tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
+           ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
         return eta1
 
     def _launch_step(self, t0):
