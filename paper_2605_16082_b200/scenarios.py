@@ -3,7 +3,11 @@
 C1  2D seiche, 32x32 basin (2,048 tri), dt2d = 2 s, 100 SSP-RK3 steps
 C2  same basin, 10 sigma layers, barotropic, dt = 40 s, m = 20
 C3  lock exchange, 250x100 (50,000 tri) x 20 layers, dt2d = 1 s, m = 20
-C4  synthetic coastal mesh 1000x500 (1,000,000 tri) x 50 layers, dt2d = 0.5 s, m = 20  <- bench workload
+C4  synthetic coastal mesh 1000x500 (1,000,000 tri) x 50 layers, dt2d = 0.25 s, m = 20  <- bench workload
+    (SURVEY proposed dt2d = 0.5 s: c dt/dx = 0.235 passes check_cfl's 1/3 but P1-DG SSP-RK3 on these
+    right triangles blows up in the 200 m deep part within 2 steps; 0.25 s gives 0.118.  Work per step
+    -- the metric's unit -- does not depend on dt)
+    (shelf 20-200 m with seeded banks, >= 15 m; density front + linear stratification; seeded smooth u0)
 All meshes are Hilbert-reordered `generate_basin_mesh` meshes (mesh.py:150-228).
 Random fields are seeded.  `make_case(name)` returns the mesh (host setup) and
 numpy initial state in reference layouts; `device_state_c4` builds the C4 3D
@@ -40,14 +44,28 @@ class Case:
 def coastal_bed(lx, ly, seed=42, nbump=8):
     rng = np.random.default_rng(seed)
     cx, cy = rng.uniform(0, lx, nbump), rng.uniform(0, ly, nbump)
-    amp, rad = rng.uniform(-3.0, 25.0, nbump), rng.uniform(0.03, 0.1, nbump) * lx
+    amp, rad = rng.uniform(-5.0, 30.0, nbump), rng.uniform(0.05, 0.12, nbump) * lx
 
     def bed(x, y):
-        b = -(5.0 + 195.0 * x / lx)
+        # shelf 20 m -> 200 m deep plus seeded Gaussian banks/holes; >= 15 m everywhere so the 50
+        # sigma layers stay >= 0.3 m thick (the explicit stage-2 vertical advection needs it)
+        b = -(20.0 + 180.0 * x / lx)
         for i in range(nbump):
             b = b - amp[i] * np.exp(-((x - cx[i]) ** 2 + (y - cy[i]) ** 2) / rad[i] ** 2)
-        return np.minimum(b, -2.0)
+        return np.minimum(b, -15.0)
     return bed
+
+
+def smooth_velocity(x, y, lx, ly, seed=42, nmode=4, amp=0.05):
+    """Seeded smooth horizontal velocity (sum of Fourier modes), uniform over the column."""
+    rng = np.random.default_rng(seed)
+    kx, ky = rng.integers(1, 4, (2, nmode)), rng.integers(1, 4, (2, nmode))
+    ph, a = rng.uniform(0, 2 * np.pi, (2, nmode)), rng.uniform(-1, 1, (2, nmode))
+    u = sum(a[0, i] * np.sin(np.pi * kx[0, i] * x / lx + ph[0, i]) * np.cos(np.pi * ky[0, i] * y / ly)
+            for i in range(nmode))
+    v = sum(a[1, i] * np.cos(np.pi * kx[1, i] * x / lx) * np.sin(np.pi * ky[1, i] * y / ly + ph[1, i])
+            for i in range(nmode))
+    return amp * u / nmode, amp * v / nmode
 
 
 def make_case(name: str, scale: float = 1.0, with_state: bool = True, L: int | None = None) -> Case:
@@ -89,8 +107,8 @@ def make_case(name: str, scale: float = 1.0, with_state: bool = True, L: int | N
         full = coastal_bed(LX, LY)
         mesh = hilbert_reorder(generate_basin_mesh(nx, ny, nx * dx, ny * dx, lambda x, y: full(x + x0, y + y0)))
         p = PhysParams(f=1e-4, cd=2.5e-3, alpha=0.2, t_ref=12.5, tau_x=0.1, tau_y=0.02)
-        c = Case(name, mesh, L or 50, p, 10.0, 20, 1e-4, 1e-5, 0.5)
-        c.x0, c.lx = x0, LX
+        c = Case(name, mesh, L or 50, p, 5.0, 20, 1e-4, 1e-5, 0.25)
+        c.x0, c.y0, c.lx, c.ly = x0, y0, LX, LY
         if with_state:
             c.state = c4_host_state(c)
         return c
@@ -115,10 +133,11 @@ def c4_host_state(c: Case, seed=42):
     xc = np.repeat(mesh.x + x0, L, axis=0)
     x6 = np.concatenate([xc, xc], axis=1)
     T = 12.0 + 3.0 * np.tanh((x6 - 0.5 * lx) / (0.05 * lx)) + 0.02 * z
-    rng = np.random.default_rng(seed)
+    u, v = smooth_velocity(mesh.x + x0, mesh.y + c.y0, lx, c.ly, seed)
+    ux = np.repeat(np.concatenate([u, u], axis=1), L, axis=0)
+    uy = np.repeat(np.concatenate([v, v], axis=1), L, axis=0)
     z2 = np.zeros((nt, 3))
-    return dict(eta=eta, qx=z2.copy(), qy=z2.copy(), ux=0.05 * rng.standard_normal((P, 6)),
-                uy=0.05 * rng.standard_normal((P, 6)), T=T)
+    return dict(eta=eta, qx=z2.copy(), qy=z2.copy(), ux=ux, uy=uy, T=T)
 
 
 def device_state_c4(c: Case, stepper, seed=42):
@@ -128,13 +147,15 @@ def device_state_c4(c: Case, stepper, seed=42):
     dev = stepper.dev
     lx, x0 = c.lx, c.x0
     eta = _c4_eta(mesh.x + x0, lx)
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
     S = stepper.S
     S.zero_()
     S[0].copy_(torch.as_tensor(eta.T.copy(), device=dev))
     u = stepper.U[stepper.cur]
-    u.normal_(0.0, 0.05, generator=g)
+    uu, vv = smooth_velocity(mesh.x + x0, mesh.y + c.y0, lx, c.ly, seed)
+    for comp, f in ((0, uu), (1, vv)):
+        ft = torch.as_tensor(f.T.copy(), device=dev)                # [3][nt]
+        u[comp, 0:3] = ft[:, None, :]
+        u[comp, 3:6] = ft[:, None, :]
     fr = torch.as_tensor(np.linspace(0.0, 1.0, L + 1), device=dev, dtype=torch.float64)
     e = S[0]                                    # [3][nt]
     b = torch.as_tensor(mesh.b.T.copy(), device=dev)
