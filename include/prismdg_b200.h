@@ -100,6 +100,81 @@ int pdg_ext2d_cfl(pdg_ctx* ctx, const double* eta, double g, double dt, double* 
 int pdg_apply_mh(const double* v, const double* j2d, int n, int nc, int inverse, double* out, pdg_err* err,
                  void* stream);
 
+int pdg_eos(const double* T, const double* S, long long n, double alpha, double beta, double tref, double sref,
+            double* out, void* stream);                                    /* eos_density external2d.py:81-87 */
+
+/* ---- 3D internal mode (internal3d.py); eta_g = the grid's free surface (C3), geometry is
+ *      rebuilt on device from (eta_g, mesh b, sigma fractions) -------------------------------- */
+int pdg_prism_mass(pdg_ctx* ctx, const double* eta_g, const int* els, int n_els, double* mass,
+                   void* stream);                                          /* prism_mass :114-123 */
+/* mass_apply / mass_solve (:126-151): mass [36][L][nt], f/out [nc][6][L][nt]; solve != 0 -> LU */
+int pdg_mass_op(int L, int nt, int nc, int solve, const double* mass, const double* f, double* out, pdg_err* err,
+                void* stream);
+/* project_transport (:164-181); mass NULL -> exact Kronecker form; qsum [2][3][nt] (column
+ * sum of q) and htot [3][nt] (2 sum Jz) optional */
+int pdg_project_transport(pdg_ctx* ctx, const double* eta_g, const double* ux, const double* uy, const double* mass,
+                          const int* els, int n_els, double* q, double* qsum, double* htot, void* stream);
+int pdg_column_sum(int nt, int L, int ncomp, const double* f, double* out, void* stream);   /* :184-187 */
+int pdg_total_thickness(pdg_ctx* ctx, const double* eta_g, double* htot, void* stream); /* mesh.py:422 */
+/* (Qbar - sum_col q) / H  and  consistent_transport (:190-208) */
+int pdg_mismatch(pdg_ctx* ctx, const double* qbar, const double* qsum, const double* htot, double* mis,
+                 void* stream);
+int pdg_consistent_transport(pdg_ctx* ctx, const double* eta_g, const double* q, const double* mis, const int* els,
+                             int n_els, double* out, void* stream);
+int pdg_lateral_flux_factor(pdg_ctx* ctx, const double* eta_g, const double* q, double g, const int* els, int n_els,
+                            double* fac, void* stream);                      /* :275-314 */
+/* compute_r (:327-405) incl. the top-down sweep; from_T != 0 applies the linear EOS inline */
+int pdg_compute_r(pdg_ctx* ctx, const double* eta_g, const double* rho_or_T, int from_T, double alpha, double tref,
+                  double g, const int* els, int n_els, double* r, void* stream);
+int pdg_compute_w(pdg_ctx* ctx, const double* eta_g, const double* q, const double* ux, const double* uy,
+                  const double* fac, const int* els, int n_els, double* w, void* stream);   /* :434-502 */
+/* compute_wtilde (:505-541); mis != NULL -> qbar = qb + Jz mis and its factor on the fly */
+int pdg_compute_wtilde(pdg_ctx* ctx, const double* eta_g, const double* qb, const double* fac, const double* mis,
+                       double g, const int* els, int n_els, double* w, void* stream);
+/* horizontal_rhs (ncomp 2, :695-751) / tracer_horizontal_rhs (ncomp 1, :754-792), kappa = 0 */
+int pdg_horizontal_rhs(pdg_ctx* ctx, const double* eta_g, const double* u, int ncomp, const double* q_adv,
+                       const double* fac, const double* r, const double* mass, double f, double rho0, int mass_terms,
+                       const int* els, int n_els, double* out, void* stream);
+int pdg_mass_terms(int L, int nt, const double* mass, const double* u, const double* r, double f, double rho0,
+                   double* out, void* stream);                             /* :745-750 over all rows */
+int pdg_stress_rhs(pdg_ctx* ctx, const double* ux, const double* uy, double tsx, double tsy, double cd, const int* els,
+                   int n_els, double* out, void* stream);                  /* :919-934 */
+
+/* ---- column solvers (columns.py) ------------------------------------------------------------ */
+/* solve_r_column (kind 0, :95-122) / solve_w_column (kind 1, :125-151): rhs/out [nc][6][L][ncol] */
+int pdg_solve_sweep(int kind, int ncol, int L, int nc, const double* rhs, const double* j2d, const int* layers,
+                    double* out, pdg_err* err, void* stream);
+/* solve_banded_column (:292-348); gu/gw receive the propagation tiles (may alias u/w) */
+int pdg_solve_banded(int ncol, int L, int nc, const double* d, const double* u, const double* w, double* gu,
+                     double* gw, const double* rhs, double* x, pdg_err* err, void* stream);
+int pdg_apply_banded(int ncol, int L, int nc, const double* d, const double* u, const double* w, const double* x,
+                     double* y, void* stream);                               /* :356-366 */
+int pdg_build_implicit(long long P, const double* mass, const double* d, const double* u, const double* w, double dt,
+                       double* od, double* ou, double* ow, void* stream);    /* internal3d.py:902-906 */
+/* solve_tridiagonal (:507-531): arrays [n][nb] (batch contiguous), work [n][nb] */
+int pdg_solve_tridiagonal(int nb, int n, const double* lower, const double* diag, const double* upper,
+                          const double* rhs, double* x, double* work, pdg_err* err, void* stream);
+/* assemble_vertical_operator (internal3d.py:800-899): outputs compact over the selected columns */
+int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, const double* wm, double kh, double kv,
+                          double n0, int order, const int* els, int n_els, double* d, double* u, double* w,
+                          void* stream);
+
+/* ---- fused IMEX stage entries (the stepper) ---------------- */
+/* F3D->2D = column sum of horizontal_rhs(u, q, fac(q)) + stress_rhs  -> [2][3][nt] */
+int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r, double g,
+                   double f, double rho0, double tsx, double tsy, double cd, double* f3d2d, void* stream);
+/* stage right-hand sides: ncomp 2: M0 u0 + dt (F_h(u, q + Jz mis) + stress + M1 F2D/H1);
+ * ncomp 1: M0 T0 + dt F_T(T, q + Jz mis) */
+int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta0, const double* eta1,
+                 const double* u, const double* u0, const double* q, const double* mis, const double* r,
+                 const double* f2d, double g, double f, double rho0, double tsx, double tsy, double cd, double dt,
+                 double* out, void* stream);
+/* vertical stage: implicit (M1 - dt A) x = rhs by block Thomas, or explicit x = M1^-1 (rhs + dt A xin),
+ * A = assemble_vertical_operator(eta_u, wt, w_m = (z(eta1) - z(eta0)) / dt_mesh, kh, kv) in registers */
+int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
+                      const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
+                      double dt, const double* rhs, const double* xin, double* x, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
