@@ -306,20 +306,38 @@ __global__ void k_tridiag(int nb, int n, const double* __restrict__ lo, const do
 }
 
 // ============================================================================ vertical operator
-// per-layer geometry factors of assemble_vertical_operator (internal3d.py:825, 838, 875-891)
+// assemble_vertical_operator (internal3d.py:800-899) in factorised form.  Every block is a
+// combination of symmetric 3x3 "face / layer masses" of the triangle rule:
+//   R_l[a][b]   = sum_q QW BARY_a BARY_b / jzq_l(q)          (diffusion: dphi/dzeta products / Jz)
+//   Sadv_m[a][b]= J2D sum_c T3[a][b][c] (K[m][0] dw_top[c] + K[m][1] dw_bot[c])   (advective volume)
+//   F(x)[a][b]  = sum_q QW BARY_a BARY_b x(q)                 (upwinded face fluxes)
+// so a layer costs ~400 FMAs instead of the ~1500 of the literal 12-point contractions.
 struct VG {
-  double jzq[6];
-  double kis;      // ki[0] + ki[1]  (kv + kh |m_h/m_z|^2 at the two vertical points)
-  double kt, kb;   // kv + kh |grad z_top|^2, kv + kh |grad z_bot|^2
-  double hgt;      // 2 mean(Jz)
-  double nz;       // 1/sqrt(1 + |grad z_top|^2)
+  double R[3][3];  // symmetric
+  double kis;      // sum over the two vertical points of kv + kh |m_h/m_z|^2   (internal3d.py:838)
+  double kt, kb;   // kv + kh |grad z_top|^2, kv + kh |grad z_bot|^2           (:875-876)
+  double hgt;      // 2 mean(Jz)                                               (:888)
+  double nz;       // 1/sqrt(1 + |grad z_top|^2)                               (:891)
 };
 
 __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double ft, double fb, double kh, double kv,
                                      VG& V) {
   LGeo G;
   layer_geo(C, eta, ft, fb, G);
-  hq(G.jz, V.jzq);
+  double jzq[6], ij[6];
+  hq(G.jz, jzq);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) ij[q] = QW[q] / jzq[q];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) s += ij[q] * (BARY[q][a] * BARY[q][b]);
+      V.R[a][b] = s;
+      V.R[b][a] = s;
+    }
   double ks = 0.0;
 #pragma unroll
   for (int vv = 0; vv < 2; ++vv) {
@@ -340,144 +358,180 @@ __device__ __forceinline__ double pen_sigma(double la, double lb, double n0, int
   return n0 * (order + 1.0) * (order + 3.0) / (2.0 * 3.0 * lmin);
 }
 
-// layer l of A: d (6x6), u (3x6, coupling to layer l-1), w (3x6, coupling to layer l+1).
-// dw = w~ - w_m on the 6 nodes of layer l; wtn = w~ top nodes of layer l+1; wmb = w_m bottom of l.
-__device__ __forceinline__ void vop_layer(double j2d, int l, int L, const VG& Vp, const VG& V, const VG& Vn,
-                                          const double dw[6], const double wt_top[3], const double wm[6],
-                                          const double wtn[3], double n0, int order, pdg_err* err, double d[6][6],
-                                          double u[3][6], double w[3][6]) {
+// F(x) for x at the 6 points, symmetric
+__device__ __forceinline__ void face3(const double x[6], double F[3][3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) s += (QW[q] * BARY[q][a] * BARY[q][b]) * x[q];
+      F[a][b] = s;
+      F[b][a] = s;
+    }
+}
+
+// per-layer factorised pieces of A (all that vop_layer and vop_apply need)
+struct VPieces {
+  double Sa[2][3][3];   // advective volume per column level m (d[i][j] += DV[li] Sa[lj][ai][aj])
+  double Ft[3][3];      // top face: pos part (whole speed at the surface)      -> d top-top (-)
+  double Fn[3][3];      // top face: neg part (l >= 1)                           -> u[:,3:6] (-)
+  double Fi[3][3];      // bottom face: inflow part (l <= L-2)                   -> d bot-bot (+)
+  double Fo[3][3];      // bottom face: outflow part                             -> w[:,0:3] (+)
+  double cvol;          // J2D * kis                (diffusion volume coefficient on R_l)
+  double ct, ca;        // 0.5 J2D kt_l (on R_l), 0.5 J2D kb_{l-1} (on R_{l-1})  (top face, l >= 1)
+  double cb, cn;        // 0.5 J2D kb_l (on R_l), 0.5 J2D kt_{l+1} (on R_{l+1})  (bottom face, l <= L-2)
+  double pt, pb;        // 0.5 x penalty factor of the top / bottom face
+};
+
+__device__ __forceinline__ void vop_pieces(double j2d, int l, int L, const VG& Vp, const VG& V, const VG& Vn,
+                                           const double wt[6], const double wm[6], const double wtn[3], double n0,
+                                           int order, pdg_err* err, VPieces& P) {
+  double dwt[3], dwb[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    dwt[c] = wt[c] - wm[c];
+    dwb[c] = wt[3 + c] - wm[3 + c];
+  }
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    double y[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c] = j2d * (KM[mm][0] * dwt[c] + KM[mm][1] * dwb[c]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = a; b < 3; ++b) {
+        const double s = T3[a][b][0] * y[0] + T3[a][b][1] * y[1] + T3[a][b][2] * y[2];
+        P.Sa[mm][a][b] = s;
+        P.Sa[mm][b][a] = s;
+      }
+  }
+  // top face of the layer: surface keeps the interior trace; interior faces split by sign
+  double sp[6], spos[6], sneg[6];
+  {
+    double d3[3] = {wt[0] - wm[0], wt[1] - wm[1], wt[2] - wm[2]};
+    hq(d3, sp);
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    spos[q] = j2d * (l == 0 ? sp[q] : (sp[q] >= 0.0 ? sp[q] : 0.0));
+    sneg[q] = j2d * (l == 0 ? 0.0 : (sp[q] < 0.0 ? sp[q] : 0.0));
+  }
+  face3(spos, P.Ft);
+  face3(sneg, P.Fn);
+  if (l < L - 1) {
+    double a3[6], b3[6], sin_[6], sout[6];
+    hq(wtn, a3);
+    hq(wm + 3, b3);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double sb = a3[q] - b3[q];
+      sin_[q] = j2d * (sb <= 0.0 ? sb : 0.0);
+      sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
+    }
+    face3(sin_, P.Fi);
+    face3(sout, P.Fo);
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        P.Fi[a][b] = 0.0;
+        P.Fo[a][b] = 0.0;
+      }
+  }
+  P.cvol = j2d * V.kis;
+  P.ct = 0.5 * j2d * V.kt;
+  P.ca = 0.5 * j2d * Vp.kb;
+  P.cb = 0.5 * j2d * V.kb;
+  P.cn = 0.5 * j2d * Vn.kt;
+  P.pt = l > 0 ? 0.5 * (pen_sigma(V.hgt, Vp.hgt, n0, order, err) * fmax(V.kt, Vp.kb) * V.nz * j2d) : 0.0;
+  P.pb = l < L - 1 ? 0.5 * (pen_sigma(Vn.hgt, V.hgt, n0, order, err) * fmax(Vn.kt, V.kb) * Vn.nz * j2d) : 0.0;
+}
+
+// explicit blocks of layer l: d (6x6), u (3x6, to layer l-1), w (3x6, to layer l+1)
+__device__ __forceinline__ void vop_blocks(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VPieces& P,
+                                           double d[6][6], double u[3][6], double w[3][6]) {
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
-    for (int j = 0; j < 6; ++j) d[i][j] = 0.0;
+    for (int j = 0; j < 6; ++j) {
+      const int li = i / 3, lj = j / 3, a = i % 3, b = j % 3;
+      double v = DV[li] * P.Sa[lj][a][b] - DV[li] * DV[lj] * P.cvol * V.R[a][b];
+      if (li == 0 && lj == 0) v -= P.Ft[a][b] + P.pt * MHQ[a][b];
+      if (li == 1 && lj == 1) v += P.Fi[a][b] - P.pb * MHQ[a][b];
+      if (li == 0 && l > 0) v += DV[lj] * P.ct * V.R[a][b];
+      if (li == 1 && l < L - 1) v -= DV[lj] * P.cb * V.R[a][b];
+      d[i][j] = v;
+    }
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+  for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-      u[i][j] = 0.0;
-      w[i][j] = 0.0;
-    }
-  double dt3[6], db3[6];
-  hq(dw, dt3);
-  hq(dw + 3, db3);
-  // advective volume + implicit diffusion volume (internal3d.py:832-841)
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    double A[2];
-#pragma unroll
-    for (int lj = 0; lj < 2; ++lj) {
-      double s = 0.0;
-#pragma unroll
-      for (int vv = 0; vv < 2; ++vv) {
-        const double spd = VS[vv][0] * dt3[q] + VS[vv][1] * db3[q];
-        s += QW[q] * (j2d * spd) * VS[vv][lj];
+      const int lj = j / 3, b = j % 3;
+      double uu = 0.0, ww = 0.0;
+      if (l > 0) {
+        uu = DV[lj] * P.ca * Vp.R[a][b];
+        if (lj == 1) uu += P.pt * MHQ[a][b] - P.Fn[a][b];
       }
-      A[lj] = s;
-    }
-    const double kd = QW[q] * V.kis * (j2d / V.jzq[q]);
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        const double bb = BARY[q][i % 3] * BARY[q][j % 3];
-        d[i][j] += DV[i / 3] * bb * A[j / 3] - kd * DV[i / 3] * DV[j / 3] * bb;
+      if (l < L - 1) {
+        ww = -DV[lj] * P.cn * Vn.R[a][b];
+        if (lj == 0) ww += P.Fo[a][b] + P.pb * MHQ[a][b];
       }
-  }
-  // advective interface fluxes (internal3d.py:843-870)
-  double wtt[6], wmt[6];
-  hq(wt_top, wtt);
-  hq(wm, wmt);
-  if (l == 0 || true) {
-    // top face: surface keeps the interior trace; interior faces split by sign
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double sp = wtt[q] - wmt[q];
-      const double pos = l == 0 ? sp : (sp >= 0.0 ? sp : 0.0);
-      const double neg = l == 0 ? 0.0 : (sp < 0.0 ? sp : 0.0);
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const double bb = QW[q] * BARY[q][i] * BARY[q][j];
-          d[i][j] -= bb * (j2d * pos);
-          u[i][3 + j] -= bb * (j2d * neg);
-        }
+      u[a][j] = uu;
+      w[a][j] = ww;
     }
+}
+
+__device__ __forceinline__ void mv3(const double M[3][3], const double x[3], double y[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) y[a] = M[a][0] * x[0] + M[a][1] * x[1] + M[a][2] * x[2];
+}
+
+// y = A x for layer l, matrix free: x rows of layers l-1 (xa), l (xc), l+1 (xb), 6 nodes each
+__device__ __forceinline__ void vop_apply(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VPieces& P,
+                                          const double xa[6], const double xc[6], const double xb[6], double y[6]) {
+  double t[3], s[3], dzc[3], r[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) dzc[a] = DV[0] * xc[a] + DV[1] * xc[3 + a];
+  // advective volume + diffusion volume
+  mv3(P.Sa[0], xc, t);
+  mv3(P.Sa[1], xc + 3, s);
+  mv3(V.R, dzc, r);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double av = t[a] + s[a];
+    y[a] = DV[0] * av - DV[0] * P.cvol * r[a];
+    y[3 + a] = DV[1] * av - DV[1] * P.cvol * r[a];
   }
-  if (l < L - 1) {
-    double wnt[6], wmb[6];
-    hq(wtn, wnt);
-    hq(wm + 3, wmb);
+  // top face
+  mv3(P.Ft, xc, t);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double sb = wnt[q] - wmb[q];
-      const double into = sb <= 0.0 ? sb : 0.0, outof = sb > 0.0 ? sb : 0.0;
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const double bb = QW[q] * BARY[q][i] * BARY[q][j];
-          d[3 + i][3 + j] += bb * (j2d * into);
-          w[i][j] += bb * (j2d * outof);
-        }
-    }
-  }
-  // diffusive mean flux and interior penalty on interior horizontal faces (internal3d.py:873-897)
-  double mf[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) s += QW[q] * BARY[q][i] * BARY[q][j];
-      mf[i][j] = s;
-    }
+  for (int a = 0; a < 3; ++a) y[a] -= t[a];
   if (l > 0) {
+    double dza[3], ra[3], mt[3], ma[3], fn[3];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double hi = 0.5 * j2d * V.kt / V.jzq[q];
-      const double he = 0.5 * j2d * Vp.kb / Vp.jzq[q];
+    for (int a = 0; a < 3; ++a) dza[a] = DV[0] * xa[a] + DV[1] * xa[3 + a];
+    mv3(Vp.R, dza, ra);
+    mv3(MHQ, xc, mt);
+    mv3(MHQ, xa + 3, ma);
+    mv3(P.Fn, xa + 3, fn);
 #pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          const double bd = QW[q] * BARY[q][i] * (DV[j / 3] * BARY[q][j % 3]);
-          d[i][j] += hi * bd;
-          u[i][j] += he * bd;
-        }
-    }
-    const double pf = pen_sigma(V.hgt, Vp.hgt, n0, order, err) * fmax(V.kt, Vp.kb) * V.nz * j2d;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        d[i][j] -= 0.5 * pf * mf[i][j];
-        u[i][3 + j] += 0.5 * pf * mf[i][j];
-      }
+    for (int a = 0; a < 3; ++a) y[a] += P.ct * r[a] + P.ca * ra[a] - P.pt * mt[a] + P.pt * ma[a] - fn[a];
   }
   if (l < L - 1) {
+    double dzb[3], rb[3], mb[3], mn[3], fi[3], fo[3];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double he = 0.5 * j2d * V.kb / V.jzq[q];
-      const double hi = 0.5 * j2d * Vn.kt / Vn.jzq[q];
+    for (int a = 0; a < 3; ++a) dzb[a] = DV[0] * xb[a] + DV[1] * xb[3 + a];
+    mv3(Vn.R, dzb, rb);
+    mv3(MHQ, xc + 3, mb);
+    mv3(MHQ, xb, mn);
+    mv3(P.Fi, xc + 3, fi);
+    mv3(P.Fo, xb, fo);
 #pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          const double bd = QW[q] * BARY[q][i] * (DV[j / 3] * BARY[q][j % 3]);
-          d[3 + i][j] -= he * bd;
-          w[i][j] -= hi * bd;
-        }
-    }
-    const double pf = pen_sigma(Vn.hgt, V.hgt, n0, order, err) * fmax(Vn.kt, V.kb) * Vn.nz * j2d;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        d[3 + i][3 + j] -= 0.5 * pf * mf[i][j];
-        w[i][j] += 0.5 * pf * mf[i][j];
-      }
+    for (int a = 0; a < 3; ++a) y[3 + a] += fi[a] - P.cb * r[a] - P.cn * rb[a] - P.pb * mb[a] + P.pb * mn[a] + fo[a];
   }
 }
 
@@ -509,7 +563,7 @@ __device__ __forceinline__ void wm_layer(const VopArgs& a, const double b[3], co
   }
 }
 
-// assemble_vertical_operator (API): writes d [36][L][nt], u/w [18][L][nt]
+// assemble_vertical_operator (API): writes d [36][L][n], u/w [18][L][n] (compact over els)
 __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __restrict__ els, int n,
                                              double* __restrict__ od, double* __restrict__ ou,
                                              double* __restrict__ ow) {
@@ -521,23 +575,23 @@ __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __re
   double eta[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) eta[k] = a.eta_u[k * nt + c];
-  // output rows are compact over the selected columns (reference returns (n_els, L, ...))
   VG Vp, V, Vn;
   vgeo(C, eta, m.fracs[0], m.fracs[1], a.kh, a.kv, V);
   Vp = V;
+  Vn = V;
   for (int l = 0; l < L; ++l) {
     if (l < L - 1) vgeo(C, eta, m.fracs[l + 1], m.fracs[l + 2], a.kh, a.kv, Vn);
-    double wt[6], wm[6], wtn[3] = {0, 0, 0}, dw[6];
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
     ld6(a.wt, l, c, L, nt, wt);
     wm_layer(a, C.b, nullptr, nullptr, 0, 0, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
     }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) dw[k] = wt[k] - wm[k];
+    VPieces P;
+    vop_pieces(C.j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.n0, a.order, m.err, P);
     double d[6][6], u[3][6], w[3][6];
-    vop_layer(C.j2d, l, L, Vp, V, Vn, dw, wt, wm, wtn, a.n0, a.order, m.err, d, u, w);
+    vop_blocks(l, L, Vp, V, Vn, P, d, u, w);
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
@@ -554,14 +608,48 @@ __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __re
   }
 }
 
+// unpivoted 6x6 LU that keeps the reciprocal pivots (solves then multiply instead of divide)
+__device__ __forceinline__ int lu6r(double a[6][6], double rp[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    if (a[k][k] == 0.0) return k;
+    const double inv = 1.0 / a[k][k];
+    rp[k] = inv;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      a[i][k] = a[i][k] * inv;
+#pragma unroll
+      for (int j = k + 1; j < 6; ++j) a[i][j] = a[i][j] - a[i][k] * a[k][j];
+    }
+  }
+  return -1;
+}
+template <int NR>
+__device__ __forceinline__ void lu6r_solve(const double a[6][6], const double rp[6], double b[6][NR]) {
+#pragma unroll
+  for (int i = 1; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) b[i][r] = b[i][r] - a[i][j] * b[j][r];
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) b[i][r] = b[i][r] - a[i][j] * b[j][r];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) b[i][r] = b[i][r] * rp[i];
+  }
+}
+
 // ============================================================================ fused vertical step
-// IMPLICIT: x = (M1 - dt A)^-1 rhs by block Thomas with A assembled per layer in registers.
-// EXPLICIT: x = M1^-1 (rhs + dt A xin)  (internal3d.py:902-906 + columns.py:292-366 + :134-151).
-// Scratch: G tiles [36][L][nt] (implicit only).
-template <int NC, bool IMPLICIT>
-__global__ void __launch_bounds__(128) k_vstep(DMesh m, VopArgs a, double dt, const double* __restrict__ rhs,
-                                               const double* __restrict__ xin, double* __restrict__ Gs,
-                                               double* __restrict__ x) {
+// IMPLICIT: (M1 - dt A) x = rhs by block Thomas (columns.py:292-348 order) with the layer blocks
+// assembled in registers; only the propagation tile G_l (36) is kept (workspace) for the back
+// substitution; the reduced RHS g_l is parked in x.  x may alias rhs.
+template <int NC>
+__global__ void __launch_bounds__(128) k_vimplicit(DMesh m, VopArgs a, double dt, const double* rhs,
+                                                   double* __restrict__ Gs, double* x) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
   if (c >= nt) return;
@@ -576,201 +664,230 @@ __global__ void __launch_bounds__(128) k_vstep(DMesh m, VopArgs a, double dt, co
     e1[k] = a.eta1[k * nt + c];
   }
   const double j2d = C.j2d;
-  const double K00 = VS[0][0] * VS[0][0] + VS[1][0] * VS[1][0];
-  const double K01 = VS[0][0] * VS[0][1] + VS[1][0] * VS[1][1];
   VG Vp, V, Vn;
   vgeo(C, eta, m.fracs[0], m.fracs[1], a.kh, a.kv, V);
   Vp = V;
+  Vn = V;
   double gp[6][NC];
-  double xa[NC][6], xc[NC][6], xb[NC][6];  // explicit: x_{l-1}, x_l, x_{l+1}
-  if (!IMPLICIT) {
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      ld6(xin + cc * P6, 0, c, L, nt, xc[cc]);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) xa[cc][k] = 0.0;
-    }
-  }
   for (int l = 0; l < L; ++l) {
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     if (l < L - 1) vgeo(C, eta, fb, m.fracs[l + 2], a.kh, a.kv, Vn);
-    double wt[6], wm[6], wtn[3] = {0, 0, 0}, dw[6];
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
     ld6(a.wt, l, c, L, nt, wt);
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
     }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) dw[k] = wt[k] - wm[k];
+    VPieces P;
+    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.n0, a.order, m.err, P);
     double d[6][6], u[3][6], w[3][6];
-    vop_layer(j2d, l, L, Vp, V, Vn, dw, wt, wm, wtn, a.n0, a.order, m.err, d, u, w);
-    // M1 of this layer (Kronecker form)
-    double jz1[3], q1[6], M1h[3][3];
+    vop_blocks(l, L, Vp, V, Vn, P, d, u, w);
+    // M1 - dt A   (M1 = K (x) J2D Mjz(eta1))
+    double jz1[3], M1h[3][3];
     layer_jz(C.b, e1, ft, fb, jz1);
-    hq(jz1, q1);
-    mass_h(q1, M1h);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p; q < 3; ++q) {
+        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+        M1h[p][q] = s;
+        M1h[q][p] = s;
+      }
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) d[i][j] = KM[i / 3][j / 3] * M1h[i % 3][j % 3] - dt * d[i][j];
     double g[6][NC];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) g[i][cc] = rhs[cc * P6 + ((size_t)i * L + l) * nt + c];
-    if (IMPLICIT) {
-      // (M1 - dt A) blocks
+    if (l > 0) {
 #pragma unroll
-      for (int i = 0; i < 6; ++i)
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          const double Kij = (i / 3 == j / 3) ? K00 : K01;
-          d[i][j] = Kij * (j2d * M1h[i % 3][j % 3]) - dt * d[i][j];
-        }
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          u[i][j] = -dt * u[i][j];
-          w[i][j] = -dt * w[i][j];
-        }
-      if (l > 0) {
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          double G[6];
-#pragma unroll
-          for (int k = 0; k < 6; ++k) G[k] = Gs[((size_t)(k * 6 + j) * L + (l - 1)) * nt + c];
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) acc = acc + u[i][k] * G[k];
-            d[i][j] = d[i][j] - acc;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int cc = 0; cc < NC; ++cc) {
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) acc = acc + u[i][k] * gp[k][cc];
-            g[i][cc] = g[i][cc] - acc;
-          }
-      }
-      const int bad = lu6(d);
-      if (bad >= 0) {
-        report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
-        return;
-      }
-      if (l < L - 1) {
-        double t[6][6];
-#pragma unroll
-        for (int j = 0; j < 6; ++j)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            t[i][j] = 0.0;
-            t[3 + i][j] = w[i][j];
-          }
-        lu6_solve<6>(d, t);
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-          for (int j = 0; j < 6; ++j) Gs[((size_t)(i * 6 + j) * L + l) * nt + c] = t[i][j];
-      }
-      lu6_solve<NC>(d, g);
-#pragma unroll
-      for (int i = 0; i < 6; ++i)
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) {
-          x[cc * P6 + ((size_t)i * L + l) * nt + c] = g[i][cc];
-          gp[i][cc] = g[i][cc];
-        }
-    } else {
-      // rhs + dt (D x_l + [U x_{l-1}; W x_{l+1}]), then M1^-1 via K^-1 (x) (J2D Mjz)^-1
-      if (l < L - 1) {
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) ld6(xin + cc * P6, l + 1, c, L, nt, xb[cc]);
-      }
-      const double det = K00 * K00 - K01 * K01;
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        double y[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          double t = 0.0;
-#pragma unroll
-          for (int j = 0; j < 6; ++j) t += d[i][j] * xc[cc][j];
-          if (i < 3 && l > 0) {
-#pragma unroll
-            for (int j = 0; j < 6; ++j) t += u[i][j] * xa[cc][j];
-          }
-          if (i >= 3 && l < L - 1) {
-#pragma unroll
-            for (int j = 0; j < 6; ++j) t += w[i - 3][j] * xb[cc][j];
-          }
-          y[i] = g[i][cc] + dt * t;
-        }
-        double z[2][3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          z[0][k] = (K00 * y[k] - K01 * y[3 + k]) / det;
-          z[1][k] = (-K01 * y[k] + K00 * y[3 + k]) / det;
-        }
-#pragma unroll
-        for (int lev = 0; lev < 2; ++lev) {
-          double A[3][3];
-#pragma unroll
-          for (int p = 0; p < 3; ++p)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) A[p][q] = j2d * M1h[p][q];
-          if (!solve3(A, z[lev])) report(m.err, PDG_ERR_ZERO_PIVOT, l, 3 * lev, 0.0);
-        }
-        double o[6];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          o[k] = z[0][k];
-          o[3 + k] = z[1][k];
-        }
-        st6(x + cc * P6, l, c, L, nt, o);
-      }
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          xa[cc][k] = xc[cc][k];
-          xc[cc][k] = xb[cc][k];
-        }
-    }
-    Vp = V;
-    V = Vn;
-  }
-  if (IMPLICIT) {
-    double xn[6][NC];
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) xn[i][cc] = gp[i][cc];
-    for (int l = L - 2; l >= 0; --l) {
-      double xl[6][NC];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
+      for (int j = 0; j < 6; ++j) {
         double G[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = Gs[((size_t)(i * 6 + k) * L + l) * nt + c];
+        for (int k = 0; k < 6; ++k) G[k] = Gs[((size_t)(k * 6 + j) * L + (l - 1)) * nt + c];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * G[k];
+          d[i][j] = d[i][j] - acc;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + G[k] * xn[k][cc];
-          xl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c] - acc;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 6; ++i)
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) {
-          x[cc * P6 + ((size_t)i * L + l) * nt + c] = xl[i][cc];
-          xn[i][cc] = xl[i][cc];
+          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * gp[k][cc];
+          g[i][cc] = g[i][cc] - acc;
         }
     }
+    double rp[6];
+    const int bad = lu6r(d, rp);
+    if (bad >= 0) {
+      report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
+      return;
+    }
+    if (l < L - 1) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        double t[6][1];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          t[i][0] = 0.0;
+          t[3 + i][0] = -dt * w[i][j];
+        }
+        lu6r_solve<1>(d, rp, t);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) Gs[((size_t)(i * 6 + j) * L + l) * nt + c] = t[i][0];
+      }
+    }
+    lu6r_solve<NC>(d, rp, g);
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        x[cc * P6 + ((size_t)i * L + l) * nt + c] = g[i][cc];
+        gp[i][cc] = g[i][cc];
+      }
+    Vp = V;
+    V = Vn;
+  }
+  double xn[6][NC];
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = gp[i][cc];
+  for (int l = L - 2; l >= 0; --l) {
+    double xl[6][NC];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      double G[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) G[k] = Gs[((size_t)(i * 6 + k) * L + l) * nt + c];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) acc = acc + G[k] * xn[k][cc];
+        xl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c] - acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        x[cc * P6 + ((size_t)i * L + l) * nt + c] = xl[i][cc];
+        xn[i][cc] = xl[i][cc];
+      }
+  }
+}
+
+// EXPLICIT: x = M1^-1 (rhs + dt A xin), A applied matrix free; M1^-1 = K^-1 (x) (J2D Mjz)^-1.
+template <int NC>
+__global__ void __launch_bounds__(128) k_vexplicit(DMesh m, VopArgs a, double dt, const double* rhs,
+                                                   const double* __restrict__ xin, double* x) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = m.nt, L = m.L;
+  if (c >= nt) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3], e0[3], e1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    eta[k] = a.eta_u[k * nt + c];
+    e0[k] = a.eta0[k * nt + c];
+    e1[k] = a.eta1[k * nt + c];
+  }
+  const double j2d = C.j2d;
+  const double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
+  VG Vp, V, Vn;
+  vgeo(C, eta, m.fracs[0], m.fracs[1], a.kh, a.kv, V);
+  Vp = V;
+  Vn = V;
+  double xa[NC][6], xc[NC][6], xb[NC][6];
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    ld6(xin + cc * P6, 0, c, L, nt, xc[cc]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      xa[cc][k] = 0.0;
+      xb[cc][k] = 0.0;
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    if (l < L - 1) {
+      vgeo(C, eta, fb, m.fracs[l + 2], a.kh, a.kv, Vn);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) ld6(xin + cc * P6, l + 1, c, L, nt, xb[cc]);
+    }
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
+    ld6(a.wt, l, c, L, nt, wt);
+    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if (l < L - 1) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+    }
+    VPieces P;
+    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.n0, a.order, m.err, P);
+    double jz1[3], A1[3][3];
+    layer_jz(C.b, e1, ft, fb, jz1);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p; q < 3; ++q) {
+        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+        A1[p][q] = s;
+        A1[q][p] = s;
+      }
+    // LDL-free 3x3 factorisation of J2D Mjz(eta1), shared by every component
+    double r0 = 1.0 / A1[0][0];
+    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
+    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
+    const double a22p = A1[2][2] - l20 * A1[0][2];
+    const double r1 = 1.0 / a11;
+    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
+    const double r2 = 1.0 / (a22p - l21 * a12);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      double y[6], g[6];
+      vop_apply(l, L, Vp, V, Vn, P, xa[cc], xc[cc], xb[cc], y);
+      ld6(rhs + cc * P6, l, c, L, nt, g);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) y[k] = g[k] + dt * y[k];
+      double o[6];
+#pragma unroll
+      for (int lev = 0; lev < 2; ++lev) {
+        double z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          z[k] = lev == 0 ? (KM[1][1] * y[k] - KM[0][1] * y[3 + k]) / det : (-KM[1][0] * y[k] + KM[0][0] * y[3 + k]) / det;
+        z[1] -= l10 * z[0];
+        z[2] -= l20 * z[0] + l21 * z[1];
+        z[2] *= r2;
+        z[1] = (z[1] - a12 * z[2]) * r1;
+        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
+      }
+      st6(x + cc * P6, l, c, L, nt, o);
+    }
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        xa[cc][k] = xc[cc][k];
+        xc[cc][k] = xb[cc][k];
+      }
+    Vp = V;
+    V = Vn;
   }
 }
 
@@ -846,24 +963,21 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
                       double dt, const double* rhs, const double* xin, double* x, void* stream) {
   VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, kh, kv, n0, order};
   const int nt = ctx->nt;
-  double* Gs = nullptr;
-  if (implicit) {
-    Gs = ctx->ws3((size_t)36 * ctx->L * nt);
-    if (!Gs) return PDG_ERR_CUDA;
-  }
   const dim3 g(nblocks(nt, 128)), b(128);
   cudaStream_t s = (cudaStream_t)stream;
   DMesh m = ctx->view();
-  if (ncomp == 2) {
-    if (implicit)
-      k_vstep<2, true><<<g, b, 0, s>>>(m, a, dt, rhs, xin, Gs, x);
+  if (implicit) {
+    double* Gs = ctx->ws3((size_t)36 * ctx->L * nt);
+    if (!Gs) return PDG_ERR_CUDA;
+    if (ncomp == 2)
+      k_vimplicit<2><<<g, b, 0, s>>>(m, a, dt, rhs, Gs, x);
     else
-      k_vstep<2, false><<<g, b, 0, s>>>(m, a, dt, rhs, xin, Gs, x);
+      k_vimplicit<1><<<g, b, 0, s>>>(m, a, dt, rhs, Gs, x);
   } else {
-    if (implicit)
-      k_vstep<1, true><<<g, b, 0, s>>>(m, a, dt, rhs, xin, Gs, x);
+    if (ncomp == 2)
+      k_vexplicit<2><<<g, b, 0, s>>>(m, a, dt, rhs, xin, x);
     else
-      k_vstep<1, false><<<g, b, 0, s>>>(m, a, dt, rhs, xin, Gs, x);
+      k_vexplicit<1><<<g, b, 0, s>>>(m, a, dt, rhs, xin, x);
   }
   return check_launch(ctx);
 }

@@ -40,6 +40,25 @@ __device__ constexpr double DV[2] = {0.5, -0.5};
 // ES[h][s]: edge point h, shape s in the edge's own traversal order
 __device__ constexpr double ES[2][2] = {{VHI, VLO}, {VLO, VHI}};
 
+// Derived constants of the same quadrature (exact P1 integrals as the rule evaluates them):
+//   W1[a]      = sum_q QW BARY_a            (= 1/6 up to the 13-digit rule literals)
+//   MHQ[a][b]  = sum_q QW BARY_a BARY_b     (triangle mass pattern, = MH of columns.py:35)
+//   T3[a][b][c]= sum_q QW BARY_a BARY_b BARY_c
+//   K[a][b]    = sum_v VS[v][a] VS[v][b]   (1D P1 mass on [-1,1] / 2: [[2/3,1/3],[1/3,2/3]])
+//   K3[m][a][b]= sum_v VS[v][m] VS[v][a] VS[v][b]
+__device__ constexpr double W1[3] = {0.16666666666666607, 0.16666666666666607, 0.16666666666666605};
+__device__ constexpr double MHQ[3][3] = {{0.08333333333333315, 0.041666666666666484, 0.041666666666666484},
+                                         {0.041666666666666484, 0.08333333333333315, 0.041666666666666484},
+                                         {0.041666666666666484, 0.041666666666666484, 0.08333333333333315}};
+constexpr double T3D = 0.04999999999999996, T3A = 0.0166666666666666, T3C = 0.008333333333333285;
+__device__ constexpr double T3[3][3][3] = {{{T3D, T3A, T3A}, {T3A, T3A, T3C}, {T3A, T3C, T3A}},
+                                           {{T3A, T3A, T3C}, {T3A, T3D, T3A}, {T3C, T3A, T3A}},
+                                           {{T3A, T3C, T3A}, {T3C, T3A, T3A}, {T3A, T3A, T3D}}};
+__device__ constexpr double KM[2][2] = {{0.6666666666666666, 0.33333333333333326},
+                                        {0.33333333333333326, 0.6666666666666666}};
+constexpr double K3A = 0.5, K3B = 0.16666666666666663;
+__device__ constexpr double K3[2][2][2] = {{{K3A, K3B}, {K3B, K3B}}, {{K3B, K3B}, {K3B, K3A}}};
+
 __host__ __device__ constexpr int EV0(int k) { return k; }
 __host__ __device__ constexpr int EV1(int k) { return k == 2 ? 0 : k + 1; }
 
