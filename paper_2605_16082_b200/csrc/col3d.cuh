@@ -85,8 +85,9 @@ __device__ __forceinline__ void lat_add(double acc[6], int k, const double x[2][
 // per-column neighbour data of one interior edge, loaded once per column
 struct EdgeNb {
   int e2, k2;
-  double eta0, eta1, b0, b1;  // neighbour free surface / bed at its edge corners (own traversal order)
-  double stab[2];             // 0.5 [[eta]] max(c) at the two edge points (internal3d.py:296-301)
+  double stab[2];  // 0.5 [[eta]] max(c) at the two edge points (internal3d.py:296-301)
+  double hm[2];    // 0.5 (H_own + H_nbr) at the edge points: {Jz} = (f_b - f_t)/2 * hm on sigma layers
+  double hn[2];    // neighbour depth H at its two edge corners (own traversal order)
 };
 
 __device__ __forceinline__ void edge_setup(const DMesh& m, const Col& C, const double eta[3],
@@ -96,61 +97,73 @@ __device__ __forceinline__ void edge_setup(const DMesh& m, const Col& C, const d
   E.k2 = C.nk[k];
   if (C.tag[k] != 0) return;
   const int i0 = EV0(E.k2) * nt + E.e2, i1 = EV1(E.k2) * nt + E.e2;
-  E.eta0 = eta_g[i0];
-  E.eta1 = eta_g[i1];
-  E.b0 = ldg(m.b + i0);
-  E.b1 = ldg(m.b + i1);
+  const double eta0 = eta_g[i0], eta1 = eta_g[i1];
+  const double b0 = ldg(m.b + i0), b1 = ldg(m.b + i1);
+  E.hn[0] = eta0 - b0;
+  E.hn[1] = eta1 - b1;
   double ei[2], ee[2], bi[2], be[2];
   tr2_own(eta, k, ei);
   tr2_own(C.b, k, bi);
-  tr2_nb(E.eta0, E.eta1, ee);
-  tr2_nb(E.b0, E.b1, be);
+  tr2_nb(eta0, eta1, ee);
+  tr2_nb(b0, b1, be);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const double hi = ei[h] - bi[h], he = ee[h] - be[h];
-    E.stab[h] = 0.5 * (ei[h] - ee[h]) * fmax(sqrt(g * hi), sqrt(g * he));
+    // max(sqrt(g hi), sqrt(g he)) == sqrt(g max(hi, he)) exactly (sqrt is monotone, correctly rounded)
+    E.stab[h] = 0.5 * (ei[h] - ee[h]) * sqrt(g * fmax(hi, he));
+    E.hm[h] = 0.5 * (hi + he);
   }
 }
 
-// neighbour half thicknesses at its two edge corners for layer fractions (ft, fb)
-__device__ __forceinline__ void nb_jz(const EdgeNb& E, double ft, double fb, double& j0, double& j1) {
-  const double H0 = __dsub_rn(E.eta0, E.b0), H1 = __dsub_rn(E.eta1, E.b1);
-  j0 = __dmul_rn(0.5, __dsub_rn(__dsub_rn(E.eta0, __dmul_rn(ft, H0)), __dsub_rn(E.eta0, __dmul_rn(fb, H0))));
-  j1 = __dmul_rn(0.5, __dsub_rn(__dsub_rn(E.eta1, __dmul_rn(ft, H1)), __dsub_rn(E.eta1, __dmul_rn(fb, H1))));
+// combine own and neighbour lateral nodes so one trace gives the interface mean:
+// own trace uses (o0, o1) with ES[h][0..1], the mirrored neighbour (n0, n1) with ES[h][1..0]
+__device__ __forceinline__ void tr_mean(const double o[6], int k, const double n4[4], double t[2][2]) {
+  const int a = EV0(k), b = EV1(k);
+  const double c0 = o[a] + n4[1], c1 = o[b] + n4[0], c2 = o[3 + a] + n4[3], c3 = o[3 + b] + n4[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double ht = c0 * ES[h][0] + c1 * ES[h][1];
+    const double hb = c2 * ES[h][0] + c3 * ES[h][1];
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv) t[vv][h] = 0.5 * (VS[vv][0] * ht + VS[vv][1] * hb);
+  }
+}
+
+// half jump 0.5 (own - nbr) at the face points from combined nodes
+__device__ __forceinline__ void tr_jump(const double o[6], int k, const double n4[4], double t[2][2]) {
+  const int a = EV0(k), b = EV1(k);
+  const double c0 = o[a] - n4[1], c1 = o[b] - n4[0], c2 = o[3 + a] - n4[3], c3 = o[3 + b] - n4[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double ht = c0 * ES[h][0] + c1 * ES[h][1];
+    const double hb = c2 * ES[h][0] + c3 * ES[h][1];
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv) t[vv][h] = 0.5 * (VS[vv][0] * ht + VS[vv][1] * hb);
+  }
 }
 
 // stabilised lateral flux factor n.{q} + {Jz/H} max(c) [[eta]] on interior edge k
-// (internal3d.py:275-314).  qo: own q (2 comps x 6 nodes), qn: neighbour lateral nodes (2 x 4)
-__device__ __forceinline__ void lat_factor(const Col& C, const EdgeNb& E, int k, const double jz[3],
-                                           const double eta[3], double ft, double fb, const double qo[2][6],
+// (internal3d.py:275-314).  On sigma layers Jz/H = (f_b - f_t)/2 =: jm for every column.
+__device__ __forceinline__ void lat_factor(const Col& C, const EdgeNb& E, int k, double jm, const double qo[2][6],
                                            const double qn[2][4], double fac[2][2]) {
-  double ti[2][2][2], te[2][2][2];  // [comp][v][h]
+  double o[6], n4[4];
 #pragma unroll
-  for (int cc = 0; cc < 2; ++cc) {
-    tr_own(qo[cc], k, ti[cc]);
-    tr_nb(qn[cc], te[cc]);
-  }
-  double jo[3];
+  for (int i = 0; i < 6; ++i) o[i] = C.nx[k] * qo[0][i] + C.ny[k] * qo[1][i];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) jo[i] = jz[i] / (eta[i] - C.b[i]);
-  double j0, j1;
-  nb_jz(E, ft, fb, j0, j1);
-  j0 = j0 / (E.eta0 - E.b0);
-  j1 = j1 / (E.eta1 - E.b1);
-  double a2[2], b2[2], ja[2][2], jb[2][2];
-  tr2_own(jo, k, a2);
-  tr2_nb(j0, j1, b2);
-  tr_dup(a2, ja);
-  tr_dup(b2, jb);
+  for (int i = 0; i < 4; ++i) n4[i] = C.nx[k] * qn[0][i] + C.ny[k] * qn[1][i];
+  double t[2][2];
+  tr_mean(o, k, n4, t);
 #pragma unroll
   for (int vv = 0; vv < 2; ++vv)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const double qx = 0.5 * (ti[0][vv][h] + te[0][vv][h]);
-      const double qy = 0.5 * (ti[1][vv][h] + te[1][vv][h]);
-      const double jm = 0.5 * (ja[vv][h] + jb[vv][h]);
-      fac[vv][h] = C.nx[k] * qx + C.ny[k] * qy + jm * E.stab[h];
-    }
+    for (int h = 0; h < 2; ++h) fac[vv][h] = t[vv][h] + jm * E.stab[h];
+}
+
+// bilinear P1 x P1 integral over the prism against phi_z: S[m] = sum_{l1,l2} K3[m][l1][l2] a_l1^T MHQ b_l2
+// (= sum_vq QW VS[v][m] a(v,q) b(v,q), exact for the 12-point rule)
+__device__ __forceinline__ void mhq_vec(const double x[3], double y[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) y[a] = MHQ[a][0] * x[0] + MHQ[a][1] * x[1] + MHQ[a][2] * x[2];
 }
 
 // iso-zeta divergence test term: acc[lev*3+i] += J2D (dphx_i S[lev][0] + dphy_i S[lev][1])

@@ -243,9 +243,7 @@ __global__ void k_factor(DMesh m, const double* __restrict__ eta_g, const double
 #pragma unroll
   for (int k = 0; k < 3; ++k) edge_setup(m, C, eta, eta_g, k, g, E[k]);
   for (int l = 0; l < L; ++l) {
-    const double ft = m.fracs[l], fb = m.fracs[l + 1];
-    double jz[3];
-    layer_jz(C.b, eta, ft, fb, jz);
+    const double jm = 0.5 * (m.fracs[l + 1] - m.fracs[l]);
     double qo[2][6];
     ld6(q, l, c, L, nt, qo[0]);
     ld6(q + P6, l, c, L, nt, qo[1]);
@@ -256,7 +254,7 @@ __global__ void k_factor(DMesh m, const double* __restrict__ eta_g, const double
         double qn[2][4];
         ld_nb4(q, E[k].k2, E[k].e2, l, L, nt, qn[0]);
         ld_nb4(q + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
-        lat_factor(C, E[k], k, jz, eta, ft, fb, qo, qn, f);
+        lat_factor(C, E[k], k, jm, qo, qn, f);
       }
 #pragma unroll
       for (int vv = 0; vv < 2; ++vv)
@@ -276,6 +274,8 @@ __device__ __forceinline__ void ld_fac(const double* __restrict__ fac, int k, in
 
 // ============================================================================ baroclinic head r
 // internal3d.py:327-405 + columns.py:95-122.  FROM_T: rho' = -alpha (T - t_ref) inline.
+// Volume term in closed form: -g J2D sum_v VS[v][lev] (grad_iso(v) (MHQ Jz)_a - mid2(v) (MHQ drho/dzeta)_a)
+// (meas * m_h = -J2D mid2 cancels the 1/Jz of the metric); lateral {Jz} = (f_b - f_t)/2 {H}.
 template <bool FROM_T>
 __global__ void __launch_bounds__(128) k_compute_r(DMesh m, const double* __restrict__ eta_g,
                                                    const double* __restrict__ rhoT, double alpha, double tref,
@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(128) k_compute_r(DMesh m, const double* __rest
   double prevb[3] = {0, 0, 0};
   for (int l = 0; l < L; ++l) {
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    const double jm = 0.5 * (fb - ft);
     LGeo G;
     layer_geo(C, eta, ft, fb, G);
     double rho[6];
@@ -306,41 +307,32 @@ __global__ void __launch_bounds__(128) k_compute_r(DMesh m, const double* __rest
 #pragma unroll
       for (int n = 0; n < 6; ++n) rho[n] = -alpha * (rho[n] - tref);
     }
-    double jzq[6];
-    hq(G.jz, jzq);
-    double acc[2][6] = {{0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}};
-    // volume: -g <phi grad_h(rho) J2D Jz>, grad_h = iso part + m_h d/dzeta  (meas * m_h = -J2D mid2)
+    double acc[2][6];
     {
-      double gi[2][2];
+      double gi[2][2], A[3], B[3], dzn[3];
 #pragma unroll
       for (int lev = 0; lev < 2; ++lev) {
         gi[lev][0] = (rho[3 * lev] * C.dx[0] + rho[3 * lev + 1] * C.dx[1]) + rho[3 * lev + 2] * C.dx[2];
         gi[lev][1] = (rho[3 * lev] * C.dy[0] + rho[3 * lev + 1] * C.dy[1]) + rho[3 * lev + 2] * C.dy[2];
       }
-      double rt[6], rb[6];
-      hq(rho, rt);
-      hq(rho + 3, rb);
 #pragma unroll
-      for (int vv = 0; vv < 2; ++vv) {
-        double gv[2], mid2[2];
+      for (int a = 0; a < 3; ++a) dzn[a] = 0.5 * (rho[a] - rho[3 + a]);
+      mhq_vec(G.jz, A);
+      mhq_vec(dzn, B);
 #pragma unroll
-        for (int d = 0; d < 2; ++d) {
-          gv[d] = VS[vv][0] * gi[0][d] + VS[vv][1] * gi[1][d];
-          mid2[d] = G.dzmid[d] + ZQP[vv] * G.djz[d];
+      for (int d = 0; d < 2; ++d) {
+        double t[2][3];
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv) {
+          const double gv = VS[vv][0] * gi[0][d] + VS[vv][1] * gi[1][d];
+          const double md = d == 0 ? G.dzmid[0] + ZQP[vv] * G.djz[0] : G.dzmid[1] + ZQP[vv] * G.djz[1];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) t[vv][a] = gv * A[a] - md * B[a];
         }
 #pragma unroll
-        for (int qq = 0; qq < 6; ++qq) {
-          const double dzr = 0.5 * (rt[qq] - rb[qq]);
-          const double wj = QW[qq] * j2d;
+        for (int lev = 0; lev < 2; ++lev)
 #pragma unroll
-          for (int d = 0; d < 2; ++d) {
-            const double t = g * (wj * jzq[qq] * gv[d] - wj * mid2[d] * dzr);
-#pragma unroll
-            for (int lev = 0; lev < 2; ++lev)
-#pragma unroll
-              for (int a = 0; a < 3; ++a) acc[d][3 * lev + a] -= VS[vv][lev] * BARY[qq][a] * t;
-          }
-        }
+          for (int a = 0; a < 3; ++a) acc[d][3 * lev + a] = -(g * j2d) * (VS[0][lev] * t[0][a] + VS[1][lev] * t[1][a]);
       }
     }
     // interior horizontal face above this layer: 2g J2D (-grad z_face) . int phi [[rho]]
@@ -360,29 +352,21 @@ __global__ void __launch_bounds__(128) k_compute_r(DMesh m, const double* __rest
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if (C.tag[k] != 0) continue;
-      double n4[4], ti[2][2], te[2][2];
+      double n4[4], dj[2][2];
       ld_nb4(rhoT, E[k].k2, E[k].e2, l, L, nt, n4);
       if (FROM_T) {
 #pragma unroll
         for (int n = 0; n < 4; ++n) n4[n] = -alpha * (n4[n] - tref);
       }
-      tr_own(rho, k, ti);
-      tr_nb(n4, te);
-      double j0, j1, a2[2], b2[2], ja[2][2], jb[2][2];
-      nb_jz(E[k], ft, fb, j0, j1);
-      tr2_own(G.jz, k, a2);
-      tr2_nb(j0, j1, b2);
-      tr_dup(a2, ja);
-      tr_dup(b2, jb);
+      tr_jump(rho, k, n4, dj);
       double xx[2][2], xy[2][2];
 #pragma unroll
       for (int vv = 0; vv < 2; ++vv)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const double drh = 0.5 * (ti[vv][h] - te[vv][h]);
-          const double jm = 0.5 * (ja[vv][h] + jb[vv][h]);
-          xx[vv][h] = C.nx[k] * drh * jm;
-          xy[vv][h] = C.ny[k] * drh * jm;
+          const double x = dj[vv][h] * (jm * E[k].hm[h]);
+          xx[vv][h] = C.nx[k] * x;
+          xy[vv][h] = C.ny[k] * x;
         }
       const double je = 0.5 * C.el[k];
       lat_add(acc[0], k, xx, g * je);
@@ -579,7 +563,8 @@ __global__ void __launch_bounds__(128) k_compute_w(DMesh m, const double* __rest
 }
 
 // ============================================================================ w~ (API + fused)
-// internal3d.py:505-541.  FUSED: qbar = q + Jz mis and its factor rebuilt on the fly.
+// internal3d.py:505-541.  FUSED: qbar = q + Jz mis and its factor rebuilt on the fly (Jz mis =
+// jm * (H mis) on sigma layers).  Iso volume moment in closed form: S[m] = sum_l K[m][l] W1 . q_l.
 template <bool FUSED>
 __global__ void __launch_bounds__(128) k_compute_wtilde(DMesh m, const double* __restrict__ eta_g,
                                                         const double* __restrict__ qb, const double* __restrict__ fac,
@@ -594,19 +579,19 @@ __global__ void __launch_bounds__(128) k_compute_wtilde(DMesh m, const double* _
   double eta[3];
   load_eta(eta_g, c, nt, eta);
   EdgeNb E[3];
-  double mo[2][3], mn[3][2][2];  // own mismatch, neighbour mismatch at its edge corners
+  double mo[2][3], mn[3][2][2];  // H * mismatch: own corners, neighbour edge corners
   if (FUSED) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       edge_setup(m, C, eta, eta_g, k, g, E[k]);
-      mo[0][k] = mis[k * nt + c];
-      mo[1][k] = mis[(3 + k) * nt + c];
+      mo[0][k] = mis[k * nt + c] * (eta[k] - C.b[k]);
+      mo[1][k] = mis[(3 + k) * nt + c] * (eta[k] - C.b[k]);
       if (C.tag[k] == 0) {
         const int e2 = E[k].e2, k2 = E[k].k2;
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          mn[k][cc][0] = mis[(cc * 3 + EV0(k2)) * nt + e2];
-          mn[k][cc][1] = mis[(cc * 3 + EV1(k2)) * nt + e2];
+          mn[k][cc][0] = mis[(cc * 3 + EV0(k2)) * nt + e2] * E[k].hn[0];
+          mn[k][cc][1] = mis[(cc * 3 + EV1(k2)) * nt + e2] * E[k].hn[1];
         }
       }
     }
@@ -614,35 +599,29 @@ __global__ void __launch_bounds__(128) k_compute_wtilde(DMesh m, const double* _
   const double j2d = C.j2d;
   double s[3] = {0, 0, 0};
   for (int l = L - 1; l >= 0; --l) {
-    const double ft = m.fracs[l], fb = m.fracs[l + 1];
-    double qv[2][6], jz[3];
+    const double jm = 0.5 * (m.fracs[l + 1] - m.fracs[l]);
+    double qv[2][6];
     ld6(qb, l, c, L, nt, qv[0]);
     ld6(qb + P6, l, c, L, nt, qv[1]);
     if (FUSED) {
-      layer_jz(C.b, eta, ft, fb, jz);
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jz[n % 3] * mo[cc][n % 3];
+        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jm * mo[cc][n % 3];
     }
     double acc[6] = {0, 0, 0, 0, 0, 0};
     {
-      double qp[2][2][6];
-      at_pts(qv[0], qp[0]);
-      at_pts(qv[1], qp[1]);
+      double wq[2][2];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev)
+          wq[cc][lev] = W1[0] * qv[cc][3 * lev] + W1[1] * qv[cc][3 * lev + 1] + W1[2] * qv[cc][3 * lev + 2];
       double S[2][2];
 #pragma unroll
       for (int mm = 0; mm < 2; ++mm) {
-        double sx = 0.0, sy = 0.0;
-#pragma unroll
-        for (int vv = 0; vv < 2; ++vv)
-#pragma unroll
-          for (int qq = 0; qq < 6; ++qq) {
-            sx += QW[qq] * VS[vv][mm] * qp[0][vv][qq];
-            sy += QW[qq] * VS[vv][mm] * qp[1][vv][qq];
-          }
-        S[mm][0] = sx;
-        S[mm][1] = sy;
+        S[mm][0] = KM[mm][0] * wq[0][0] + KM[mm][1] * wq[0][1];
+        S[mm][1] = KM[mm][0] * wq[1][0] + KM[mm][1] * wq[1][1];
       }
       iso_add(C, S, acc);
     }
@@ -651,18 +630,17 @@ __global__ void __launch_bounds__(128) k_compute_wtilde(DMesh m, const double* _
       if (C.tag[k] != 0) continue;
       double f[2][2];
       if (FUSED) {
-        double qn[2][4], jn0, jn1;
+        double qn[2][4];
         ld_nb4(qb, E[k].k2, E[k].e2, l, L, nt, qn[0]);
         ld_nb4(qb + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
-        nb_jz(E[k], ft, fb, jn0, jn1);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          qn[cc][0] = qn[cc][0] + jn0 * mn[k][cc][0];
-          qn[cc][1] = qn[cc][1] + jn1 * mn[k][cc][1];
-          qn[cc][2] = qn[cc][2] + jn0 * mn[k][cc][0];
-          qn[cc][3] = qn[cc][3] + jn1 * mn[k][cc][1];
+          qn[cc][0] = qn[cc][0] + jm * mn[k][cc][0];
+          qn[cc][1] = qn[cc][1] + jm * mn[k][cc][1];
+          qn[cc][2] = qn[cc][2] + jm * mn[k][cc][0];
+          qn[cc][3] = qn[cc][3] + jm * mn[k][cc][1];
         }
-        lat_factor(C, E[k], k, jz, eta, ft, fb, qv, qn, f);
+        lat_factor(C, E[k], k, jm, qv, qn, f);
       } else {
         ld_fac(fac, k, l, c, L, nt, f);
       }
@@ -706,6 +684,31 @@ struct HArgs {
   int mass_terms;
 };
 
+__device__ __forceinline__ void mjz(const double jz[3], double M[3][3]) {
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = p; q < 3; ++q) {
+      const double s = T3[p][q][0] * jz[0] + T3[p][q][1] * jz[1] + T3[p][q][2] * jz[2];
+      M[p][q] = s;
+      M[q][p] = s;
+    }
+}
+// y = (K (x) J2D Mjz) x  -- the prism mass of internal3d.py:114-123 applied in Kronecker form
+__device__ __forceinline__ void kron_apply(const double M[3][3], double j2d, const double x[6], double y[6]) {
+  double h0[3], h1[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    h0[a] = j2d * (M[a][0] * x[0] + M[a][1] * x[1] + M[a][2] * x[2]);
+    h1[a] = j2d * (M[a][0] * x[3] + M[a][1] * x[4] + M[a][2] * x[5]);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    y[a] = KM[0][0] * h0[a] + KM[0][1] * h1[a];
+    y[3 + a] = KM[1][0] * h0[a] + KM[1][1] * h1[a];
+  }
+}
+
 template <int NC, int MODE>
 __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -717,22 +720,24 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
   double eta[3];
   load_eta(a.eta_u, c, nt, eta);
   EdgeNb E[3];
-  double mo[2][3], mn[3][2][2];
+  double mo[2][3], mn[3][2][2];   // H * mismatch (STAGE)
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    if (MODE != 0) edge_setup(m, C, eta, a.eta_u, k, a.g, E[k]);
-    else {
+    if (MODE != 0) {
+      edge_setup(m, C, eta, a.eta_u, k, a.g, E[k]);
+    } else {
       E[k].e2 = C.nb[k];
       E[k].k2 = C.nk[k];
     }
     if (MODE == 2) {
-      mo[0][k] = a.mis[k * nt + c];
-      mo[1][k] = a.mis[(3 + k) * nt + c];
+      const double H = eta[k] - C.b[k];
+      mo[0][k] = a.mis[k * nt + c] * H;
+      mo[1][k] = a.mis[(3 + k) * nt + c] * H;
       if (C.tag[k] == 0) {
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          mn[k][cc][0] = a.mis[(cc * 3 + EV0(E[k].k2)) * nt + E[k].e2];
-          mn[k][cc][1] = a.mis[(cc * 3 + EV1(E[k].k2)) * nt + E[k].e2];
+          mn[k][cc][0] = a.mis[(cc * 3 + EV0(E[k].k2)) * nt + E[k].e2] * E[k].hn[0];
+          mn[k][cc][1] = a.mis[(cc * 3 + EV1(E[k].k2)) * nt + E[k].e2] * E[k].hn[1];
         }
       }
     }
@@ -758,8 +763,7 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
     for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
   for (int l = 0; l < L; ++l) {
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
-    double jz[3];
-    layer_jz(C.b, eta, ft, fb, jz);
+    const double jm = 0.5 * (fb - ft);
     double u[NC][6], qv[2][6];
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) ld6(a.u + cc * P6, l, c, L, nt, u[cc]);
@@ -769,24 +773,36 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jz[n % 3] * mo[cc][n % 3];
+        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jm * mo[cc][n % 3];
     }
     double acc[NC][6];
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-      for (int n = 0; n < 6; ++n) acc[cc][n] = 0.0;
-    // volume advection: J2D grad_h(phi_h) . sum_vq W phi_z u (q . )
+    // volume advection J2D grad_h(phi_h) . <phi_z u q>: bilinear closed form
     {
-      double qp[2][2][6];
-      at_pts(qv[0], qp[0]);
-      at_pts(qv[1], qp[1]);
+      double z[2][2][3];   // MHQ q_{d, level}
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev) mhq_vec(qv[d] + 3 * lev, z[d][lev]);
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
-        double up[2][6], S[2][2];
-        at_pts(u[cc], up);
-        adv_moment(up, qp[0], qp[1], S);
-        iso_add(C, S, acc[cc]);
+        double S[2][2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          double dot[2][2];
+#pragma unroll
+          for (int l1 = 0; l1 < 2; ++l1)
+#pragma unroll
+            for (int l2 = 0; l2 < 2; ++l2)
+              dot[l1][l2] = u[cc][3 * l1] * z[d][l2][0] + u[cc][3 * l1 + 1] * z[d][l2][1] + u[cc][3 * l1 + 2] * z[d][l2][2];
+#pragma unroll
+          for (int mm = 0; mm < 2; ++mm)
+            S[mm][d] = K3[mm][0][0] * dot[0][0] + K3[mm][0][1] * dot[0][1] + K3[mm][1][0] * dot[1][0] +
+                       K3[mm][1][1] * dot[1][1];
+        }
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+          for (int p = 0; p < 3; ++p) acc[cc][3 * lev + p] = j2d * (C.dx[p] * S[lev][0] + C.dy[p] * S[lev][1]);
       }
     }
     // lateral upwind flux on interior faces
@@ -801,17 +817,15 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
         ld_nb4(a.qa, E[k].k2, E[k].e2, l, L, nt, qn[0]);
         ld_nb4(a.qa + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
         if (MODE == 2) {
-          double jn0, jn1;
-          nb_jz(E[k], ft, fb, jn0, jn1);
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
-            qn[cc][0] = qn[cc][0] + jn0 * mn[k][cc][0];
-            qn[cc][1] = qn[cc][1] + jn1 * mn[k][cc][1];
-            qn[cc][2] = qn[cc][2] + jn0 * mn[k][cc][0];
-            qn[cc][3] = qn[cc][3] + jn1 * mn[k][cc][1];
+            qn[cc][0] = qn[cc][0] + jm * mn[k][cc][0];
+            qn[cc][1] = qn[cc][1] + jm * mn[k][cc][1];
+            qn[cc][2] = qn[cc][2] + jm * mn[k][cc][0];
+            qn[cc][3] = qn[cc][3] + jm * mn[k][cc][1];
           }
         }
-        lat_factor(C, E[k], k, jz, eta, ft, fb, qv, qn, f);
+        lat_factor(C, E[k], k, jm, qv, qn, f);
       }
       const double je = -(0.5 * C.el[k]);
 #pragma unroll
@@ -827,51 +841,60 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
         lat_add(acc[cc], k, x, je);
       }
     }
-    // Coriolis f M (u_y, -u_x) and -M r / rho0   (momentum)
-    if constexpr (NC == 2) if (MODE != 0 || a.mass_terms) {
-      double mu[2][6], mr[2][6];
-      double rr[2][6];
-      ld6(a.r, l, c, L, nt, rr[0]);
-      ld6(a.r + P6, l, c, L, nt, rr[1]);
-      if (MODE == 0) {
-        double M[6][6];
+    double Mu[3][3];
+    bool have_mu = false;
+    // Coriolis f M (u_y, -u_x) and -M r / rho0 (momentum), internal3d.py:746-750
+    if constexpr (NC == 2) {
+      if (MODE != 0 || a.mass_terms) {
+        double rr[2][6];
+        ld6(a.r, l, c, L, nt, rr[0]);
+        ld6(a.r + P6, l, c, L, nt, rr[1]);
+        if (MODE == 0) {
+          double M[6][6];
 #pragma unroll
-        for (int p = 0; p < 6; ++p)
+          for (int p = 0; p < 6; ++p)
 #pragma unroll
-          for (int s = 0; s < 6; ++s) M[p][s] = a.mass[((size_t)(p * 6 + s) * L + l) * nt + c];
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc)
+            for (int q = 0; q < 6; ++q) M[p][q] = a.mass[((size_t)(p * 6 + q) * L + l) * nt + c];
 #pragma unroll
           for (int p = 0; p < 6; ++p) {
-            double t0 = 0.0, t1 = 0.0;
+            double mu0 = 0, mu1 = 0, mr0 = 0, mr1 = 0;
 #pragma unroll
-            for (int s = 0; s < 6; ++s) {
-              t0 += M[p][s] * u[cc][s];
-              t1 += M[p][s] * rr[cc][s];
+            for (int q = 0; q < 6; ++q) {
+              mu0 += M[p][q] * u[0][q];
+              mu1 += M[p][q] * u[1][q];
+              mr0 += M[p][q] * rr[0][q];
+              mr1 += M[p][q] * rr[1][q];
             }
-            mu[cc][p] = t0;
-            mr[cc][p] = t1;
+            if (a.f != 0.0) {
+              acc[0][p] += a.f * mu1;
+              acc[1][p] -= a.f * mu0;
+            }
+            acc[0][p] -= mr0 / a.rho0;
+            acc[1][p] -= mr1 / a.rho0;
           }
-      } else {
-        double jzq[6], Mh[3][3];
-        hq(jz, jzq);
-        mass_h(jzq, Mh);
+        } else {
+          double jz[3];
+          layer_jz(C.b, eta, ft, fb, jz);
+          mjz(jz, Mu);
+          have_mu = true;
+          const double ir = 1.0 / a.rho0;
+          double y0[6], y1[6], m0[6], m1[6];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          mass_apply_k(Mh, j2d, u[cc], mu[cc]);
-          mass_apply_k(Mh, j2d, rr[cc], mr[cc]);
-        }
-      }
+          for (int n = 0; n < 6; ++n) {
+            y0[n] = a.f * u[1][n] - rr[0][n] * ir;
+            y1[n] = -a.f * u[0][n] - rr[1][n] * ir;
+          }
+          kron_apply(Mu, j2d, y0, m0);
+          kron_apply(Mu, j2d, y1, m1);
 #pragma unroll
-      for (int n = 0; n < 6; ++n) {
-        if (a.f != 0.0) {
-          acc[0][n] += a.f * mu[1][n];
-          acc[1][n] -= a.f * mu[0][n];
+          for (int n = 0; n < 6; ++n) {
+            acc[0][n] += m0[n];
+            acc[1][n] += m1[n];
+          }
         }
-        acc[0][n] -= mr[0][n] / a.rho0;
-        acc[1][n] -= mr[1][n] / a.rho0;
       }
     }
+    (void)have_mu;
     // surface wind and bottom drag (internal3d.py:919-934)
     if constexpr (NC == 2 && MODE != 0) {
       if (l == 0) {
@@ -905,28 +928,31 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
 #pragma unroll
         for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
     } else if (MODE == 2) {
-      double j0[3], j1[3], q0[6], q1[6], M0h[3][3], M1h[3][3];
+      double j0[3], M0[3][3];
       layer_jz(C.b, eta0, ft, fb, j0);
-      layer_jz(C.b, eta1, ft, fb, j1);
-      hq(j0, q0);
-      hq(j1, q1);
-      mass_h(q0, M0h);
-      mass_h(q1, M1h);
+      mjz(j0, M0);
+      double mf[2][3];
+      if constexpr (NC == 2) {
+        double j1[3], M1[3][3];
+        layer_jz(C.b, eta1, ft, fb, j1);
+        mjz(j1, M1);
+        const double kk = (KM[0][0] + KM[0][1]) * j2d;   // F2D/H1 is the same on both levels
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int p = 0; p < 3; ++p) mf[cc][p] = kk * (M1[p][0] * F1[cc][0] + M1[p][1] * F1[cc][1] + M1[p][2] * F1[cc][2]);
+      }
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double x0[6], m0x[6], o[6];
         ld6(a.u0 + cc * P6, l, c, L, nt, x0);
-        mass_apply_k(M0h, j2d, x0, m0x);
-        if constexpr (NC == 2) {
-          double F6[6], m1f[6];
+        kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
-          for (int n = 0; n < 6; ++n) F6[n] = F1[cc][n % 3];
-          mass_apply_k(M1h, j2d, F6, m1f);
-#pragma unroll
-          for (int n = 0; n < 6; ++n) o[n] = m0x[n] + a.dt * (acc[cc][n] + m1f[n]);
-        } else {
-#pragma unroll
-          for (int n = 0; n < 6; ++n) o[n] = m0x[n] + a.dt * acc[cc][n];
+        for (int n = 0; n < 6; ++n) {
+          if constexpr (NC == 2)
+            o[n] = m0x[n] + a.dt * (acc[cc][n] + mf[cc][n % 3]);
+          else
+            o[n] = m0x[n] + a.dt * acc[cc][n];
         }
         st6(out + cc * P6, l, c, L, nt, o);
       }
@@ -936,7 +962,6 @@ __global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double*
     }
   }
   if (MODE == 1) {
-    // (Fh + st) column sum -> [NC][3][nt]
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
