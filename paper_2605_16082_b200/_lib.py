@@ -29,6 +29,7 @@ _SIGS = {
     "pdg_last_error": (I, [P, P, ctypes.POINTER(I), ctypes.POINTER(LL), ctypes.POINTER(LL), ctypes.POINTER(D)]),
     "pdg_cuda_error_string": (ctypes.c_char_p, []),
     "pdg_launch_count": (LL, [P]),
+    "pdg_tune": (I, [I, I]),
     "pdg_ext2d_eval": (I, [P, P, P, P, P, P, P, I, D, D, D, P, I, I, P, P, P, P]),
     "pdg_ext2d_subcycle": (I, [P, P, I, D, D, D, P, P, P, P, P, P, I, P]),
     "pdg_ext2d_cfl": (I, [P, P, D, D, P, P]),

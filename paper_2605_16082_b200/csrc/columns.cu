@@ -647,8 +647,8 @@ __device__ __forceinline__ void lu6r_solve(const double a[6][6], const double rp
 // IMPLICIT: (M1 - dt A) x = rhs by block Thomas (columns.py:292-348 order) with the layer blocks
 // assembled in registers; only the propagation tile G_l (36) is kept (workspace) for the back
 // substitution; the reduced RHS g_l is parked in x.  x may alias rhs.
-template <int NC>
-__global__ void __launch_bounds__(128) k_vimplicit(DMesh m, VopArgs a, double dt, const double* rhs,
+template <int NC, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, double dt, const double* rhs,
                                                    double* __restrict__ Gs, double* x) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
@@ -789,8 +789,8 @@ __global__ void __launch_bounds__(128) k_vimplicit(DMesh m, VopArgs a, double dt
 }
 
 // EXPLICIT: x = M1^-1 (rhs + dt A xin), A applied matrix free; M1^-1 = K^-1 (x) (J2D Mjz)^-1.
-template <int NC>
-__global__ void __launch_bounds__(128) k_vexplicit(DMesh m, VopArgs a, double dt, const double* rhs,
+template <int NC, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, double dt, const double* rhs,
                                                    const double* __restrict__ xin, double* x) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
@@ -895,6 +895,13 @@ __global__ void __launch_bounds__(128) k_vexplicit(DMesh m, VopArgs a, double dt
 
 using namespace pdg;
 
+#define DISPATCH_MINB(key, KERNEL, ...)                                          \
+  switch (tune_get(key)) {                                                      \
+    case 3: KERNEL<__VA_ARGS__, 3><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
+    case 4: KERNEL<__VA_ARGS__, 4><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
+    default: KERNEL<__VA_ARGS__, 1><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
+  }
+
 extern "C" {
 
 int pdg_solve_sweep(int kind, int ncol, int L, int nc, const double* rhs, const double* j2d, const int* layers,
@@ -963,21 +970,27 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
                       double dt, const double* rhs, const double* xin, double* x, void* stream) {
   VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, kh, kv, n0, order};
   const int nt = ctx->nt;
-  const dim3 g(nblocks(nt, 128)), b(128);
-  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 grid(nblocks(nt, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
   if (implicit) {
     double* Gs = ctx->ws3((size_t)36 * ctx->L * nt);
     if (!Gs) return PDG_ERR_CUDA;
-    if (ncomp == 2)
-      k_vimplicit<2><<<g, b, 0, s>>>(m, a, dt, rhs, Gs, x);
-    else
-      k_vimplicit<1><<<g, b, 0, s>>>(m, a, dt, rhs, Gs, x);
+#define LAUNCH_ARGS m, a, dt, rhs, Gs, x
+    if (ncomp == 2) {
+      DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 2)
+    } else {
+      DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 1)
+    }
+#undef LAUNCH_ARGS
   } else {
-    if (ncomp == 2)
-      k_vexplicit<2><<<g, b, 0, s>>>(m, a, dt, rhs, xin, x);
-    else
-      k_vexplicit<1><<<g, b, 0, s>>>(m, a, dt, rhs, xin, x);
+#define LAUNCH_ARGS m, a, dt, rhs, xin, x
+    if (ncomp == 2) {
+      DISPATCH_MINB(TUNE_VEXPL, k_vexplicit, 2)
+    } else {
+      DISPATCH_MINB(TUNE_VEXPL, k_vexplicit, 1)
+    }
+#undef LAUNCH_ARGS
   }
   return check_launch(ctx);
 }

@@ -6,6 +6,11 @@
 #include "ctx.cuh"
 
 static thread_local char g_errbuf[512] = "";
+static int g_tune[pdg::TUNE_NKEYS] = {1, 1, 1, 4, 1, 1, 1, 1};  // measured: scripts/tune.py
+
+namespace pdg {
+int tune_get(int key) { return (key >= 0 && key < TUNE_NKEYS) ? g_tune[key] : 1; }
+}  // namespace pdg
 static long long g_noctx_launches = 0;
 
 namespace pdg {
@@ -120,6 +125,13 @@ int pdg_last_error(pdg_ctx* c, void* stream, int* code, long long* i0, long long
 }
 
 const char* pdg_cuda_error_string(void) { return g_errbuf; }
+
+int pdg_tune(int key, int value) {
+  if (key < 0 || key >= pdg::TUNE_NKEYS) return PDG_ERR_SHAPE;
+  int old = g_tune[key];
+  if (value > 0) g_tune[key] = value;
+  return old;
+}
 
 long long pdg_launch_count(pdg_ctx* c) { return c ? c->launches : g_noctx_launches; }
 

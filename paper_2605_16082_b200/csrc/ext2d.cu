@@ -128,7 +128,7 @@ __device__ __forceinline__ void ext2d_residual(const DMesh& m, const Col& C, int
     for (int h = 0; h < 2; ++h) {
       const double hi = ei[h] - bi[h], he = ee[h] - be[h];
       if (hi <= 0.0 || he <= 0.0) report(m.err, PDG_ERR_DRY, -1, 0, fmin(hi, he));
-      const double cel = fmax(sqrt(g * hi), sqrt(g * he));
+      const double cel = sqrt(g * fmax(hi, he));   // == max(sqrt(g hi), sqrt(g he)) exactly
       const double fe = nx * 0.5 * (xi[h] + xe[h]) + ny * 0.5 * (yi[h] + ye[h]) + cel * 0.5 * (ei[h] - ee[h]);
       const double hm = 0.5 * (hi + he);
       const double de = 0.5 * (ei[h] - ee[h]);
@@ -193,7 +193,7 @@ __global__ void k_ext2d_eval(DMesh m, Ext2DIn a, const int* __restrict__ els, in
 // one SSP-RK3 stage: X = state evaluated, S0 = substep start (3 fields x C3), Y = output.
 // STAGE 0: Y = S0 + dt d(X);  1: Y = 3/4 S0 + 1/4 (X + dt d);  2: Y = S0/3 + 2/3 (X + dt d), qbar += Y.q
 template <int STAGE>
-__global__ void __launch_bounds__(256) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
+__global__ void __launch_bounds__(256, 2) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
                                                   double* Y, double dt, double* __restrict__ qbar) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;

@@ -276,8 +276,8 @@ __device__ __forceinline__ void ld_fac(const double* __restrict__ fac, int k, in
 // internal3d.py:327-405 + columns.py:95-122.  FROM_T: rho' = -alpha (T - t_ref) inline.
 // Volume term in closed form: -g J2D sum_v VS[v][lev] (grad_iso(v) (MHQ Jz)_a - mid2(v) (MHQ drho/dzeta)_a)
 // (meas * m_h = -J2D mid2 cancels the 1/Jz of the metric); lateral {Jz} = (f_b - f_t)/2 {H}.
-template <bool FROM_T>
-__global__ void __launch_bounds__(128) k_compute_r(DMesh m, const double* __restrict__ eta_g,
+template <bool FROM_T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* __restrict__ eta_g,
                                                    const double* __restrict__ rhoT, double alpha, double tref,
                                                    double g, Cols cs, double* __restrict__ r) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -565,8 +565,8 @@ __global__ void __launch_bounds__(128) k_compute_w(DMesh m, const double* __rest
 // ============================================================================ w~ (API + fused)
 // internal3d.py:505-541.  FUSED: qbar = q + Jz mis and its factor rebuilt on the fly (Jz mis =
 // jm * (H mis) on sigma layers).  Iso volume moment in closed form: S[m] = sum_l K[m][l] W1 . q_l.
-template <bool FUSED>
-__global__ void __launch_bounds__(128) k_compute_wtilde(DMesh m, const double* __restrict__ eta_g,
+template <bool FUSED, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_compute_wtilde(DMesh m, const double* __restrict__ eta_g,
                                                         const double* __restrict__ qb, const double* __restrict__ fac,
                                                         const double* __restrict__ mis, double g, Cols cs,
                                                         double* __restrict__ w) {
@@ -709,8 +709,8 @@ __device__ __forceinline__ void kron_apply(const double M[3][3], double j2d, con
   }
 }
 
-template <int NC, int MODE>
-__global__ void __launch_bounds__(128) k_hrhs(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
+template <int NC, int MODE, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cs.n) return;
   const int c = cs.col(i), nt = m.nt, L = m.L;
@@ -1044,6 +1044,13 @@ __global__ void k_stress(DMesh m, const double* __restrict__ ux, const double* _
 // ============================================================================ C ABI
 using namespace pdg;
 
+#define DISPATCH_MINB(key, KERNEL, ...)                                     \
+  switch (tune_get(key)) {                                                 \
+    case 3: KERNEL<__VA_ARGS__, 3><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
+    case 4: KERNEL<__VA_ARGS__, 4><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
+    default: KERNEL<__VA_ARGS__, 1><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
+  }
+
 #define COLS(els, n) Cols{els, (els) ? (n) : ctx->nt}
 #define GRID1(nn) nblocks((nn), 128), 128, 0, (cudaStream_t)stream
 
@@ -1104,10 +1111,15 @@ int pdg_compute_r(pdg_ctx* ctx, const double* eta_g, const double* rho_or_T, int
                   double g, const int* els, int n_els, double* r, void* stream) {
   Cols cs = COLS(els, n_els);
   if (cs.n == 0) return PDG_OK;
-  if (from_T)
-    k_compute_r<true><<<GRID1(cs.n)>>>(ctx->view(), eta_g, rho_or_T, alpha, tref, g, cs, r);
-  else
-    k_compute_r<false><<<GRID1(cs.n)>>>(ctx->view(), eta_g, rho_or_T, alpha, tref, g, cs, r);
+  const dim3 grid(nblocks(cs.n, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
+#define LAUNCH_ARGS ctx->view(), eta_g, rho_or_T, alpha, tref, g, cs, r
+  if (from_T) {
+    DISPATCH_MINB(TUNE_R, k_compute_r, true)
+  } else {
+    DISPATCH_MINB(TUNE_R, k_compute_r, false)
+  }
+#undef LAUNCH_ARGS
   return check_launch(ctx);
 }
 
@@ -1123,10 +1135,15 @@ int pdg_compute_wtilde(pdg_ctx* ctx, const double* eta_g, const double* qb, cons
                        double g, const int* els, int n_els, double* w, void* stream) {
   Cols cs = COLS(els, n_els);
   if (cs.n == 0) return PDG_OK;
-  if (mis)
-    k_compute_wtilde<true><<<GRID1(cs.n)>>>(ctx->view(), eta_g, qb, nullptr, mis, g, cs, w);
-  else
-    k_compute_wtilde<false><<<GRID1(cs.n)>>>(ctx->view(), eta_g, qb, fac, nullptr, g, cs, w);
+  const dim3 grid(nblocks(cs.n, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
+#define LAUNCH_ARGS ctx->view(), eta_g, qb, fac, mis, g, cs, w
+  if (mis) {
+    DISPATCH_MINB(TUNE_WT, k_compute_wtilde, true)
+  } else {
+    DISPATCH_MINB(TUNE_WT, k_compute_wtilde, false)
+  }
+#undef LAUNCH_ARGS
   return check_launch(ctx);
 }
 
@@ -1147,9 +1164,9 @@ int pdg_horizontal_rhs(pdg_ctx* ctx, const double* eta_g, const double* u, int n
   a.rho0 = rho0;
   a.mass_terms = mass_terms;
   if (ncomp == 2)
-    k_hrhs<2, 0><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+    k_hrhs<2, 0, 1><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
   else
-    k_hrhs<1, 0><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+    k_hrhs<1, 0, 1><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
   return check_launch(ctx);
 }
 
@@ -1184,7 +1201,11 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   a.tsy = tsy;
   a.cd = cd;
   Cols cs{nullptr, ctx->nt};
-  k_hrhs<2, 1><<<GRID1(cs.n)>>>(ctx->view(), a, cs, f3d2d);
+  const dim3 grid(nblocks(cs.n, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
+#define LAUNCH_ARGS ctx->view(), a, cs, f3d2d
+  DISPATCH_MINB(TUNE_HRHS, k_hrhs, 2, 1)
+#undef LAUNCH_ARGS
   return check_launch(ctx);
 }
 
@@ -1212,10 +1233,15 @@ int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta
   a.cd = cd;
   a.dt = dt;
   Cols cs{nullptr, ctx->nt};
-  if (ncomp == 2)
-    k_hrhs<2, 2><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
-  else
-    k_hrhs<1, 2><<<GRID1(cs.n)>>>(ctx->view(), a, cs, out);
+  const dim3 grid(nblocks(cs.n, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
+#define LAUNCH_ARGS ctx->view(), a, cs, out
+  if (ncomp == 2) {
+    DISPATCH_MINB(TUNE_HRHS, k_hrhs, 2, 2)
+  } else {
+    DISPATCH_MINB(TUNE_HRHS, k_hrhs, 1, 2)
+  }
+#undef LAUNCH_ARGS
   return check_launch(ctx);
 }
 
