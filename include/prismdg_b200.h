@@ -73,6 +73,9 @@ int pdg_ctx_create(const pdg_mesh_desc* mesh, int device, pdg_ctx** out);
 int pdg_ctx_destroy(pdg_ctx* ctx);
 /* sigma fractions (L+1 host doubles, mesh.py:389) -- np.linspace(0, 1, L+1) */
 int pdg_ctx_set_layers(pdg_ctx* ctx, int L, const double* fracs);
+/* partitioned runs: columns 0..nown-1 are owned (computed), nown..nt-1 are ghost columns whose
+ * values arrive by halo exchange.  Default nown = nt. */
+int pdg_ctx_set_owned(pdg_ctx* ctx, int nown);
 /* synchronises `stream`, returns and clears the first recorded device error */
 int pdg_last_error(pdg_ctx* ctx, void* stream, int* code, long long* i0, long long* i1, double* val);
 const char* pdg_cuda_error_string(void);
@@ -97,6 +100,16 @@ int pdg_ext2d_eval(pdg_ctx* ctx, const double* eta, const double* qx, const doub
 int pdg_ext2d_subcycle(pdg_ctx* ctx, double* state, int m, double dt, double g, double rho0, const double* f3d2d,
                        const double* source, const double* patm, const double* bc_vals, double* qbar, double* f2d,
                        int check_cfl, void* stream);
+/* the same sub-cycle one RK stage at a time, so a partitioned run can exchange the stage state
+ * (halo) between stages: begin (CFL check, Q0 copy, Qbar = 0), rk_stage(0|1|2), end (Qbar /= m, F2D) */
+int pdg_ext2d_subcycle_begin(pdg_ctx* ctx, const double* state, double g, double dt, int check_cfl, double* qbar,
+                             void* stream);
+/* stage 0: Y = S0 + dt d(X); 1: Y = 3/4 S0 + 1/4 (X + dt d(X)); 2: Y = S0/3 + 2/3 (X + dt d(X)), qbar += Y.Q */
+int pdg_ext2d_rk_stage(pdg_ctx* ctx, int stage, const double* X, const double* S0, double* Y, double dt, double g,
+                       double rho0, const double* f3d2d, const double* source, const double* patm, int has_bc,
+                       double eta_bc, double* qbar, void* stream);
+int pdg_ext2d_subcycle_end(pdg_ctx* ctx, const double* state, const double* f3d2d, int m, double dt, double* qbar,
+                           double* f2d, void* stream);
 /* check_cfl on device; writes the ratio to ratio_dev[0] (device) and the error word */
 int pdg_ext2d_cfl(pdg_ctx* ctx, const double* eta, double g, double dt, double* ratio_dev, void* stream);
 /* apply_mh / apply_mh_inv (columns.py:45-69) on n triangles: v [nc][3][n], j2d [n] */
@@ -161,6 +174,10 @@ int pdg_solve_tridiagonal(int nb, int n, const double* lower, const double* diag
 int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, const double* wm, double kh, double kv,
                           double n0, int order, const int* els, int n_els, double* d, double* u, double* w,
                           void* stream);
+
+/* ---- halo exchange (partitioned runs): field = nplanes planes of nt doubles; buf = [nplanes][n] */
+int pdg_halo_pack(const double* field, long long nplanes, int nt, const int* idx, int n, double* buf, void* stream);
+int pdg_halo_unpack(const double* buf, long long nplanes, int nt, const int* idx, int n, double* field, void* stream);
 
 /* ---- fused IMEX stage entries (the stepper) ---------------- */
 /* F3D->2D = column sum of horizontal_rhs(u, q, fac(q)) + stress_rhs  -> [2][3][nt] */

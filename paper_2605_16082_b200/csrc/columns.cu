@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
                                                    double* __restrict__ Gs, double* x) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
-  if (c >= nt) return;
+  if (c >= m.nown) return;
   const size_t P6 = (size_t)6 * L * nt;
   Col C;
   load_col(m, c, C);
@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
                                                    const double* __restrict__ xin, double* x) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
-  if (c >= nt) return;
+  if (c >= m.nown) return;
   const size_t P6 = (size_t)6 * L * nt;
   Col C;
   load_col(m, c, C);
@@ -957,7 +957,7 @@ int pdg_solve_tridiagonal(int nb, int n, const double* lo, const double* di, con
 int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, const double* wm, double kh, double kv,
                           double n0, int order, const int* els, int n_els, double* d, double* u, double* w,
                           void* stream) {
-  const int n = els ? n_els : ctx->nt;
+  const int n = els ? n_els : ctx->nown;
   if (n == 0) return PDG_OK;
   VopArgs a{eta_g, wt, wm, nullptr, nullptr, 1.0, kh, kv, n0, order};
   k_vop<<<nblocks(n, 128), 128, 0, (cudaStream_t)stream>>>(ctx->view(), a, els, n, d, u, w);
@@ -970,7 +970,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
                       double dt, const double* rhs, const double* xin, double* x, void* stream) {
   VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, kh, kv, n0, order};
   const int nt = ctx->nt;
-  const dim3 grid(nblocks(nt, 128)), blk(128);
+  const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
   if (implicit) {

@@ -74,6 +74,7 @@ __device__ inline void report(pdg_err* e, int code, long long i0, long long i1, 
 // ---------------------------------------------------------------- mesh view passed by value
 struct DMesh {
   int nt, L;
+  int nown;           // columns computed by the stepper (owned); nt = owned + ghosts
   const double* j2d;   // [nt]
   const double* dphx;  // [3][nt]
   const double* dphy;

@@ -59,6 +59,7 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
   pdg_ctx* c = new pdg_ctx();
   c->device = device;
   c->nt = d->nt;
+  c->nown = d->nt;
   c->min_edge = d->min_edge;
   int nt = d->nt;
   int rc = PDG_OK;
@@ -105,6 +106,12 @@ int pdg_ctx_set_layers(pdg_ctx* c, int L, const double* fracs) {
     return PDG_ERR_CUDA;
   c->fracs_host.assign(fracs, fracs + L + 1);
   c->L = L;
+  return PDG_OK;
+}
+
+int pdg_ctx_set_owned(pdg_ctx* c, int nown) {
+  if (nown < 0 || nown > c->nt) return PDG_ERR_SHAPE;
+  c->nown = nown;
   return PDG_OK;
 }
 

@@ -7,6 +7,7 @@
 struct pdg_ctx {
   int device = 0;
   int nt = 0;
+  int nown = 0;   // owned (computed) columns: 0..nown-1; the rest are ghost columns (partitioned runs)
   int L = 0;
   double min_edge = 0.0;
   double *j2d = nullptr, *dphx = nullptr, *dphy = nullptr, *elen = nullptr, *enx = nullptr, *eny = nullptr,
@@ -23,6 +24,7 @@ struct pdg_ctx {
   pdg::DMesh view() const {
     pdg::DMesh m;
     m.nt = nt;
+    m.nown = nown;
     m.L = L;
     m.j2d = j2d;
     m.dphx = dphx;

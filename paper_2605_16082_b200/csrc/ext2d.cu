@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256, 2) k_rk_stage(DMesh m, Ext2DIn a, const d
                                                   double* Y, double dt, double* __restrict__ qbar) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
-  if (c >= nt) return;
+  if (c >= m.nown) return;
   Col C;
   load_col(m, c, C);
   double r[3][3];
@@ -231,7 +231,7 @@ __global__ void k_subcycle_final(DMesh m, const double* __restrict__ S, const do
                                  double* __restrict__ f2d) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
-  if (c >= nt) return;
+  if (c >= m.nown) return;
   const double j2d = m.j2d[c];
 #pragma unroll
   for (int comp = 0; comp < 2; ++comp) {
@@ -260,7 +260,7 @@ __global__ void k_cfl_partial(DMesh m, const double* __restrict__ eta, double* _
   const int nt = m.nt;
   double mn = 1e300, mx = -1e300;
   long long arg = 0x7fffffffffffffffLL;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nt; c += gridDim.x * blockDim.x) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.nown; c += gridDim.x * blockDim.x) {
     double rowmin = 1e300;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -355,7 +355,7 @@ int pdg_ext2d_eval(pdg_ctx* ctx, const double* eta, const double* qx, const doub
                    const int* els, int n_els, int mode, double* oe, double* ox, double* oy, void* stream) {
   cudaSetDevice(ctx->device);
   Ext2DIn a{eta, qx, qy, f3d2d, source, patm, has_bc, eta_bc, g, rho0};
-  const int n = els ? n_els : ctx->nt;
+  const int n = els ? n_els : ctx->nown;
   if (n == 0) return PDG_OK;
   k_ext2d_eval<<<nblocks(n, 128), 128, 0, (cudaStream_t)stream>>>(ctx->view(), a, els, n, mode, oe, ox, oy);
   return check_launch(ctx);
@@ -381,7 +381,7 @@ int pdg_ext2d_subcycle(pdg_ctx* ctx, double* S, int msub, double dt, double g, d
       cudaSuccess)
     return PDG_ERR_CUDA;
   if (cudaMemsetAsync(qbar, 0, (size_t)6 * nt * sizeof(double), s) != cudaSuccess) return PDG_ERR_CUDA;
-  const int bs = 256, nb = nblocks(nt, bs);
+  const int bs = 256, nb = nblocks(ctx->nown, bs);
   for (int it = 0; it < msub; ++it) {
     const int hb = bc_vals != nullptr;
     Ext2DIn a{S, S + (size_t)3 * nt, S + (size_t)6 * nt, f3d2d, source, patm, hb, hb ? bc_vals[3 * it] : 0.0, g, rho0};
@@ -397,6 +397,48 @@ int pdg_ext2d_subcycle(pdg_ctx* ctx, double* S, int msub, double dt, double g, d
     if (check_launch(ctx)) return PDG_ERR_CUDA;
   }
   k_subcycle_final<<<nb, bs, 0, s>>>(m, S, q0, f3d2d, msub, msub * dt, qbar, f2d);
+  return check_launch(ctx);
+}
+
+// ---- per-RK-stage entries (partitioned runs exchange the stage state between stages) ----
+int pdg_ext2d_subcycle_begin(pdg_ctx* ctx, const double* S, double g, double dt, int check_cfl, double* qbar,
+                             void* stream) {
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nt = ctx->nt;
+  if (check_cfl && run_cfl(ctx, S, g, dt, ctx->red + 4000, s)) return PDG_ERR_CUDA;
+  double* q0 = ctx->ws2d + (size_t)18 * nt;
+  if (cudaMemcpyAsync(q0, S + (size_t)3 * nt, (size_t)6 * nt * sizeof(double), cudaMemcpyDeviceToDevice, s) !=
+      cudaSuccess)
+    return PDG_ERR_CUDA;
+  if (cudaMemsetAsync(qbar, 0, (size_t)6 * nt * sizeof(double), s) != cudaSuccess) return PDG_ERR_CUDA;
+  return PDG_OK;
+}
+
+// one SSP-RK3 stage: X = state evaluated, S0 = substep start, Y = output (stage 2 may write Y = S0)
+int pdg_ext2d_rk_stage(pdg_ctx* ctx, int stage, const double* X, const double* S0, double* Y, double dt, double g,
+                       double rho0, const double* f3d2d, const double* source, const double* patm, int has_bc,
+                       double eta_bc, double* qbar, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nt = ctx->nt;
+  DMesh m = ctx->view();
+  const int bs = 256, nb = nblocks(ctx->nown, bs);
+  Ext2DIn a{X, X + (size_t)3 * nt, X + (size_t)6 * nt, f3d2d, source, patm, has_bc, eta_bc, g, rho0};
+  if (stage == 0)
+    k_rk_stage<0><<<nb, bs, 0, s>>>(m, a, S0, Y, dt, qbar);
+  else if (stage == 1)
+    k_rk_stage<1><<<nb, bs, 0, s>>>(m, a, S0, Y, dt, qbar);
+  else
+    k_rk_stage<2><<<nb, bs, 0, s>>>(m, a, S0, Y, dt, qbar);
+  return check_launch(ctx);
+}
+
+int pdg_ext2d_subcycle_end(pdg_ctx* ctx, const double* S, const double* f3d2d, int msub, double dt, double* qbar,
+                           double* f2d, void* stream) {
+  const int nt = ctx->nt;
+  double* q0 = ctx->ws2d + (size_t)18 * nt;
+  k_subcycle_final<<<nblocks(ctx->nown, 256), 256, 0, (cudaStream_t)stream>>>(ctx->view(), S, q0, f3d2d, msub,
+                                                                              msub * dt, qbar, f2d);
   return check_launch(ctx);
 }
 

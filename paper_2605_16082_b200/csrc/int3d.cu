@@ -170,7 +170,7 @@ __global__ void k_colsum(int nt, int L, int ncomp, const double* __restrict__ f,
 __global__ void k_htot(DMesh m, const double* __restrict__ eta_g, double* __restrict__ htot) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
-  if (c >= nt) return;
+  if (c >= m.nown) return;
   double eta[3], b[3], hs[3] = {0, 0, 0};
   load_eta(eta_g, c, nt, eta);
 #pragma unroll
@@ -186,10 +186,10 @@ __global__ void k_htot(DMesh m, const double* __restrict__ eta_g, double* __rest
 }
 
 // transport mismatch (Qbar - sum_col q) / H per column corner (internal3d.py:198-200)
-__global__ void k_mismatch(int nt, const double* __restrict__ qbar, const double* __restrict__ qsum,
+__global__ void k_mismatch(int nt, int nown, const double* __restrict__ qbar, const double* __restrict__ qsum,
                            const double* __restrict__ htot, double* __restrict__ mis) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nt) return;
+  if (c >= nown) return;
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -1051,7 +1051,7 @@ using namespace pdg;
     default: KERNEL<__VA_ARGS__, 1><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
   }
 
-#define COLS(els, n) Cols{els, (els) ? (n) : ctx->nt}
+#define COLS(els, n) Cols{els, (els) ? (n) : ctx->nown}
 #define GRID1(nn) nblocks((nn), 128), 128, 0, (cudaStream_t)stream
 
 extern "C" {
@@ -1081,13 +1081,13 @@ int pdg_column_sum(int nt, int L, int ncomp, const double* f, double* out, void*
 }
 
 int pdg_total_thickness(pdg_ctx* ctx, const double* eta_g, double* htot, void* stream) {
-  k_htot<<<GRID1(ctx->nt)>>>(ctx->view(), eta_g, htot);
+  k_htot<<<GRID1(ctx->nown)>>>(ctx->view(), eta_g, htot);
   return check_launch(ctx);
 }
 
 int pdg_mismatch(pdg_ctx* ctx, const double* qbar, const double* qsum, const double* htot, double* mis,
                  void* stream) {
-  k_mismatch<<<GRID1(ctx->nt)>>>(ctx->nt, qbar, qsum, htot, mis);
+  k_mismatch<<<GRID1(ctx->nown)>>>(ctx->nt, ctx->nown, qbar, qsum, htot, mis);
   return check_launch(ctx);
 }
 
@@ -1200,7 +1200,7 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   a.tsx = tsx;
   a.tsy = tsy;
   a.cd = cd;
-  Cols cs{nullptr, ctx->nt};
+  Cols cs{nullptr, ctx->nown};
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, f3d2d
@@ -1232,7 +1232,7 @@ int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta
   a.tsy = tsy;
   a.cd = cd;
   a.dt = dt;
-  Cols cs{nullptr, ctx->nt};
+  Cols cs{nullptr, ctx->nown};
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out

@@ -38,6 +38,7 @@ class DeviceMesh:
 
     def __init__(self, mesh, device=None):
         require_cuda()
+        _drain_pending()
         self.mesh = mesh
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.nt = mesh.nt
@@ -77,16 +78,35 @@ class DeviceMesh:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and _lib._lib is not None:
-            try:
-                _lib.lib().pdg_ctx_destroy(h)
-            except Exception:
-                pass
+            # cudaFree is illegal while any stream is being captured into a CUDA graph (global capture
+            # mode); garbage collection can run this finaliser in the middle of a capture -> defer.
+            _PENDING.append(h)
+            _drain_pending()
+
+
+_PENDING = []
+
+
+def _drain_pending():
+    try:
+        if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+            return
+    except Exception:
+        return
+    while _PENDING:
+        h = _PENDING.pop()
+        try:
+            _lib.lib().pdg_ctx_destroy(h)
+        except Exception:
+            pass
 
 
 def mesh_fingerprint(mesh) -> bytes:
     hsh = hashlib.blake2b(digest_size=16)
-    for k in ("tri", "nbr", "nbrk", "btag", "vx", "vy", "vb"):
-        hsh.update(np.ascontiguousarray(getattr(mesh, k)).tobytes())
+    for k in ("tri", "nbr", "nbrk", "btag", "vx", "vy", "vb", "b"):
+        a = getattr(mesh, k, None)
+        if a is not None:
+            hsh.update(np.ascontiguousarray(a).tobytes())
     return hsh.digest()
 
 

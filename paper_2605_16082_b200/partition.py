@@ -1,0 +1,290 @@
+"""Horizontal domain decomposition and halo exchange (no reference code exists).
+
+decompose(mesh, P): contiguous ranges of the Hilbert order balanced by prism count (weights =
+layers per column) with a greedy prefix split, plus a one-ring ghost layer = every column that
+shares an edge with an owned column.  Local numbering: owned columns first
+(in global order), then ghosts (ascending global id).  The send/recv maps of every pair of
+ranks list the same global ids in the same (ascending) order, so a halo message is a plain
+[plane][i] block.
+
+Because every assembly kernel is gather-only, a partitioned run reproduces the P = 1 run
+bitwise (tests/test_partition*.py).
+
+Transports: `DistHalo` (one process per GPU, torch.distributed send/recv -- NCCL over NVLink on
+the GPU box, gloo on CPU) and `VirtualGroup` (P ranks in one process on one device; messages are
+device-to-device copies) -- the latter makes the partitioned path testable on a single GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from types import SimpleNamespace
+
+import numpy as np
+
+from .errors import MapMismatch, TooManyRanks
+
+
+@dataclass
+class Part:
+    rank: int
+    nparts: int
+    lo: int                     # owned global range [lo, hi)
+    hi: int
+    ghosts: np.ndarray          # global ids of ghost columns (ascending)
+    send: dict = field(default_factory=dict)   # peer -> local indices (owned) to send
+    recv: dict = field(default_factory=dict)   # peer -> local indices (ghost slots) to fill
+
+    @property
+    def n_own(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def local(self) -> np.ndarray:
+        """global ids of the local columns (owned then ghosts)."""
+        return np.concatenate([np.arange(self.lo, self.hi), self.ghosts])
+
+
+def split_ranges(weights, P):
+    """Greedy prefix split: boundary k is the first prefix whose weight reaches k W / P (exact integers)."""
+    w = np.asarray(weights, dtype=np.int64)
+    n = w.size
+    if P < 1:
+        raise ValueError("P must be >= 1")
+    if P > n:
+        raise TooManyRanks(f"{P} ranks for {n} columns")
+    cum = np.cumsum(w)
+    W = int(cum[-1])
+    bounds = [0]
+    for k in range(1, P):
+        b = int(np.searchsorted(cum * P, k * W, side="left")) + 1
+        b = max(b, bounds[-1] + 1)            # never an empty part
+        b = min(b, n - (P - k))
+        bounds.append(b)
+    bounds.append(n)
+    return np.asarray(bounds, dtype=np.int64)
+
+
+def decompose(mesh, P: int, layers=None):
+    """list of Part for ranks 0..P-1."""
+    nt = mesh.nt
+    weights = np.ones(nt, np.int64) if layers is None else np.asarray(layers, np.int64)
+    b = split_ranges(weights, P)
+    owner = np.repeat(np.arange(P), np.diff(b))
+    parts = []
+    nbr = np.asarray(mesh.nbr)
+    for r in range(P):
+        lo, hi = int(b[r]), int(b[r + 1])
+        nb = nbr[lo:hi].ravel()
+        nb = nb[nb >= 0]
+        ghosts = np.unique(nb[(nb < lo) | (nb >= hi)])
+        parts.append(Part(r, P, lo, hi, ghosts))
+    for r, p in enumerate(parts):
+        for s in np.unique(owner[p.ghosts]) if p.ghosts.size else []:
+            s = int(s)
+            sel = p.ghosts[owner[p.ghosts] == s]                      # ascending global ids
+            p.recv[s] = (p.n_own + np.searchsorted(p.ghosts, sel)).astype(np.int32)
+            parts[s].send[r] = (sel - parts[s].lo).astype(np.int32)
+    for p in parts:
+        for s, idx in p.recv.items():
+            if parts[s].send.get(p.rank) is None or parts[s].send[p.rank].size != idx.size:
+                raise MapMismatch(f"ranks {s} -> {p.rank}")
+    return parts
+
+
+def local_mesh(mesh, part: Part):
+    """Mesh arrays of the local columns (owned + ghosts); neighbours remapped to local ids
+    (-1 where a ghost's neighbour is not local -- never read: only owned columns are computed)."""
+    gl = part.local
+    g2l = np.full(mesh.nt, -1, dtype=np.int64)
+    g2l[gl] = np.arange(gl.size)
+    lm = SimpleNamespace()
+    for k in ("j2d", "dphx", "dphy", "elen", "enx", "eny", "b", "x", "y", "nbrk", "btag"):
+        setattr(lm, k, np.ascontiguousarray(np.asarray(getattr(mesh, k))[gl]))
+    nbr = np.asarray(mesh.nbr)[gl]
+    lm.nbr = np.where(nbr >= 0, g2l[np.maximum(nbr, 0)], -1).astype(np.int64)
+    lm.nt = gl.size
+    lm.min_edge = float(mesh.min_edge)
+    lm.global_ids = gl
+    lm.tri = np.asarray(mesh.tri)[gl]
+    return lm
+
+
+# ----------------------------------------------------------------------------- exchange
+
+class _Maps:
+    """Device copies of one rank's send / recv index lists."""
+
+    def __init__(self, part: Part, device):
+        import torch
+        self.part = part
+        self.send = {s: torch.as_tensor(v, device=device) for s, v in sorted(part.send.items())}
+        self.recv = {s: torch.as_tensor(v, device=device) for s, v in sorted(part.recv.items())}
+
+
+def _pack(fields, nt, idx, buf):
+    """fields: tensors whose last dim-run is [..][nt] (planes of nt columns); buf: 1-D [sum nplanes * n].
+    CUDA tensors use the pdg_halo_pack kernel; CPU tensors (gloo tests) torch indexing."""
+    off = 0
+    n = idx.numel()
+    for f in fields:
+        npl = f.numel() // nt
+        if f.is_cuda:
+            import ctypes
+            from . import _lib
+            from .device import stream_ptr
+            _lib.check(_lib.lib().pdg_halo_pack(ctypes.c_void_p(f.data_ptr()), npl, nt,
+                                                ctypes.c_void_p(idx.data_ptr()), n,
+                                                ctypes.c_void_p(buf.data_ptr() + 8 * off), stream_ptr()), "pack")
+        else:
+            buf[off:off + npl * n] = f.reshape(npl, nt)[:, idx.long()].reshape(-1)
+        off += npl * n
+
+
+def _unpack(fields, nt, idx, buf):
+    off = 0
+    n = idx.numel()
+    for f in fields:
+        npl = f.numel() // nt
+        if f.is_cuda:
+            import ctypes
+            from . import _lib
+            from .device import stream_ptr
+            _lib.check(_lib.lib().pdg_halo_unpack(ctypes.c_void_p(buf.data_ptr() + 8 * off), npl, nt,
+                                                  ctypes.c_void_p(idx.data_ptr()), n,
+                                                  ctypes.c_void_p(f.data_ptr()), stream_ptr()), "unpack")
+        else:
+            f.view(npl, nt)[:, idx.long()] = buf[off:off + npl * n].reshape(npl, n)
+        off += npl * n
+
+
+class DistHalo:
+    """One rank of a torch.distributed job (NCCL on GPUs, gloo on CPU for the host-side tests)."""
+
+    def __init__(self, part: Part, nt_local: int, device):
+        self.maps = _Maps(part, device)
+        self.nt = nt_local
+        self.device = device
+        self.exchanges = 0
+
+    def exchange(self, fields):
+        import torch
+        import torch.distributed as dist
+        tot = sum(f.numel() // self.nt for f in fields)
+        sends, recvs, ops = {}, {}, []
+        for peer, idx in self.maps.send.items():
+            buf = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
+            _pack(fields, self.nt, idx, buf)
+            sends[peer] = buf
+        for peer, idx in self.maps.recv.items():
+            recvs[peer] = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
+        for peer in sorted(set(sends) | set(recvs)):
+            if peer in sends:
+                ops.append(dist.P2POp(dist.isend, sends[peer], peer))
+            if peer in recvs:
+                ops.append(dist.P2POp(dist.irecv, recvs[peer], peer))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for peer, idx in self.maps.recv.items():
+            _unpack(fields, self.nt, idx, recvs[peer])
+        self.exchanges += 1
+
+
+class VirtualGroup:
+    """P ranks in one process on one device: halo messages are device-to-device copies."""
+
+    def __init__(self, parts, nts, device):
+        self.maps = [_Maps(p, device) for p in parts]
+        self.nts = nts
+        self.device = device
+        self.exchanges = 0
+
+    def exchange_all(self, fields_per_rank):
+        import torch
+        msgs = {}
+        for r, (mp, fields) in enumerate(zip(self.maps, fields_per_rank)):
+            tot = sum(f.numel() // self.nts[r] for f in fields)
+            for peer, idx in mp.send.items():
+                buf = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
+                _pack(fields, self.nts[r], idx, buf)
+                msgs[(r, peer)] = buf
+        for r, (mp, fields) in enumerate(zip(self.maps, fields_per_rank)):
+            for peer, idx in mp.recv.items():
+                _unpack(fields, self.nts[r], idx, msgs[(peer, r)])
+        self.exchanges += 1
+
+
+class PartitionedRun:
+    """P partitions of one mesh, each an ImexStepper over its owned + ghost columns.
+
+    transport "virtual": all ranks in this process on one device (VirtualGroup);
+    transport "dist": this process is rank `rank` of a torch.distributed job (DistHalo).
+    """
+
+    def __init__(self, mesh, L, params, dt, m, kv, nu_v, P, transport="virtual", rank=None, device=None):
+        import torch
+        from .stepper import ImexStepper
+        self.mesh, self.L, self.P = mesh, L, P
+        self.parts = decompose(mesh, P, np.full(mesh.nt, L))
+        self.local = [local_mesh(mesh, p) for p in self.parts]
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        ranks = range(P) if transport == "virtual" else [rank]
+        self.ranks = list(ranks)
+        self.st = {r: ImexStepper(self.local[r], L, params, dt, m, kv, nu_v, part=self.parts[r], device=dev.index)
+                   for r in ranks}
+        if transport == "virtual":
+            self.group = VirtualGroup(self.parts, [lm.nt for lm in self.local], dev)
+        else:
+            self.group = None
+            self.st[rank].halo = DistHalo(self.parts[rank], self.local[rank].nt, dev)
+
+    def set_state(self, eta, qx, qy, ux, uy, T, t=0.0):
+        L = self.L
+        for r, st in self.st.items():
+            gl = self.local[r].global_ids
+            pr = (gl[:, None] * L + np.arange(L)[None, :]).ravel()
+            st.set_state(eta[gl], qx[gl], qy[gl], ux[pr], uy[pr], T[pr], t)
+
+    def get_state(self):
+        """Global numpy state gathered from the owned columns (virtual transport: all ranks here)."""
+        L, nt = self.L, self.mesh.nt
+        out = dict(eta=np.zeros((nt, 3)), qx=np.zeros((nt, 3)), qy=np.zeros((nt, 3)), ux=np.zeros((nt * L, 6)),
+                   uy=np.zeros((nt * L, 6)), T=np.zeros((nt * L, 6)))
+        for r, st in self.st.items():
+            p = self.parts[r]
+            s = st.get_state()
+            own = slice(0, p.n_own)
+            out["eta"][p.lo:p.hi] = s["eta"][own]
+            out["qx"][p.lo:p.hi] = s["qx"][own]
+            out["qy"][p.lo:p.hi] = s["qy"][own]
+            for k in ("ux", "uy", "T"):
+                out[k][p.lo * L:p.hi * L] = s[k][:p.n_own * L]
+            out["t"] = s["t"]
+        return out
+
+    def step(self, n=1):
+        import torch
+        for _ in range(n):
+            if self.group is not None:
+                gens = {r: st._step_gen(st.t) for r, st in self.st.items()}
+                while True:
+                    fields, done = [], 0
+                    for r in self.ranks:          # every rank runs the same phase, then one exchange
+                        try:
+                            fields.append(next(gens[r]))
+                        except StopIteration:
+                            done += 1
+                    if done:
+                        if done != len(self.ranks):
+                            raise MapMismatch("ranks reached different exchange points")
+                        break
+                    self.group.exchange_all(fields)
+            else:
+                for st in self.st.values():
+                    st._launch_step(st.t)
+            for st in self.st.values():
+                st._advance()
+
+    def check(self):
+        for st in self.st.values():
+            st.check()

@@ -38,7 +38,7 @@ class ImexStepper:
     """Device-resident internal+external stepper for one mesh / layer count."""
 
     def __init__(self, mesh, L: int, params: PhysParams, dt: float, m: int, kv: float, nu_v: float,
-                 pen: PenaltyParams = PenaltyParams(), device=None):
+                 pen: PenaltyParams = PenaltyParams(), device=None, part=None):
         if m % 2:
             raise ValueError("m must be even (stage 1 uses m/2 substeps)")
         if params.kappa_h or params.kappa_v or params.nu_h or params.nu_v:
@@ -47,7 +47,14 @@ class ImexStepper:
                                       "diffusion is set by kv / nu_v")
         self.mesh, self.L, self.p = mesh, L, params
         self.dt, self.m, self.kv, self.nu_v, self.pen = float(dt), int(m), float(kv), float(nu_v), pen
-        self.dm = device_mesh(mesh, L)
+        self.part = part          # partition.Part when this stepper owns only part of the columns
+        if part is None:
+            self.dm = device_mesh(mesh, L)
+        else:
+            from .device import DeviceMesh
+            self.dm = DeviceMesh(mesh, device).set_layers(L)
+            _lib.check(_lib.lib().pdg_ctx_set_owned(self.dm.h, part.n_own), "set_owned")
+        self.halo = None          # DistHalo for multi-process runs (VirtualGroup drives several steppers)
         self.dev = self.dm.device
         nt = self.nt = mesh.nt
         z = lambda *s: torch.zeros(s, dtype=F64, device=self.dev)  # noqa: E731
@@ -60,6 +67,7 @@ class ImexStepper:
         self.wt = z(6, L, nt)
         self.qsum, self.htot, self.f3d2d = z(2, 3, nt), z(3, nt), z(2, 3, nt)
         self.qbar, self.f2d, self.mis = z(2, 3, nt), z(2, 3, nt), z(2, 3, nt)
+        self.W12 = (z(3, 3, nt), z(3, 3, nt)) if part is not None else None   # RK stage states (partitioned)
         self.cur = 0
         self.t = 0.0
         self.graphs = {}
@@ -105,21 +113,40 @@ class ImexStepper:
 
     # ------------------------------------------------------------------ one stage
     def _stage(self, s, eta_u, u, T, u0, T0, Sw, out_u, out_T, dt_s, m_s, implicit, t_wind):
+        """One IMEX stage as a generator: yields the fields whose ghost columns must be refreshed
+        (partitioned runs only) and returns the end-of-stage free surface."""
         lb, h, p = _lib.lib(), self.dm.h, self.p
         tm = self._timed
+        part = self.part is not None
         eta0 = self.S[0]
         tsx, tsy = p.wind(t_wind)
         tag = "impl" if implicit else "expl"
         tm("r", lb.pdg_compute_r, h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s)
         tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
            ptr(self.qsum), ptr(self.htot), s)
+        if part:
+            yield [self.q]
         tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
         Sw.copy_(self.S)
-        tm(f"subcycle{m_s}", lb.pdg_ext2d_subcycle, h, ptr(Sw), m_s, dt_s / m_s, p.g, p.rho0, ptr(self.f3d2d), None,
-           None, None, ptr(self.qbar), ptr(self.f2d), 1, s)
+        dt2 = dt_s / m_s
+        if not part:
+            tm(f"subcycle{m_s}", lb.pdg_ext2d_subcycle, h, ptr(Sw), m_s, dt2, p.g, p.rho0, ptr(self.f3d2d), None,
+               None, None, ptr(self.qbar), ptr(self.f2d), 1, s)
+        else:
+            tm("sub_begin", lb.pdg_ext2d_subcycle_begin, h, ptr(Sw), p.g, dt2, 1, ptr(self.qbar), s)
+            W1, W2 = self.W12
+            for _ in range(m_s):
+                for k, (X, Y) in enumerate(((Sw, W1), (W1, W2), (W2, Sw))):
+                    tm(f"rk{k}", lb.pdg_ext2d_rk_stage, h, k, ptr(X), ptr(Sw), ptr(Y), dt2, p.g, p.rho0,
+                       ptr(self.f3d2d), None, None, 0, 0.0, ptr(self.qbar), s)
+                    yield [Y]
+            tm("sub_end", lb.pdg_ext2d_subcycle_end, h, ptr(Sw), ptr(self.f3d2d), m_s, dt2, ptr(self.qbar),
+               ptr(self.f2d), s)
         eta1 = Sw[0]
         tm("mismatch", lb.pdg_mismatch, h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s)
+        if part:
+            yield [self.mis]
         tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
            ptr(self.wt), s)
         tm("rhs_u", lb.pdg_step_rhs, h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q),
@@ -131,32 +158,41 @@ class ImexStepper:
            ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
         tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
+        if part:
+            yield [out_u, out_T]
         return eta1
 
-    def _launch_step(self, t0):
+    def _step_gen(self, t0):
         s = stream_ptr()
         a, b, c = self.cur, (self.cur + 1) % 3, (self.cur + 2) % 3
         U, T = self.U, self.T
-        eta_h = self._stage(s, self.S[0], U[a], T[a], U[a], T[a], self.Sw[0], U[b], T[b], 0.5 * self.dt,
-                            self.m // 2, True, t0)
-        self._stage(s, eta_h, U[b], T[b], U[a], T[a], self.Sw[1], U[c], T[c], self.dt, self.m, False,
-                    t0 + 0.5 * self.dt)
+        eta_h = yield from self._stage(s, self.S[0], U[a], T[a], U[a], T[a], self.Sw[0], U[b], T[b], 0.5 * self.dt,
+                                       self.m // 2, True, t0)
+        yield from self._stage(s, eta_h, U[b], T[b], U[a], T[a], self.Sw[1], U[c], T[c], self.dt, self.m, False,
+                               t0 + 0.5 * self.dt)
         self.S.copy_(self.Sw[1])
+
+    def _launch_step(self, t0):
+        for fields in self._step_gen(t0):
+            self.halo.exchange(fields)
+
+    def _advance(self):
+        self.cur = (self.cur + 2) % 3
+        self.t = self.t + self.dt
 
     def step(self, n: int = 1):
         """Advance n internal steps (stream ordered, no host sync)."""
         with torch.cuda.device(self.dev):
             for _ in range(n):
                 wind_varies = self.p.tau_x1 is not None
-                if self.use_graph and not wind_varies:
+                if self.use_graph and not wind_varies and self.part is None:
                     g = self.graphs.get(self.cur)
                     if g is None:
                         g = self._capture()
                     g.replay()
                 else:
                     self._launch_step(self.t)
-                self.cur = (self.cur + 2) % 3
-                self.t = self.t + self.dt
+                self._advance()
 
     def _capture(self):
         # warm the workspace (block-Thomas scratch is sized on first use), then capture
@@ -168,8 +204,16 @@ class ImexStepper:
             self._launch_step(self.t)                          # sizes workspaces (result discarded)
             self.S.copy_(saved[0])
         torch.cuda.current_stream().wait_stream(side)
-        with torch.cuda.graph(g):
-            self._launch_step(self.t)
+        import gc
+        gc.collect()                       # run pending finalisers before the capture, not inside it
+        gcflag = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g):
+                self._launch_step(self.t)
+        finally:
+            if gcflag:
+                gc.enable()
         self.graphs[self.cur] = g
         return g
 
