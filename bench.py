@@ -188,6 +188,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="process group for N>1 (gloo: host-staged halos, testing)")
+    ap.add_argument("--dump", default=None, help="write the final local state to this .npz (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -200,26 +202,42 @@ def main():
 
     import torch
     import torch.distributed as dist
+    if args.backend == "gloo":
+        local = 0 if torch.cuda.device_count() == 1 else local     # ranks may share one GPU for testing
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2605_16082_b200 import stepper as S
+    from paper_2605_16082_b200.partition import PartitionedRun
     from paper_2605_16082_b200.scenarios import device_state_c4, make_case
 
     t_setup = time.perf_counter()
     case = make_case(args.config, with_state=(args.config != "c4"))
-    st = S.ImexStepper(case.mesh, case.L, case.params, case.dt, case.m, case.kv, case.nu_v)
+    if world == 1:
+        st = S.ImexStepper(case.mesh, case.L, case.params, case.dt, case.m, case.kv, case.nu_v)
+        stepper = st
+    else:
+        # strong scaling: the one C4 mesh split into `world` Hilbert ranges, halos over NCCL
+        run = PartitionedRun(case.mesh, case.L, case.params, case.dt, case.m, case.kv, case.nu_v, world,
+                             transport="dist", rank=rank, device=local)
+        st = run.st[rank]
+        stepper = run
     if args.config == "c4":
         device_state_c4(case, st)
-    else:
+    elif world == 1:
         st.set_state(**case.state)
+    else:
+        run.set_state(**case.state)
     setup_s = time.perf_counter() - t_setup
     P = case.prisms
-    dof_per_step = 6.0 * P
+    dof_per_step = 6.0 * P          # whole job (all ranks together)
 
     # warm-up (graph capture happens on the first step)
-    st.step(args.warmup)
+    stepper.step(args.warmup)
     torch.cuda.synchronize()
     st.check()
 
@@ -230,7 +248,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         e0.record()
-        st.step(args.steps)
+        stepper.step(args.steps)
         e1.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -241,13 +259,13 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     st.check()
-    value = dof_per_step * world / (t_ms * 1e-3)
+    value = dof_per_step / (t_ms * 1e-3)
 
     # ---- per-kernel breakdown (same K steps, unfused launches with CUDA events on the launching stream)
     launches = st.launches_per_step()
     st.use_graph = False
     st.prof = {}
-    st.step(args.steps)
+    stepper.step(args.steps)
     torch.cuda.synchronize()
     prof = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in st.prof.items()}
     counts = {k: len(v) / args.steps for k, v in st.prof.items()}
@@ -256,12 +274,15 @@ def main():
     step_sum = sum(prof[k] * counts[k] for k in prof)
     hbm, peak_kind = peaks()
     per = {}
+    P_local = st.nt * case.L if world == 1 else st.part.n_own * case.L
     for k, ms in prof.items():
         if k in KERNEL_BYTES:
-            b = KERNEL_BYTES[k] * P
+            b = KERNEL_BYTES[k] * P_local
         elif k.startswith("subcycle"):
             msub = int(k[len("subcycle"):])
-            b = RK_STAGE_BYTES_PER_TRI * case.mesh.nt * 3 * msub
+            b = RK_STAGE_BYTES_PER_TRI * (P_local // case.L) * 3 * msub
+        elif k.startswith("rk"):
+            b = RK_STAGE_BYTES_PER_TRI * (P_local // case.L)
         else:
             b = 0
         per[k] = {"ms": ms, "share": ms * counts[k] / step_sum, "GBps": (b / (ms * 1e-3) / 1e9) if b else None,
@@ -272,7 +293,7 @@ def main():
                 "peak_kind": peak_kind, "traffic": None,
                 "bytes_per_launch": per[dom]["bytes"], "launch_ms": per[dom]["ms"],
                 "step_model_M2": {"bytes_per_prism": M2_BYTES_PER_PRISM(case.L, case.m),
-                                  "frac": M2_BYTES_PER_PRISM(case.L, case.m) * P / (t_ms * 1e-3) / 1e9 / hbm}}
+                                  "frac": M2_BYTES_PER_PRISM(case.L, case.m) * P / world / (t_ms * 1e-3) / 1e9 / hbm}}
 
     # ---- e2e: public API, host pinned buffers, full state round trip every step
     e2e = None
@@ -287,7 +308,7 @@ def main():
         for _ in range(ke):
             dv = {k: (v.to("cuda", non_blocking=True) if isinstance(v, torch.Tensor) else v) for k, v in pin.items()}
             st.set_state(dv["eta"], dv["qx"], dv["qy"], dv["ux"], dv["uy"], dv["T"], dv["t"])
-            st.step(1)
+            stepper.step(1)
             out = st.get_state(numpy=False)
             for k, v in out.items():
                 if isinstance(v, torch.Tensor):
@@ -299,8 +320,8 @@ def main():
             tt = torch.tensor([te], device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-        e2e = {"value": dof_per_step * world / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": h2d, "ms_per_step": te, "steps": ke,
+        e2e = {"value": dof_per_step / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": h2d * world, "ms_per_step": te, "steps": ke,
                "path": "ImexStepper.set_state/step/get_state with pinned host buffers (full state round trip)"}
 
     # ---- CPU baseline (rank 0, N=1 only)
@@ -312,15 +333,22 @@ def main():
                "sample": f"2 full IMEX steps (L={case.L}, m={case.m}) of a {prisms}-prism patch of {args.config}, "
                          f"numpy oracle (oracle/stepper.py), single process; {tstep:.2f} s/step"}
 
+    if args.dump:
+        s_ = st.get_state()
+        n_own = st.part.n_own if world > 1 else st.nt
+        gid = (st.mesh.global_ids if world > 1 else np.arange(st.nt))[:n_own]
+        np.savez(f"{args.dump}.{rank}.npz", gid=gid, eta=s_["eta"][:n_own], T=s_["T"][:n_own * case.L],
+                 ux=s_["ux"][:n_own * case.L])
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-               "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded coastal basin; inputs larger than L2, no flush needed)",
                "config": {"workload": f"{args.config}: {case.mesh.nt} tri x {case.L} layers = {P} prisms, "
                                       f"m={case.m}, dt2d={case.dt2d} s, momentum+tracer, FP64",
                           "nt": case.mesh.nt, "L": case.L, "m": case.m, "prism_dof_per_step": dof_per_step,
-                          "parallelism": f"replicas{world}" if world > 1 else "single GPU",
+                          "parallelism": (f"column partition x{world} (Hilbert ranges, one-ring ghosts, NCCL "
+                                          "halo send/recv)") if world > 1 else "single GPU",
                           "l2": "inputs larger than L2 (~48 GB resident fields)"},
                "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),

@@ -161,10 +161,14 @@ class DistHalo:
     """One rank of a torch.distributed job (NCCL on GPUs, gloo on CPU for the host-side tests)."""
 
     def __init__(self, part: Part, nt_local: int, device):
+        import torch.distributed as dist
         self.maps = _Maps(part, device)
         self.nt = nt_local
         self.device = device
         self.exchanges = 0
+        # gloo cannot send CUDA tensors: stage the packed messages through host memory (lets the
+        # multi-process path run -- and be tested -- with several ranks sharing one GPU)
+        self.host_staging = dist.is_initialized() and dist.get_backend() == "gloo" and device.type == "cuda"
 
     def exchange(self, fields):
         import torch
@@ -174,9 +178,10 @@ class DistHalo:
         for peer, idx in self.maps.send.items():
             buf = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
             _pack(fields, self.nt, idx, buf)
-            sends[peer] = buf
+            sends[peer] = buf.cpu() if self.host_staging else buf
         for peer, idx in self.maps.recv.items():
-            recvs[peer] = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
+            recvs[peer] = torch.empty(tot * idx.numel(), dtype=torch.float64,
+                                      device="cpu" if self.host_staging else self.device)
         for peer in sorted(set(sends) | set(recvs)):
             if peer in sends:
                 ops.append(dist.P2POp(dist.isend, sends[peer], peer))
@@ -186,7 +191,8 @@ class DistHalo:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         for peer, idx in self.maps.recv.items():
-            _unpack(fields, self.nt, idx, recvs[peer])
+            buf = recvs[peer].to(self.device) if self.host_staging else recvs[peer]
+            _unpack(fields, self.nt, idx, buf)
         self.exchanges += 1
 
 

@@ -141,9 +141,10 @@ def c4_host_state(c: Case, seed=42):
 
 
 def device_state_c4(c: Case, stepper, seed=42):
-    """Fill a stepper with the C4 initial state generated on device, in device layouts."""
+    """Fill a stepper with the C4 initial state generated on device, in device layouts
+    (works for a partition's local mesh too: every value is a function of the node position)."""
     import torch
-    mesh, L, nt = c.mesh, c.L, c.mesh.nt
+    mesh, L = stepper.mesh, c.L
     dev = stepper.dev
     lx, x0 = c.lx, c.x0
     eta = _c4_eta(mesh.x + x0, lx)
