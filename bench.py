@@ -145,6 +145,7 @@ def cpu_oracle_throughput(name, steps, procs, scale, skip=0):
     import multiprocessing as mp
     for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):   # one BLAS thread per process
         os.environ[v] = "1"
+    os.environ["PDG_MESH_HOST"] = "1"          # the CPU arm never touches the GPU
     L = 50 if name == "c4" else None
     jobs = [(name, scale, L, steps, i) for i in range(procs)]
     if procs == 1:

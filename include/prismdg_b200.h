@@ -68,6 +68,17 @@ typedef struct pdg_mesh_desc {
   double min_edge;
 } pdg_mesh_desc;
 
+/* ---- Mesh2D setup on device (mesh.py:79-127, 187-228) ---------------------------------------
+ * pdg_mesh_build: nodal coordinates, J2D, grad phi, edge lengths/normals and the edge pairing
+ * (nbr, nbrk, btag; bit-exact with the reference's dict pass via a stable radix sort).  All DEVICE
+ * pointers in the reference (nt,3) layout; tri int64 (nt,3).  err: code 8 = NonPositiveArea.
+ * pdg_hilbert_perm: hilbert_reorder's permutation (stable sort of the order-`order` curve distance). */
+int pdg_mesh_build(int nt, long long nv, const double* vx, const double* vy, const double* vb, const long long* tri,
+                   double* x, double* y, double* b, double* j2d, double* dphx, double* dphy, double* elen,
+                   double* enx, double* eny, long long* nbr, long long* nbrk, long long* btag, pdg_err* err,
+                   void* stream);
+int pdg_hilbert_perm(int nt, int order, const double* x, const double* y, long long* perm, void* stream);
+
 /* ---- context ------------------------------------------------------------------------- */
 int pdg_ctx_create(const pdg_mesh_desc* mesh, int device, pdg_ctx** out);
 int pdg_ctx_destroy(pdg_ctx* ctx);

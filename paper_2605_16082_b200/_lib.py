@@ -31,6 +31,8 @@ _SIGS = {
     "pdg_launch_count": (LL, [P]),
     "pdg_tune": (I, [I, I]),
     "pdg_ctx_set_owned": (I, [P, I]),
+    "pdg_mesh_build": (I, [I, LL] + [P] * 16 + [P]),
+    "pdg_hilbert_perm": (I, [I, I, P, P, P, P]),
     "pdg_ext2d_subcycle_begin": (I, [P, P, D, D, I, P, P]),
     "pdg_ext2d_rk_stage": (I, [P, I, P, P, P, D, D, D, P, P, P, I, D, P, P]),
     "pdg_ext2d_subcycle_end": (I, [P, P, P, I, D, P, P, P]),

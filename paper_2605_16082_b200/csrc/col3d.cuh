@@ -18,6 +18,21 @@ __device__ __forceinline__ void st6(double* __restrict__ f, int l, int c, int L,
   for (int k = 0; k < 6; ++k) f[((size_t)k * L + l) * nt + c] = v[k];
 }
 
+// L1 prefetch of the 6 node planes of layer l (issued one layer ahead: the thread-per-column
+// kernels run at ~8 warps/SM, too few to hide HBM latency, and have no registers to spare for
+// software pipelining -- a prefetch costs no register)
+__device__ __forceinline__ void pf6(const double* f, int l, int c, int L, int nt) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)k * L + l) * nt + c));
+}
+__device__ __forceinline__ void pf_nb4(const double* f, int k2, int e2, int l, int L, int nt) {
+  const int a = EV0(k2), b = EV1(k2);
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)a * L + l) * nt + e2));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)b * L + l) * nt + e2));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)(3 + a) * L + l) * nt + e2));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)(3 + b) * L + l) * nt + e2));
+}
+
 // the 4 lateral nodes (t0, t1, b0, b1) of the neighbour prism across local edge k2 of column e2
 __device__ __forceinline__ void ld_nb4(const double* __restrict__ f, int k2, int e2, int l, int L, int nt,
                                        double n4[4]) {

@@ -671,6 +671,11 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
   double gp[6][NC];
   for (int l = 0; l < L; ++l) {
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    if (l + 2 < L) pf6(a.wt, l + 2, c, L, nt);
+    if (l + 1 < L) {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) pf6(rhs + cc * P6, l + 1, c, L, nt);
+    }
     if (l < L - 1) vgeo(C, eta, fb, m.fracs[l + 2], a.kh, a.kv, Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
     ld6(a.wt, l, c, L, nt, wt);
@@ -764,6 +769,12 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) xn[i][cc] = gp[i][cc];
   for (int l = L - 2; l >= 0; --l) {
+    if (l > 0) {
+#pragma unroll
+      for (int e = 0; e < 36; e += 6) pf6(Gs + (size_t)e * L * nt, l - 1, c, L, nt);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) pf6(x + cc * P6, l - 1, c, L, nt);
+    }
     double xl[6][NC];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
@@ -823,6 +834,15 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
   }
   for (int l = 0; l < L; ++l) {
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    if (l + 2 < L) {
+      pf6(a.wt, l + 2, c, L, nt);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) pf6(xin + cc * P6, l + 2, c, L, nt);
+    }
+    if (l + 1 < L) {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) pf6(rhs + cc * P6, l + 1, c, L, nt);
+    }
     if (l < L - 1) {
       vgeo(C, eta, fb, m.fracs[l + 2], a.kh, a.kv, Vn);
 #pragma unroll

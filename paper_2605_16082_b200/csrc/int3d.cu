@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
   for (int l = 0; l < L; ++l) {
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     const double jm = 0.5 * (fb - ft);
+    if (l + 1 < L) pf6(rhoT, l + 1, c, L, nt);
     LGeo G;
     layer_geo(C, eta, ft, fb, G);
     double rho[6];
@@ -600,6 +601,10 @@ __global__ void __launch_bounds__(128, MINB) k_compute_wtilde(DMesh m, const dou
   double s[3] = {0, 0, 0};
   for (int l = L - 1; l >= 0; --l) {
     const double jm = 0.5 * (m.fracs[l + 1] - m.fracs[l]);
+    if (l > 0) {
+      pf6(qb, l - 1, c, L, nt);
+      pf6(qb + P6, l - 1, c, L, nt);
+    }
     double qv[2][6];
     ld6(qb, l, c, L, nt, qv[0]);
     ld6(qb + P6, l, c, L, nt, qv[1]);

@@ -72,6 +72,46 @@ class Mesh2D:
         return self.n_interior_edges() + int(np.count_nonzero(self.nbr < 0))
 
     def _finish(self) -> "Mesh2D":
+        """Geometry + adjacency: on the GPU (csrc/mesh.cu) when one is present, else on the host."""
+        if _gpu():
+            return self._finish_device()
+        return self._finish_host()
+
+    def _finish_device(self) -> "Mesh2D":
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        from .device import stream_ptr
+        from .errors import raise_for_code
+        dev = torch.device("cuda", torch.cuda.current_device())
+        nt = self.nt
+        f = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)  # noqa: E731
+        vx, vy, vb = f(self.vx), f(self.vy), f(self.vb)
+        tri = torch.as_tensor(np.ascontiguousarray(self.tri, dtype=np.int64), device=dev)
+        out = {k: torch.empty((nt, 3), dtype=torch.float64, device=dev)
+               for k in ("x", "y", "b", "dphx", "dphy", "elen", "enx", "eny")}
+        out["j2d"] = torch.empty(nt, dtype=torch.float64, device=dev)
+        ints = {k: torch.empty((nt, 3), dtype=torch.int64, device=dev) for k in ("nbr", "nbrk", "btag")}
+        err = torch.zeros(4, dtype=torch.int64, device=dev)
+        p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(_lib.lib().pdg_mesh_build(nt, self.nv, p(vx), p(vy), p(vb), p(tri), p(out["x"]), p(out["y"]),
+                                             p(out["b"]), p(out["j2d"]), p(out["dphx"]), p(out["dphy"]),
+                                             p(out["elen"]), p(out["enx"]), p(out["eny"]), p(ints["nbr"]),
+                                             p(ints["nbrk"]), p(ints["btag"]), p(err), stream_ptr()), "mesh_build")
+        h = err.cpu()
+        if int(h[0]) & 0xFFFFFFFF:
+            raise_for_code(int(h[0]) & 0xFFFFFFFF, int(h[1]), int(h[2]), float(h[3:4].view(torch.float64).item()))
+        for k, v in out.items():
+            setattr(self, k, v.cpu().numpy())
+        for k, v in ints.items():
+            setattr(self, k, v.cpu().numpy())
+        if self.hilbert_perm is None:
+            self.hilbert_perm = np.arange(self.nt)
+        return self
+
+    def _finish_host(self) -> "Mesh2D":
         t = self.tri
         X, Y = self.vx[t], self.vy[t]
         self.x, self.y, self.b = X, Y, self.vb[t]
@@ -123,6 +163,18 @@ class Mesh2D:
         return m
 
 
+def _gpu() -> bool:
+    import os
+    if os.environ.get("PDG_MESH_HOST"):        # CPU-only processes (the oracle baseline workers)
+        return False
+    try:
+        import torch
+        from . import _lib
+        return torch.cuda.is_available() and _lib.lib() is not None
+    except Exception:
+        return False
+
+
 def make_mesh(vx, vy, vb, tri) -> Mesh2D:
     """mesh.py:140-147."""
     return Mesh2D(vx=np.asarray(vx, float), vy=np.asarray(vy, float), vb=np.asarray(vb, float),
@@ -166,7 +218,42 @@ def hilbert_index(order: int, ix, iy) -> np.ndarray:
 
 
 def hilbert_reorder(mesh: Mesh2D, order: int = 16) -> Mesh2D:
-    """mesh.py:210-228 (stable, idempotent)."""
+    """mesh.py:210-228 (stable, idempotent); the permutation is computed on the GPU when present."""
+    if _gpu():
+        perm = hilbert_perm_device(mesh, order)
+        out = make_mesh(mesh.vx, mesh.vy, mesh.vb, mesh.tri[perm])
+        out.hilbert_perm = perm
+        return out
+    cx, cy = mesh.x.mean(axis=1), mesh.y.mean(axis=1)
+    n = np.int64(1) << order
+    sx = max(cx.max() - cx.min(), 1e-300)
+    sy = max(cy.max() - cy.min(), 1e-300)
+    ix = np.minimum(n - 1, ((cx - cx.min()) / sx * (n - 1)).astype(np.int64))
+    iy = np.minimum(n - 1, ((cy - cy.min()) / sy * (n - 1)).astype(np.int64))
+    perm = np.argsort(hilbert_index(order, ix, iy), kind="stable")
+    out = make_mesh(mesh.vx, mesh.vy, mesh.vb, mesh.tri[perm])
+    out.hilbert_perm = perm
+    return out
+
+
+def hilbert_perm_device(mesh, order: int = 16) -> np.ndarray:
+    """hilbert_reorder's permutation computed on the GPU (csrc/mesh.cu: pdg_hilbert_perm)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import stream_ptr
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = torch.as_tensor(np.ascontiguousarray(mesh.x), device=dev)
+    y = torch.as_tensor(np.ascontiguousarray(mesh.y), device=dev)
+    perm = torch.empty(mesh.nt, dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().pdg_hilbert_perm(mesh.nt, order, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                           ctypes.c_void_p(perm.data_ptr()), stream_ptr()), "hilbert_perm")
+    return perm.cpu().numpy()
+
+
+def hilbert_reorder_host(mesh: Mesh2D, order: int = 16) -> Mesh2D:
     cx, cy = mesh.x.mean(axis=1), mesh.y.mean(axis=1)
     n = np.int64(1) << order
     sx = max(cx.max() - cx.min(), 1e-300)
