@@ -40,6 +40,7 @@ KERNEL_BYTES = {
     "wtilde": 96 + 48,                  # read q, write w~
     "rhs_u": 96 * 4 + 96,               # read u, u0, q, r; write rhs
     "rhs_T": 48 + 48 + 96 + 48,         # read T, T0, q; write rhs
+    "rhs_uT": 96 * 4 + 96 + 48 * 2 + 48,  # read u, u0, q, r, T, T0; write rhs_u, rhs_T
     "vertical_u_impl": 96 + 48 + 96,    # read rhs, w~; write u1
     "vertical_T_impl": 48 + 48 + 48,
     "vertical_u_expl": 96 + 48 + 96 + 96,   # + u for A u

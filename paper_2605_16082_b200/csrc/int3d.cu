@@ -687,6 +687,10 @@ struct HArgs {
   const double* f2d;     // STAGE momentum: [2][3][nt]
   double g, f, rho0, tsx, tsy, cd, dt;
   int mass_terms;
+  // per-component planes (momentum x, y[, tracer]); filled from u / u0 / out by the entry points
+  const double* uc[3];
+  const double* u0c[3];
+  double* outc[3];
 };
 
 __device__ __forceinline__ void mjz(const double jz[3], double M[3][3]) {
@@ -751,7 +755,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
   if (MODE == 2) {
     load_eta(a.eta0, c, nt, eta0);
     load_eta(a.eta1, c, nt, eta1);
-    if constexpr (NC == 2) {
+    if constexpr (NC >= 2) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const double H1 = eta1[k] - C.b[k];
@@ -771,7 +775,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
     const double jm = 0.5 * (fb - ft);
     double u[NC][6], qv[2][6];
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) ld6(a.u + cc * P6, l, c, L, nt, u[cc]);
+    for (int cc = 0; cc < NC; ++cc) ld6(a.uc[cc], l, c, L, nt, u[cc]);
     ld6(a.qa, l, c, L, nt, qv[0]);
     ld6(a.qa + P6, l, c, L, nt, qv[1]);
     if (MODE == 2) {
@@ -836,7 +840,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double n4[4], ti[2][2], te[2][2], x[2][2];
-        ld_nb4(a.u + cc * P6, E[k].k2, E[k].e2, l, L, nt, n4);
+        ld_nb4(a.uc[cc], E[k].k2, E[k].e2, l, L, nt, n4);
         tr_own(u[cc], k, ti);
         tr_nb(n4, te);
 #pragma unroll
@@ -849,7 +853,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
     double Mu[3][3];
     bool have_mu = false;
     // Coriolis f M (u_y, -u_x) and -M r / rho0 (momentum), internal3d.py:746-750
-    if constexpr (NC == 2) {
+    if constexpr (NC >= 2) {
       if (MODE != 0 || a.mass_terms) {
         double rr[2][6];
         ld6(a.r, l, c, L, nt, rr[0]);
@@ -901,7 +905,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
     }
     (void)have_mu;
     // surface wind and bottom drag (internal3d.py:919-934)
-    if constexpr (NC == 2 && MODE != 0) {
+    if constexpr (NC >= 2 && MODE != 0) {
       if (l == 0) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -913,7 +917,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
         double dx3[3], dy3[3], mx[3], my[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const double ubx = u[0][3 + k], uby = u[NC - 1][3 + k];
+          const double ubx = u[0][3 + k], uby = u[1][3 + k];
           const double sp = sqrt(ubx * ubx + uby * uby);
           dx3[k] = -a.cd * sp * ubx;
           dy3[k] = -a.cd * sp * uby;
@@ -923,7 +927,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           acc[0][3 + k] += mx[k];
-          acc[NC - 1][3 + k] += my[k];
+          acc[1][3 + k] += my[k];
         }
       }
     }
@@ -936,8 +940,8 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
       double j0[3], M0[3][3];
       layer_jz(C.b, eta0, ft, fb, j0);
       mjz(j0, M0);
-      double mf[2][3];
-      if constexpr (NC == 2) {
+      double mf[2][3] = {{0, 0, 0}, {0, 0, 0}};
+      if constexpr (NC >= 2) {
         double j1[3], M1[3][3];
         layer_jz(C.b, eta1, ft, fb, j1);
         mjz(j1, M1);
@@ -950,20 +954,20 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double x0[6], m0x[6], o[6];
-        ld6(a.u0 + cc * P6, l, c, L, nt, x0);
+        ld6(a.u0c[cc], l, c, L, nt, x0);
         kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
-          if constexpr (NC == 2)
+          if (NC >= 2 && cc < 2)
             o[n] = m0x[n] + a.dt * (acc[cc][n] + mf[cc][n % 3]);
           else
             o[n] = m0x[n] + a.dt * acc[cc][n];
         }
-        st6(out + cc * P6, l, c, L, nt, o);
+        st6(a.outc[cc], l, c, L, nt, o);
       }
     } else {
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) st6(out + cc * P6, l, c, L, nt, acc[cc]);
+      for (int cc = 0; cc < NC; ++cc) st6(a.outc[cc], l, c, L, nt, acc[cc]);
     }
   }
   if (MODE == 1) {
@@ -1161,6 +1165,13 @@ int pdg_horizontal_rhs(pdg_ctx* ctx, const double* eta_g, const double* u, int n
   HArgs a{};
   a.eta_u = eta_g;
   a.u = u;
+  {
+    const size_t P6 = (size_t)6 * ctx->L * ctx->nt;
+    for (int cc = 0; cc < ncomp; ++cc) {
+      a.uc[cc] = u + cc * P6;
+      a.outc[cc] = out + cc * P6;
+    }
+  }
   a.qa = q_adv;
   a.fac = fac;
   a.r = r;
@@ -1197,6 +1208,11 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   HArgs a{};
   a.eta_u = eta_u;
   a.u = u;
+  {
+    const size_t P6 = (size_t)6 * ctx->L * ctx->nt;
+    a.uc[0] = u;
+    a.uc[1] = u + P6;
+  }
   a.qa = q;
   a.r = r;
   a.g = g;
@@ -1226,6 +1242,14 @@ int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta
   a.eta1 = eta1;
   a.u = u;
   a.u0 = u0;
+  {
+    const size_t P6 = (size_t)6 * ctx->L * ctx->nt;
+    for (int cc = 0; cc < (ncomp == 1 ? 1 : 2); ++cc) {
+      a.uc[cc] = u + cc * P6;
+      a.u0c[cc] = u0 + cc * P6;
+      a.outc[cc] = out + cc * P6;
+    }
+  }
   a.qa = q;
   a.mis = mis;
   a.r = r;
@@ -1246,6 +1270,46 @@ int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta
   } else {
     DISPATCH_MINB(TUNE_HRHS, k_hrhs, 1, 2)
   }
+#undef LAUNCH_ARGS
+  return check_launch(ctx);
+}
+
+// momentum AND tracer stage right-hand sides in one pass (they share q~, the flux factor and the
+// masses): rhs_u = M0 u0 + dt (F_h(u, q~) + stress + M1 F2D/H1), rhs_T = M0 T0 + dt F_T(T, q~)
+int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, const double* u,
+                    const double* T, const double* u0, const double* T0, const double* q, const double* mis,
+                    const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
+                    double cd, double dt, double* out_u, double* out_T, void* stream) {
+  HArgs a{};
+  a.eta_u = eta_u;
+  a.eta0 = eta0;
+  a.eta1 = eta1;
+  const size_t P6 = (size_t)6 * ctx->L * ctx->nt;
+  a.uc[0] = u;
+  a.uc[1] = u + P6;
+  a.uc[2] = T;
+  a.u0c[0] = u0;
+  a.u0c[1] = u0 + P6;
+  a.u0c[2] = T0;
+  a.outc[0] = out_u;
+  a.outc[1] = out_u + P6;
+  a.outc[2] = out_T;
+  a.qa = q;
+  a.mis = mis;
+  a.r = r;
+  a.f2d = f2d;
+  a.g = g;
+  a.f = f;
+  a.rho0 = rho0;
+  a.tsx = tsx;
+  a.tsy = tsy;
+  a.cd = cd;
+  a.dt = dt;
+  Cols cs{nullptr, ctx->nown};
+  const dim3 grid(nblocks(cs.n, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
+#define LAUNCH_ARGS ctx->view(), a, cs, out_u
+  DISPATCH_MINB(TUNE_HRHS, k_hrhs, 3, 2)
 #undef LAUNCH_ARGS
   return check_launch(ctx);
 }

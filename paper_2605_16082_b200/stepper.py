@@ -73,6 +73,7 @@ class ImexStepper:
         self.graphs = {}
         self.use_graph = True
         self.prof = None       # {name: [(start_event, end_event), ...]} when profiling
+        self.fuse_rhs = True   # momentum + tracer stage right-hand sides in one kernel
 
     def _c(self, name, rc):
         _lib.check(rc, name)
@@ -149,10 +150,15 @@ class ImexStepper:
             yield [self.mis]
         tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
            ptr(self.wt), s)
-        tm("rhs_u", lb.pdg_step_rhs, h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q),
-           ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s)
-        tm("rhs_T", lb.pdg_step_rhs, h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q),
-           ptr(self.mis), None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s)
+        if self.fuse_rhs:
+            tm("rhs_uT", lb.pdg_step_rhs_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(T), ptr(u0), ptr(T0),
+               ptr(self.q), ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s,
+               ptr(out_u), ptr(out_T), s)
+        else:
+            tm("rhs_u", lb.pdg_step_rhs, h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q),
+               ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s)
+            tm("rhs_T", lb.pdg_step_rhs, h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q),
+               ptr(self.mis), None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s)
         pe = self.pen
         tm(f"vertical_u_{tag}", lb.pdg_step_vertical, h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
