@@ -650,6 +650,7 @@ __device__ __forceinline__ void lu6r_solve(const double a[6][6], const double rp
 template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, double dt, const double* rhs,
                                                    double* __restrict__ Gs, double* x) {
+  asm volatile(".pragma \"enable_smem_spilling\";");
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
   if (c >= m.nown) return;
@@ -709,11 +710,20 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) g[i][cc] = rhs[cc * P6 + ((size_t)i * L + l) * nt + c];
     if (l > 0) {
+      // previous layer's tile, stored contiguously per prism ([l][c][36], row-major 6x6)
+      const double2* gq = reinterpret_cast<const double2*>(Gs + ((size_t)(l - 1) * nt + c) * 36);
+      double Gp[36];
+#pragma unroll
+      for (int e = 0; e < 18; ++e) {
+        const double2 v = gq[e];
+        Gp[2 * e] = v.x;
+        Gp[2 * e + 1] = v.y;
+      }
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
         double G[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = Gs[((size_t)(k * 6 + j) * L + (l - 1)) * nt + c];
+        for (int k = 0; k < 6; ++k) G[k] = Gp[k * 6 + j];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           double acc = 0.0;
@@ -739,18 +749,27 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
       return;
     }
     if (l < L - 1) {
+      // G_l = Dtilde^-1 [0; W]: the top three RHS rows are zero, so forward substitution
+      // starts at row 3; tiles go to the per-prism-contiguous workspace with 16-byte stores
+      double Gn[36];
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
-        double t[6][1];
+        double t3 = -dt * w[0][j], t4 = -dt * w[1][j], t5 = -dt * w[2][j];
+        t4 = t4 - d[4][3] * t3;
+        t5 = t5 - d[5][3] * t3 - d[5][4] * t4;
+        double x[6];
+        x[5] = t5 * rp[5];
+        x[4] = (t4 - d[4][5] * x[5]) * rp[4];
+        x[3] = (t3 - d[3][4] * x[4] - d[3][5] * x[5]) * rp[3];
+        x[2] = (0.0 - d[2][3] * x[3] - d[2][4] * x[4] - d[2][5] * x[5]) * rp[2];
+        x[1] = (0.0 - d[1][2] * x[2] - d[1][3] * x[3] - d[1][4] * x[4] - d[1][5] * x[5]) * rp[1];
+        x[0] = (0.0 - d[0][1] * x[1] - d[0][2] * x[2] - d[0][3] * x[3] - d[0][4] * x[4] - d[0][5] * x[5]) * rp[0];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          t[i][0] = 0.0;
-          t[3 + i][0] = -dt * w[i][j];
-        }
-        lu6r_solve<1>(d, rp, t);
-#pragma unroll
-        for (int i = 0; i < 6; ++i) Gs[((size_t)(i * 6 + j) * L + l) * nt + c] = t[i][0];
+        for (int i = 0; i < 6; ++i) Gn[i * 6 + j] = x[i];
       }
+      double2* gq = reinterpret_cast<double2*>(Gs + ((size_t)l * nt + c) * 36);
+#pragma unroll
+      for (int e = 0; e < 18; ++e) gq[e] = make_double2(Gn[2 * e], Gn[2 * e + 1]);
     }
     lu6r_solve<NC>(d, rp, g);
 #pragma unroll
@@ -769,18 +788,20 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) xn[i][cc] = gp[i][cc];
   for (int l = L - 2; l >= 0; --l) {
-    if (l > 0) {
+    const double2* gq = reinterpret_cast<const double2*>(Gs + ((size_t)l * nt + c) * 36);
+    double Gt[36];
 #pragma unroll
-      for (int e = 0; e < 36; e += 6) pf6(Gs + (size_t)e * L * nt, l - 1, c, L, nt);
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) pf6(x + cc * P6, l - 1, c, L, nt);
+    for (int e = 0; e < 18; ++e) {
+      const double2 v = gq[e];
+      Gt[2 * e] = v.x;
+      Gt[2 * e + 1] = v.y;
     }
     double xl[6][NC];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       double G[6];
 #pragma unroll
-      for (int k = 0; k < 6; ++k) G[k] = Gs[((size_t)(i * 6 + k) * L + l) * nt + c];
+      for (int k = 0; k < 6; ++k) G[k] = Gt[i * 6 + k];
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double acc = 0.0;
@@ -803,6 +824,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, double dt, const double* rhs,
                                                    const double* __restrict__ xin, double* x) {
+  asm volatile(".pragma \"enable_smem_spilling\";");
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt, L = m.L;
   if (c >= m.nown) return;

@@ -194,33 +194,47 @@ __global__ void k_ext2d_eval(DMesh m, Ext2DIn a, const int* __restrict__ els, in
 // STAGE 0: Y = S0 + dt d(X);  1: Y = 3/4 S0 + 1/4 (X + dt d);  2: Y = S0/3 + 2/3 (X + dt d), qbar += Y.q
 template <int STAGE>
 __global__ void __launch_bounds__(256, 2) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
-                                                  double* Y, double dt, double* __restrict__ qbar) {
+                                                     double* Y, double dt, double* __restrict__ qbar) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
   if (c >= m.nown) return;
+  // issue the substep-start and Qbar loads first: they are independent of the flux work below,
+  // so their latency overlaps it instead of being exposed at the end (stages 1, 2)
+  double s0[3][3], qb[2][3];
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s0[f][k] = STAGE == 0 ? 0.0 : S0[(size_t)(f * 3 + k) * nt + c];
+  if (STAGE == 2) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) qb[f][k] = qbar[(size_t)(f * 3 + k) * nt + c];
+  }
   Col C;
   load_col(m, c, C);
   double r[3][3];
   ext2d_residual(m, C, c, a, r[0], r[1], r[2]);
-  const double* X[3] = {a.eta, a.qx, a.qy};
+  const double* X = nullptr;
+  (void)X;
 #pragma unroll
   for (int f = 0; f < 3; ++f) {
     double d[3];
     mh_inv3(r[f], C.j2d, d);
+    const double* Xf = f == 0 ? a.eta : (f == 1 ? a.qx : a.qy);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const size_t o = (size_t)(f * 3 + k) * nt + c;
-      const double s0 = S0[o];
       double y;
       if (STAGE == 0) {
-        y = s0 + dt * d[k];
+        y = S0[o] + dt * d[k];        // X == S0: this value is already in L1
       } else if (STAGE == 1) {
-        y = 0.75 * s0 + 0.25 * (X[f][k * nt + c] + dt * d[k]);
+        y = 0.75 * s0[f][k] + 0.25 * (Xf[k * nt + c] + dt * d[k]);
       } else {
-        y = s0 / 3.0 + (2.0 / 3.0) * (X[f][k * nt + c] + dt * d[k]);
+        y = s0[f][k] / 3.0 + (2.0 / 3.0) * (Xf[k * nt + c] + dt * d[k]);
       }
       Y[o] = y;
-      if (STAGE == 2 && f > 0) qbar[(size_t)((f - 1) * 3 + k) * nt + c] += y;
+      if (STAGE == 2 && f > 0) qbar[(size_t)((f - 1) * 3 + k) * nt + c] = qb[f - 1][k] + y;
     }
   }
 }

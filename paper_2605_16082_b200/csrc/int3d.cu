@@ -720,6 +720,7 @@ __device__ __forceinline__ void kron_apply(const double M[3][3], double j2d, con
 
 template <int NC, int MODE, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
+  asm volatile(".pragma \"enable_smem_spilling\";");
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cs.n) return;
   const int c = cs.col(i), nt = m.nt, L = m.L;
