@@ -101,8 +101,17 @@ __global__ void k_project(DMesh m, const double* __restrict__ eta_g, const doubl
         out[1][r] = rhs[r][1];
       }
     } else {
+      // one unpivoted LU of the jz-weighted triangle mass serves both levels and both components
       double Mh[3][3];
       mass_h(jzq, Mh);
+      const double r0 = 1.0 / Mh[0][0];
+      const double l10 = Mh[1][0] * r0, l20 = Mh[2][0] * r0;
+      const double a11 = Mh[1][1] - l10 * Mh[0][1], a12 = Mh[1][2] - l10 * Mh[0][2];
+      const double r1 = 1.0 / a11;
+      const double l21 = (Mh[2][1] - l20 * Mh[0][1]) * r1;
+      const double a22 = (Mh[2][2] - l20 * Mh[0][2]) - l21 * a12;
+      if (Mh[0][0] == 0.0 || a11 == 0.0 || a22 == 0.0) report(m.err, PDG_ERR_ZERO_PIVOT, l, 0, 0.0);
+      const double r2 = 1.0 / a22;
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -115,12 +124,11 @@ __global__ void k_project(DMesh m, const double* __restrict__ eta_g, const doubl
 #pragma unroll
             for (int a = 0; a < 3; ++a) R[a] += w * BARY[qq][a];
           }
-          double A[3][3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int bb = 0; bb < 3; ++bb) A[a][bb] = Mh[a][bb];
-          if (!solve3(A, R)) report(m.err, PDG_ERR_ZERO_PIVOT, l, 3 * lev, 0.0);
+          R[1] -= l10 * R[0];
+          R[2] -= l20 * R[0] + l21 * R[1];
+          R[2] *= r2;
+          R[1] = (R[1] - a12 * R[2]) * r1;
+          R[0] = (R[0] - Mh[0][1] * R[1] - Mh[0][2] * R[2]) * r0;
 #pragma unroll
           for (int a = 0; a < 3; ++a) out[cc][3 * lev + a] = R[a];
         }
@@ -1267,9 +1275,9 @@ int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out
   if (ncomp == 2) {
-    DISPATCH_MINB(TUNE_HRHS, k_hrhs, 2, 2)
+    DISPATCH_MINB(TUNE_HRHS2, k_hrhs, 2, 2)
   } else {
-    DISPATCH_MINB(TUNE_HRHS, k_hrhs, 1, 2)
+    DISPATCH_MINB(TUNE_HRHS2, k_hrhs, 1, 2)
   }
 #undef LAUNCH_ARGS
   return check_launch(ctx);
@@ -1310,7 +1318,7 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out_u
-  DISPATCH_MINB(TUNE_HRHS, k_hrhs, 3, 2)
+  DISPATCH_MINB(TUNE_HRHS2, k_hrhs, 3, 2)
 #undef LAUNCH_ARGS
   return check_launch(ctx);
 }

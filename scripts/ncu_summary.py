@@ -51,16 +51,31 @@ def launches(path):
     return "\n".join(out)
 
 
+HEADER = [True]
+
+
 def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     idx = {m: hdr.index(m) for m, _ in METRICS if m in hdr}
     ik = hdr.index("Kernel Name")
-    cols = [lbl + (f" ({units[idx[m]]})" if units[idx[m]] else "") for m, lbl in METRICS if m in idx]
-    out = ["| kernel | " + " | ".join(cols) + " |", "|---" * (len(cols) + 1) + "|"]
+    cols = [lbl for m, lbl in METRICS if m in idx]
+    out = ["| kernel | " + " | ".join(cols) + " |", "|---" * (len(cols) + 1) + "|"] if HEADER[0] else []
+    HEADER[0] = False
     for r in rows[2:]:
-        vals = [r[idx[m]] for m, _ in METRICS if m in idx]
+        vals = []
+        for m, _ in METRICS:
+            if m in idx:
+                v, u = r[idx[m]], units[idx[m]]
+                try:
+                    v = f"{float(v):.4g}"
+                except ValueError:
+                    pass
+                vals.append(v + (f" {u}" if u and u not in ("%", "inst", "warp", "register/thread") else ""))
         out.append(f"| `{short(r[ik])}` | " + " | ".join(vals) + " |")
     return "\n".join(out)
 
@@ -69,5 +84,6 @@ if __name__ == "__main__":
     print("## Launch list (ncu gpu__time_duration, --clock-control none; cold-cache, serialised)\n")
     print(launches(sys.argv[1]))
     if len(sys.argv) > 2:
-        print("\n## --set full capture of the top kernels\n")
-        print(full(sys.argv[2]))
+        print("\n## --set full capture (one launch per kernel family)\n")
+        for p in sys.argv[2:]:
+            print(full(p))

@@ -30,7 +30,7 @@ if __name__ == "__main__":
     st.step(1)
     res = {}
     for v in (1, 3, 4):
-        for key in range(5):
+        for key in range(6):
             lib.pdg_tune(key, v)
         res[v] = measure(st)
         print(v, json.dumps({k: round(x, 3) for k, x in res[v].items()}), flush=True)
