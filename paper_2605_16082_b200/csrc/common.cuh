@@ -86,6 +86,7 @@ struct DMesh {
   const int* nbrk;     // [3][nt]  neighbour's local edge
   const int* btag;     // [3][nt]  0 interior, 1 wall, 2 open
   const double* fracs; // [L+1]    sigma fractions (0 surface, 1 bed)
+  const int* ninfo;    // [3][nt]  packed (nbr << 4) | (nbrk << 2) | btag  (2D kernels)
   pdg_err* err;
 };
 
@@ -111,6 +112,36 @@ __device__ __forceinline__ void load_col(const DMesh& m, int c, Col& C) {
     C.nb[k] = __ldg(m.nbr + k * nt + c);
     C.nk[k] = __ldg(m.nbrk + k * nt + c);
     C.tag[k] = __ldg(m.btag + k * nt + c);
+  }
+}
+
+// lean per-triangle data of the 2D stage kernels: grad(phi) is rebuilt from the edge normals,
+// grad phi_i = -n_k len_k / J2D with k = (i+1) % 3 the edge opposite vertex i, and the
+// neighbour id / local edge / tag come packed in one int -- 116 instead of 188 bytes per triangle
+struct Col2 {
+  double j2d, dx[3], dy[3], el[3], nx[3], ny[3], b[3];
+  int nb[3], nk[3], tag[3];
+};
+__device__ __forceinline__ void load_col2(const DMesh& m, int c, Col2& C) {
+  const int nt = m.nt;
+  C.j2d = ldg(m.j2d + c);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    C.el[k] = ldg(m.elen + k * nt + c);
+    C.nx[k] = ldg(m.enx + k * nt + c);
+    C.ny[k] = ldg(m.eny + k * nt + c);
+    C.b[k] = ldg(m.b + k * nt + c);
+    const int info = __ldg(m.ninfo + k * nt + c);
+    C.tag[k] = info & 3;
+    C.nk[k] = (info >> 2) & 3;
+    C.nb[k] = info >> 4;
+  }
+  const double inv = 1.0 / C.j2d;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int k = i == 2 ? 0 : i + 1;
+    C.dx[i] = -(C.nx[k] * C.el[k]) * inv;
+    C.dy[i] = -(C.ny[k] * C.el[k]) * inv;
   }
 }
 

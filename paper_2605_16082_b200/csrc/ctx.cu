@@ -74,6 +74,16 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
   rc |= upload_int3(d->nbr, nt, &c->nbr);
   rc |= upload_int3(d->nbrk, nt, &c->nbrk);
   rc |= upload_int3(d->btag, nt, &c->btag);
+  {
+    std::vector<int> info((size_t)3 * nt);
+    for (int e = 0; e < nt; ++e)
+      for (int k = 0; k < 3; ++k) {
+        const long long nb = d->nbr[(size_t)e * 3 + k], nk = d->nbrk[(size_t)e * 3 + k], tg = d->btag[(size_t)e * 3 + k];
+        info[(size_t)k * nt + e] = (int)(((nb > 0 ? nb : 0) << 4) | ((nk > 0 ? nk : 0) << 2) | (tg & 3));
+      }
+    rc |= cudaMalloc(&c->ninfo, info.size() * sizeof(int)) != cudaSuccess;
+    rc |= cudaMemcpy(c->ninfo, info.data(), info.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  }
   rc |= cudaMalloc(&c->err, sizeof(pdg_err)) != cudaSuccess;
   rc |= cudaMemset(c->err, 0, sizeof(pdg_err)) != cudaSuccess;
   rc |= cudaMalloc(&c->red, 4096 * sizeof(double)) != cudaSuccess;
@@ -90,7 +100,7 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
 int pdg_ctx_destroy(pdg_ctx* c) {
   if (!c) return PDG_OK;
   void* ptrs[] = {c->j2d, c->dphx, c->dphy, c->elen, c->enx, c->eny, c->b, c->fracs,
-                  c->nbr, c->nbrk, c->btag, c->err, c->red, c->ws2d, c->ws3d};
+                  c->nbr, c->nbrk, c->btag, c->ninfo, c->err, c->red, c->ws2d, c->ws3d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;

@@ -12,7 +12,7 @@ struct pdg_ctx {
   double min_edge = 0.0;
   double *j2d = nullptr, *dphx = nullptr, *dphy = nullptr, *elen = nullptr, *enx = nullptr, *eny = nullptr,
          *b = nullptr, *fracs = nullptr;
-  int *nbr = nullptr, *nbrk = nullptr, *btag = nullptr;
+  int *nbr = nullptr, *nbrk = nullptr, *btag = nullptr, *ninfo = nullptr;
   pdg_err* err = nullptr;     // device error word
   double* red = nullptr;      // reduction scratch (device)
   double* ws2d = nullptr;     // 2D subcycle workspace: 2 stage states + q0
@@ -37,6 +37,7 @@ struct pdg_ctx {
     m.nbrk = nbrk;
     m.btag = btag;
     m.fracs = fracs;
+    m.ninfo = ninfo;
     m.err = err;
     return m;
   }

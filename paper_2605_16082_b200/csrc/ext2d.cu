@@ -20,7 +20,8 @@ struct Ext2DIn {
 };
 
 // residuals (before Mh^-1) of the free-surface and depth-momentum equations for column c
-__device__ __forceinline__ void ext2d_residual(const DMesh& m, const Col& C, int c, const Ext2DIn& a,
+template <class ColT>
+__device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, int c, const Ext2DIn& a,
                                                double re[3], double rx[3], double ry[3]) {
   const int nt = m.nt;
   const double g = a.g;
@@ -211,8 +212,8 @@ __global__ void __launch_bounds__(256, 2) k_rk_stage(DMesh m, Ext2DIn a, const d
 #pragma unroll
       for (int k = 0; k < 3; ++k) qb[f][k] = qbar[(size_t)(f * 3 + k) * nt + c];
   }
-  Col C;
-  load_col(m, c, C);
+  Col2 C;
+  load_col2(m, c, C);
   double r[3][3];
   ext2d_residual(m, C, c, a, r[0], r[1], r[2]);
   const double* X = nullptr;

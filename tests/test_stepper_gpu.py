@@ -115,3 +115,17 @@ def test_rest_state_fixed_point(pdg):
     st.step(10)
     g = st.get_state()
     assert max(np.abs(g["eta"]).max(), np.abs(g["ux"]).max(), np.abs(g["qx"]).max()) <= 1e-12
+
+
+def test_100_steps_baroclinic_parity(pdg):
+    """Lock-exchange-like baroclinic run (density front, wind, drag), 100 internal steps: <= 1e-9."""
+    L, dt, msub, kv, nu_v = 5, 20.0, 6, 1e-4, 1e-5
+    m, om, p, s0 = _setup(pdg, nx=8, ny=5, L=L, baroclinic=True)
+    st = pdg.stepper.ImexStepper(m, L, p, dt, msub, kv, nu_v)
+    st.set_state(**s0)
+    st.step(100)
+    st.check()
+    g = st.get_state()
+    o = _oracle_run(om, L, p, s0, 100, dt, msub, kv, nu_v)
+    for k, ref in [("ux", o.ux), ("uy", o.uy), ("T", o.T), ("eta", o.s2d.eta), ("qx", o.s2d.qx), ("qy", o.s2d.qy)]:
+        assert rel(g[k], ref) <= 1e-9, (k, rel(g[k], ref))
