@@ -45,6 +45,7 @@ KERNEL_BYTES = {
     "vertical_T_impl": 48 + 48 + 48,
     "vertical_u_expl": 96 + 48 + 96 + 96,   # + u for A u
     "vertical_T_expl": 48 + 48 + 48 + 48,
+    "vertical_uT_expl": 96 + 48 + 96 + 96 + 48 * 3,
 }
 # 2D RK stage per triangle: X 72 + S0 72 + geometry 188 + F3D->2D 48 + write 72 (+ Qbar 48 on stage 3)
 RK_STAGE_BYTES_PER_TRI = 72 + 72 + 188 + 48 + 72 + 16

@@ -211,6 +211,12 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
                       const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
                       double dt, const double* rhs, const double* xin, double* x, void* stream);
 
+/* explicit vertical stage of momentum (ncomp 2) and tracer in one pass */
+int pdg_step_vertical_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, double dt_mesh,
+                         const double* wt, double kh_u, double kv_u, double kh_T, double kv_T, double n0, int order,
+                         double dt, const double* rhs_u, const double* xin_u, double* x_u, const double* rhs_T,
+                         const double* xin_T, double* x_T, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

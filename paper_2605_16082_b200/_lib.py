@@ -69,6 +69,7 @@ _SIGS = {
     "pdg_solve_tridiagonal": (I, [I, I, P, P, P, P, P, P, P, P]),
     "pdg_assemble_vertical": (I, [P, P, P, P, D, D, D, I, P, I, P, P, P, P]),
     "pdg_step_vertical": (I, [P, I, I, P, P, P, D, P, D, D, D, I, D, P, P, P, P]),
+    "pdg_step_vertical_ut": (I, [P, P, P, P, D, P, D, D, D, D, D, I, D, P, P, P, P, P, P, P]),
 }
 
 _lib = None

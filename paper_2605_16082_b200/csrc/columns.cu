@@ -314,14 +314,13 @@ __global__ void k_tridiag(int nb, int n, const double* __restrict__ lo, const do
 // so a layer costs ~400 FMAs instead of the ~1500 of the literal 12-point contractions.
 struct VG {
   double R[3][3];  // symmetric
-  double kis;      // sum over the two vertical points of kv + kh |m_h/m_z|^2   (internal3d.py:838)
-  double kt, kb;   // kv + kh |grad z_top|^2, kv + kh |grad z_bot|^2           (:875-876)
-  double hgt;      // 2 mean(Jz)                                               (:888)
-  double nz;       // 1/sqrt(1 + |grad z_top|^2)                               (:891)
+  double m2a, m2b; // |m_h/m_z|^2 at the two vertical points (kappa_i = kv + kh m2, internal3d.py:838)
+  double tt, bb;   // |grad z_top|^2, |grad z_bot|^2                               (:875-876)
+  double hgt;      // 2 mean(Jz)                                                   (:888)
+  double nz;       // 1/sqrt(1 + |grad z_top|^2)                                   (:891)
 };
 
-__device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double ft, double fb, double kh, double kv,
-                                     VG& V) {
+__device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double ft, double fb, VG& V) {
   LGeo G;
   layer_geo(C, eta, ft, fb, G);
   double jzq[6], ij[6];
@@ -338,16 +337,15 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
       V.R[a][b] = s;
       V.R[b][a] = s;
     }
-  double ks = 0.0;
-#pragma unroll
-  for (int vv = 0; vv < 2; ++vv) {
-    const double mx = G.dzmid[0] + ZQP[vv] * G.djz[0], my = G.dzmid[1] + ZQP[vv] * G.djz[1];
-    ks += kv + kh * (mx * mx + my * my);
+  {
+    const double mx = G.dzmid[0] + ZQP[0] * G.djz[0], my = G.dzmid[1] + ZQP[0] * G.djz[1];
+    V.m2a = mx * mx + my * my;
+    const double nx = G.dzmid[0] + ZQP[1] * G.djz[0], ny = G.dzmid[1] + ZQP[1] * G.djz[1];
+    V.m2b = nx * nx + ny * ny;
   }
-  V.kis = ks;
   const double tt = G.dztop[0] * G.dztop[0] + G.dztop[1] * G.dztop[1];
-  V.kt = kv + kh * tt;
-  V.kb = kv + kh * (G.dzbot[0] * G.dzbot[0] + G.dzbot[1] * G.dzbot[1]);
+  V.tt = tt;
+  V.bb = G.dzbot[0] * G.dzbot[0] + G.dzbot[1] * G.dzbot[1];
   V.hgt = 2.0 * (((G.jz[0] + G.jz[1]) + G.jz[2]) / 3.0);
   V.nz = 1.0 / sqrt(1.0 + tt);
 }
@@ -372,22 +370,25 @@ __device__ __forceinline__ void face3(const double x[6], double F[3][3]) {
     }
 }
 
-// per-layer factorised pieces of A (all that vop_layer and vop_apply need)
-struct VPieces {
+// per-layer factorised pieces of A: the advective part (shared by momentum and tracer) ...
+struct VAdv {
   double Sa[2][3][3];   // advective volume per column level m (d[i][j] += DV[li] Sa[lj][ai][aj])
   double Ft[3][3];      // top face: pos part (whole speed at the surface)      -> d top-top (-)
   double Fn[3][3];      // top face: neg part (l >= 1)                           -> u[:,3:6] (-)
   double Fi[3][3];      // bottom face: inflow part (l <= L-2)                   -> d bot-bot (+)
   double Fo[3][3];      // bottom face: outflow part                             -> w[:,0:3] (+)
+};
+// ... and the diffusive part, one per (kh, kv)
+struct VDif {
   double cvol;          // J2D * kis                (diffusion volume coefficient on R_l)
   double ct, ca;        // 0.5 J2D kt_l (on R_l), 0.5 J2D kb_{l-1} (on R_{l-1})  (top face, l >= 1)
   double cb, cn;        // 0.5 J2D kb_l (on R_l), 0.5 J2D kt_{l+1} (on R_{l+1})  (bottom face, l <= L-2)
   double pt, pb;        // 0.5 x penalty factor of the top / bottom face
 };
+struct VPieces : VAdv, VDif {};
 
-__device__ __forceinline__ void vop_pieces(double j2d, int l, int L, const VG& Vp, const VG& V, const VG& Vn,
-                                           const double wt[6], const double wm[6], const double wtn[3], double n0,
-                                           int order, pdg_err* err, VPieces& P) {
+__device__ __forceinline__ void vop_adv(double j2d, int l, int L, const double wt[6], const double wm[6],
+                                        const double wtn[3], VAdv& P) {
   double dwt[3], dwb[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -442,18 +443,40 @@ __device__ __forceinline__ void vop_pieces(double j2d, int l, int L, const VG& V
         P.Fo[a][b] = 0.0;
       }
   }
-  P.cvol = j2d * V.kis;
-  P.ct = 0.5 * j2d * V.kt;
-  P.ca = 0.5 * j2d * Vp.kb;
-  P.cb = 0.5 * j2d * V.kb;
-  P.cn = 0.5 * j2d * Vn.kt;
-  P.pt = l > 0 ? 0.5 * (pen_sigma(V.hgt, Vp.hgt, n0, order, err) * fmax(V.kt, Vp.kb) * V.nz * j2d) : 0.0;
-  P.pb = l < L - 1 ? 0.5 * (pen_sigma(Vn.hgt, V.hgt, n0, order, err) * fmax(Vn.kt, V.kb) * Vn.nz * j2d) : 0.0;
+}
+
+__device__ __forceinline__ void vop_dif(double j2d, int l, int L, const VG& Vp, const VG& V, const VG& Vn, double kh,
+                                        double kv, double n0, int order, pdg_err* err, VDif& P) {
+  const double kis = (kv + kh * V.m2a) + (kv + kh * V.m2b);
+  const double kt = kv + kh * V.tt, kb = kv + kh * V.bb;
+  const double kbp = kv + kh * Vp.bb, ktn = kv + kh * Vn.tt;
+  P.cvol = j2d * kis;
+  P.ct = 0.5 * j2d * kt;
+  P.ca = 0.5 * j2d * kbp;
+  P.cb = 0.5 * j2d * kb;
+  P.cn = 0.5 * j2d * ktn;
+  P.pt = l > 0 ? 0.5 * (pen_sigma(V.hgt, Vp.hgt, n0, order, err) * fmax(kt, kbp) * V.nz * j2d) : 0.0;
+  P.pb = l < L - 1 ? 0.5 * (pen_sigma(Vn.hgt, V.hgt, n0, order, err) * fmax(ktn, kb) * Vn.nz * j2d) : 0.0;
+}
+
+__device__ __forceinline__ void vop_pieces(double j2d, int l, int L, const VG& Vp, const VG& V, const VG& Vn,
+                                           const double wt[6], const double wm[6], const double wtn[3], double kh,
+                                           double kv, double n0, int order, pdg_err* err, VPieces& P) {
+  vop_adv(j2d, l, L, wt, wm, wtn, P);
+  vop_dif(j2d, l, L, Vp, V, Vn, kh, kv, n0, order, err, P);
 }
 
 // explicit blocks of layer l: d (6x6), u (3x6, to layer l-1), w (3x6, to layer l+1)
-__device__ __forceinline__ void vop_blocks(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VPieces& P,
-                                           double d[6][6], double u[3][6], double w[3][6]) {
+__device__ __forceinline__ void vop_blocks(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VAdv& A,
+                                           const VDif& D, double d[6][6], double u[3][6], double w[3][6]) {
+  struct {
+    const double (&Sa)[2][3][3];
+    const double (&Ft)[3][3];
+    const double (&Fn)[3][3];
+    const double (&Fi)[3][3];
+    const double (&Fo)[3][3];
+    double cvol, ct, ca, cb, cn, pt, pb;
+  } P{A.Sa, A.Ft, A.Fn, A.Fi, A.Fo, D.cvol, D.ct, D.ca, D.cb, D.cn, D.pt, D.pb};
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
@@ -491,8 +514,17 @@ __device__ __forceinline__ void mv3(const double M[3][3], const double x[3], dou
 }
 
 // y = A x for layer l, matrix free: x rows of layers l-1 (xa), l (xc), l+1 (xb), 6 nodes each
-__device__ __forceinline__ void vop_apply(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VPieces& P,
-                                          const double xa[6], const double xc[6], const double xb[6], double y[6]) {
+__device__ __forceinline__ void vop_apply(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VAdv& A,
+                                          const VDif& D, const double xa[6], const double xc[6], const double xb[6],
+                                          double y[6]) {
+  struct {
+    const double (&Sa)[2][3][3];
+    const double (&Ft)[3][3];
+    const double (&Fn)[3][3];
+    const double (&Fi)[3][3];
+    const double (&Fo)[3][3];
+    double cvol, ct, ca, cb, cn, pt, pb;
+  } P{A.Sa, A.Ft, A.Fn, A.Fi, A.Fo, D.cvol, D.ct, D.ca, D.cb, D.cn, D.pt, D.pb};
   double t[3], s[3], dzc[3], r[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) dzc[a] = DV[0] * xc[a] + DV[1] * xc[3 + a];
@@ -576,11 +608,11 @@ __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __re
 #pragma unroll
   for (int k = 0; k < 3; ++k) eta[k] = a.eta_u[k * nt + c];
   VG Vp, V, Vn;
-  vgeo(C, eta, m.fracs[0], m.fracs[1], a.kh, a.kv, V);
+  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
   Vp = V;
   Vn = V;
   for (int l = 0; l < L; ++l) {
-    if (l < L - 1) vgeo(C, eta, m.fracs[l + 1], m.fracs[l + 2], a.kh, a.kv, Vn);
+    if (l < L - 1) vgeo(C, eta, m.fracs[l + 1], m.fracs[l + 2], Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
     ld6(a.wt, l, c, L, nt, wt);
     wm_layer(a, C.b, nullptr, nullptr, 0, 0, l, c, L, nt, wm);
@@ -589,9 +621,9 @@ __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __re
       for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
     }
     VPieces P;
-    vop_pieces(C.j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.n0, a.order, m.err, P);
+    vop_pieces(C.j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
     double d[6][6], u[3][6], w[3][6];
-    vop_blocks(l, L, Vp, V, Vn, P, d, u, w);
+    vop_blocks(l, L, Vp, V, Vn, P, P, d, u, w);
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
@@ -666,7 +698,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
   }
   const double j2d = C.j2d;
   VG Vp, V, Vn;
-  vgeo(C, eta, m.fracs[0], m.fracs[1], a.kh, a.kv, V);
+  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
   Vp = V;
   Vn = V;
   double gp[6][NC];
@@ -677,7 +709,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) pf6(rhs + cc * P6, l + 1, c, L, nt);
     }
-    if (l < L - 1) vgeo(C, eta, fb, m.fracs[l + 2], a.kh, a.kv, Vn);
+    if (l < L - 1) vgeo(C, eta, fb, m.fracs[l + 2], Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
     ld6(a.wt, l, c, L, nt, wt);
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
@@ -686,9 +718,9 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
       for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
     }
     VPieces P;
-    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.n0, a.order, m.err, P);
+    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
     double d[6][6], u[3][6], w[3][6];
-    vop_blocks(l, L, Vp, V, Vn, P, d, u, w);
+    vop_blocks(l, L, Vp, V, Vn, P, P, d, u, w);
     // M1 - dt A   (M1 = K (x) J2D Mjz(eta1))
     double jz1[3], M1h[3][3];
     layer_jz(C.b, e1, ft, fb, jz1);
@@ -841,7 +873,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
   const double j2d = C.j2d;
   const double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
   VG Vp, V, Vn;
-  vgeo(C, eta, m.fracs[0], m.fracs[1], a.kh, a.kv, V);
+  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
   Vp = V;
   Vn = V;
   double xa[NC][6], xc[NC][6], xb[NC][6];
@@ -866,7 +898,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
       for (int cc = 0; cc < NC; ++cc) pf6(rhs + cc * P6, l + 1, c, L, nt);
     }
     if (l < L - 1) {
-      vgeo(C, eta, fb, m.fracs[l + 2], a.kh, a.kv, Vn);
+      vgeo(C, eta, fb, m.fracs[l + 2], Vn);
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) ld6(xin + cc * P6, l + 1, c, L, nt, xb[cc]);
     }
@@ -878,7 +910,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
       for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
     }
     VPieces P;
-    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.n0, a.order, m.err, P);
+    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
     double jz1[3], A1[3][3];
     layer_jz(C.b, e1, ft, fb, jz1);
 #pragma unroll
@@ -900,7 +932,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
       double y[6], g[6];
-      vop_apply(l, L, Vp, V, Vn, P, xa[cc], xc[cc], xb[cc], y);
+      vop_apply(l, L, Vp, V, Vn, P, P, xa[cc], xc[cc], xb[cc], y);
       ld6(rhs + cc * P6, l, c, L, nt, g);
 #pragma unroll
       for (int k = 0; k < 6; ++k) y[k] = g[k] + dt * y[k];
@@ -923,6 +955,118 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
     }
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        xa[cc][k] = xc[cc][k];
+        xc[cc][k] = xb[cc][k];
+      }
+    Vp = V;
+    V = Vn;
+  }
+}
+
+// EXPLICIT stage for momentum (2 comps) AND tracer in one pass: the geometry window, the
+// advective pieces of A and the M1 factorisation are shared; only the diffusion pieces differ.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_vexplicit_ut(DMesh m, VopArgs a, double khT, double kvT, double dt,
+                                                            const double* rhs_u, const double* __restrict__ xin_u,
+                                                            double* x_u, const double* rhs_T,
+                                                            const double* __restrict__ xin_T, double* x_T) {
+  asm volatile(".pragma \"enable_smem_spilling\";");
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = m.nt, L = m.L;
+  if (c >= m.nown) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3], e0[3], e1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    eta[k] = a.eta_u[k * nt + c];
+    e0[k] = a.eta0[k * nt + c];
+    e1[k] = a.eta1[k * nt + c];
+  }
+  const double j2d = C.j2d;
+  const double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
+  const double* xin[3] = {xin_u, xin_u + P6, xin_T};
+  const double* rhs[3] = {rhs_u, rhs_u + P6, rhs_T};
+  double* xo[3] = {x_u, x_u + P6, x_T};
+  VG Vp, V, Vn;
+  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
+  Vp = V;
+  Vn = V;
+  double xa[3][6], xc[3][6], xb[3][6];
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    ld6(xin[cc], 0, c, L, nt, xc[cc]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      xa[cc][k] = 0.0;
+      xb[cc][k] = 0.0;
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    if (l < L - 1) {
+      vgeo(C, eta, fb, m.fracs[l + 2], Vn);
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) ld6(xin[cc], l + 1, c, L, nt, xb[cc]);
+    }
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
+    ld6(a.wt, l, c, L, nt, wt);
+    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if (l < L - 1) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+    }
+    VAdv A;
+    VDif Du, Dt;
+    vop_adv(j2d, l, L, wt, wm, wtn, A);
+    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, Du);
+    vop_dif(j2d, l, L, Vp, V, Vn, khT, kvT, a.n0, a.order, m.err, Dt);
+    double jz1[3], A1[3][3];
+    layer_jz(C.b, e1, ft, fb, jz1);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p; q < 3; ++q) {
+        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+        A1[p][q] = s;
+        A1[q][p] = s;
+      }
+    const double r0 = 1.0 / A1[0][0];
+    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
+    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
+    const double a22p = A1[2][2] - l20 * A1[0][2];
+    const double r1 = 1.0 / a11;
+    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
+    const double r2 = 1.0 / (a22p - l21 * a12);
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      double y[6], g[6];
+      vop_apply(l, L, Vp, V, Vn, A, cc < 2 ? Du : Dt, xa[cc], xc[cc], xb[cc], y);
+      ld6(rhs[cc], l, c, L, nt, g);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) y[k] = g[k] + dt * y[k];
+      double o[6];
+#pragma unroll
+      for (int lev = 0; lev < 2; ++lev) {
+        double z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          z[k] = lev == 0 ? (KM[1][1] * y[k] - KM[0][1] * y[3 + k]) / det : (-KM[1][0] * y[k] + KM[0][0] * y[3 + k]) / det;
+        z[1] -= l10 * z[0];
+        z[2] -= l20 * z[0] + l21 * z[1];
+        z[2] *= r2;
+        z[1] = (z[1] - a12 * z[2]) * r1;
+        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
+      }
+      st6(xo[cc], l, c, L, nt, o);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
         xa[cc][k] = xc[cc][k];
@@ -1034,6 +1178,24 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     }
 #undef LAUNCH_ARGS
   }
+  return check_launch(ctx);
+}
+
+// explicit vertical stage of momentum and tracer together (shared geometry / advective operator)
+int pdg_step_vertical_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, double dt_mesh,
+                         const double* wt, double kh_u, double kv_u, double kh_T, double kv_T, double n0, int order,
+                         double dt, const double* rhs_u, const double* xin_u, double* x_u, const double* rhs_T,
+                         const double* xin_T, double* x_T, void* stream) {
+  VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, kh_u, kv_u, n0, order};
+  const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
+  cudaStream_t strm = (cudaStream_t)stream;
+#define LAUNCH_ARGS ctx->view(), a, kh_T, kv_T, dt, rhs_u, xin_u, x_u, rhs_T, xin_T, x_T
+  switch (tune_get(TUNE_VEXPL)) {
+    case 3: k_vexplicit_ut<3><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break;
+    case 4: k_vexplicit_ut<4><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break;
+    default: k_vexplicit_ut<1><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break;
+  }
+#undef LAUNCH_ARGS
   return check_launch(ctx);
 }
 

@@ -74,6 +74,7 @@ class ImexStepper:
         self.use_graph = True
         self.prof = None       # {name: [(start_event, end_event), ...]} when profiling
         self.fuse_rhs = True   # momentum + tracer stage right-hand sides in one kernel
+        self.fuse_vexpl = False  # momentum + tracer explicit vertical in one kernel (slower: register spills)
 
     def _c(self, name, rc):
         _lib.check(rc, name)
@@ -160,6 +161,13 @@ class ImexStepper:
             tm("rhs_T", lb.pdg_step_rhs, h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q),
                ptr(self.mis), None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s)
         pe = self.pen
+        if not implicit and self.fuse_vexpl:
+            tm("vertical_uT_expl", lb.pdg_step_vertical_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt),
+               p.kappa_h, self.kv, p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u),
+               ptr(out_T), ptr(T), ptr(out_T), s)
+            if part:
+                yield [out_u, out_T]
+            return eta1
         tm(f"vertical_u_{tag}", lb.pdg_step_vertical, h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
         tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
