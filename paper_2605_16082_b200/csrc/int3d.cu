@@ -987,6 +987,284 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Shared-memory variant of the stepper flavours (MODE 1, 2): the ~58 per-column constants live in
+// shared memory and are re-read (volatile) at the point of use instead of pinning ~120 registers
+// for the whole layer loop; 64-thread blocks keep the static footprint under 48 KB.
+namespace shf {
+enum { J2D = 0, DX = 1, DY = 4, EL = 7, NX = 10, NY = 13, B = 16, ETA = 19, STAB = 22, MO = 28, MN = 34, E0 = 46,
+       E1 = 49, F1 = 52, N = 58 };
+}
+
+__device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, double st1, int k, double jm,
+                                             const double qo[2][6], const double qn[2][4], double fac[2][2]) {
+  double o[6], n4[4];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) o[i] = nx * qo[0][i] + ny * qo[1][i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) n4[i] = nx * qn[0][i] + ny * qn[1][i];
+  double t[2][2];
+  tr_mean(o, k, n4, t);
+#pragma unroll
+  for (int vv = 0; vv < 2; ++vv) {
+    fac[vv][0] = t[vv][0] + jm * st0;
+    fac[vv][1] = t[vv][1] + jm * st1;
+  }
+}
+
+template <int NC, int MODE, int MINB>
+__global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
+  __shared__ double sdm[shf::N * 64];
+  __shared__ int sim[9 * 64];
+  const int tid = threadIdx.x;
+  const int i = blockIdx.x * 64 + tid;
+  if (i >= cs.n) return;  // no block-level synchronisation below: every thread owns its own slots
+  const int c = cs.col(i), nt = m.nt, L = m.L;
+  const size_t P6 = (size_t)6 * L * nt;
+  volatile double* S = sdm;
+#define SD(f) S[(f) * 64 + tid]
+  {
+    Col C;
+    load_col(m, c, C);
+    double eta[3];
+    load_eta(a.eta_u, c, nt, eta);
+    SD(shf::J2D) = C.j2d;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      SD(shf::DX + k) = C.dx[k];
+      SD(shf::DY + k) = C.dy[k];
+      SD(shf::EL + k) = C.el[k];
+      SD(shf::NX + k) = C.nx[k];
+      SD(shf::NY + k) = C.ny[k];
+      SD(shf::B + k) = C.b[k];
+      SD(shf::ETA + k) = eta[k];
+      EdgeNb E;
+      edge_setup(m, C, eta, a.eta_u, k, a.g, E);
+      sim[(0 + k) * 64 + tid] = C.tag[k];
+      sim[(3 + k) * 64 + tid] = E.e2;
+      sim[(6 + k) * 64 + tid] = E.k2;
+      if (C.tag[k] == 0) {
+        SD(shf::STAB + 2 * k) = E.stab[0];
+        SD(shf::STAB + 2 * k + 1) = E.stab[1];
+      }
+      if (MODE == 2) {
+        const double H = eta[k] - C.b[k];
+        SD(shf::MO + k) = a.mis[k * nt + c] * H;
+        SD(shf::MO + 3 + k) = a.mis[(3 + k) * nt + c] * H;
+        if (C.tag[k] == 0) {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            SD(shf::MN + (k * 2 + cc) * 2) = a.mis[(cc * 3 + EV0(E.k2)) * nt + E.e2] * E.hn[0];
+            SD(shf::MN + (k * 2 + cc) * 2 + 1) = a.mis[(cc * 3 + EV1(E.k2)) * nt + E.e2] * E.hn[1];
+          }
+        }
+      }
+    }
+    if (MODE == 2) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        SD(shf::E0 + k) = a.eta0[k * nt + c];
+        const double e1 = a.eta1[k * nt + c];
+        SD(shf::E1 + k) = e1;
+        if constexpr (NC >= 2) {
+          const double H1 = e1 - C.b[k];
+          SD(shf::F1 + k) = a.f2d[k * nt + c] / H1;
+          SD(shf::F1 + 3 + k) = a.f2d[(3 + k) * nt + c] / H1;
+        }
+      }
+    }
+  }
+  double csum[NC][3];
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
+  for (int l = 0; l < L; ++l) {
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    const double jm = 0.5 * (fb - ft);
+    double u[NC][6], qv[2][6];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) ld6(a.uc[cc], l, c, L, nt, u[cc]);
+    ld6(a.qa, l, c, L, nt, qv[0]);
+    ld6(a.qa + P6, l, c, L, nt, qv[1]);
+    if (MODE == 2) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jm * SD(shf::MO + cc * 3 + n % 3);
+    }
+    double acc[NC][6];
+    {
+      double z[2][2][3];
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev) mhq_vec(qv[d] + 3 * lev, z[d][lev]);
+      const double j2d = SD(shf::J2D);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double Sm[2][2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          double dot[2][2];
+#pragma unroll
+          for (int l1 = 0; l1 < 2; ++l1)
+#pragma unroll
+            for (int l2 = 0; l2 < 2; ++l2)
+              dot[l1][l2] = u[cc][3 * l1] * z[d][l2][0] + u[cc][3 * l1 + 1] * z[d][l2][1] + u[cc][3 * l1 + 2] * z[d][l2][2];
+#pragma unroll
+          for (int mm = 0; mm < 2; ++mm)
+            Sm[mm][d] = K3[mm][0][0] * dot[0][0] + K3[mm][0][1] * dot[0][1] + K3[mm][1][0] * dot[1][0] +
+                        K3[mm][1][1] * dot[1][1];
+        }
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+            acc[cc][3 * lev + p] = j2d * (SD(shf::DX + p) * Sm[lev][0] + SD(shf::DY + p) * Sm[lev][1]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (sim[k * 64 + tid] != 0) continue;
+      const int e2 = sim[(3 + k) * 64 + tid], k2 = sim[(6 + k) * 64 + tid];
+      double f[2][2];
+      {
+        double qn[2][4];
+        ld_nb4(a.qa, k2, e2, l, L, nt, qn[0]);
+        ld_nb4(a.qa + P6, k2, e2, l, L, nt, qn[1]);
+        if (MODE == 2) {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const double m0 = SD(shf::MN + (k * 2 + cc) * 2), m1 = SD(shf::MN + (k * 2 + cc) * 2 + 1);
+            qn[cc][0] = qn[cc][0] + jm * m0;
+            qn[cc][1] = qn[cc][1] + jm * m1;
+            qn[cc][2] = qn[cc][2] + jm * m0;
+            qn[cc][3] = qn[cc][3] + jm * m1;
+          }
+        }
+        lat_factor_v(SD(shf::NX + k), SD(shf::NY + k), SD(shf::STAB + 2 * k), SD(shf::STAB + 2 * k + 1), k, jm, qv,
+                     qn, f);
+      }
+      const double je = -(0.5 * SD(shf::EL + k));
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double n4[4], ti[2][2], te[2][2], x[2][2];
+        ld_nb4(a.uc[cc], k2, e2, l, L, nt, n4);
+        tr_own(u[cc], k, ti);
+        tr_nb(n4, te);
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) x[vv][h] = (f[vv][h] >= 0.0 ? ti[vv][h] : te[vv][h]) * f[vv][h];
+        lat_add(acc[cc], k, x, je);
+      }
+    }
+    double bb[3], eta[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      bb[k] = SD(shf::B + k);
+      eta[k] = SD(shf::ETA + k);
+    }
+    if constexpr (NC >= 2) {
+      double rr[2][6];
+      ld6(a.r, l, c, L, nt, rr[0]);
+      ld6(a.r + P6, l, c, L, nt, rr[1]);
+      double jz[3], Mu[3][3];
+      layer_jz(bb, eta, ft, fb, jz);
+      mjz(jz, Mu);
+      const double ir = 1.0 / a.rho0;
+      double y0[6], y1[6], m0[6], m1[6];
+#pragma unroll
+      for (int n = 0; n < 6; ++n) {
+        y0[n] = a.f * u[1][n] - rr[0][n] * ir;
+        y1[n] = -a.f * u[0][n] - rr[1][n] * ir;
+      }
+      const double j2d = SD(shf::J2D);
+      kron_apply(Mu, j2d, y0, m0);
+      kron_apply(Mu, j2d, y1, m1);
+#pragma unroll
+      for (int n = 0; n < 6; ++n) {
+        acc[0][n] += m0[n];
+        acc[1][n] += m1[n];
+      }
+      if (l == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          acc[0][k] += j2d / 6.0 * a.tsx;
+          acc[1][k] += j2d / 6.0 * a.tsy;
+        }
+      }
+      if (l == L - 1 && a.cd != 0.0) {
+        double dx3[3], dy3[3], mx[3], my[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double ubx = u[0][3 + k], uby = u[1][3 + k];
+          const double sp = sqrt(ubx * ubx + uby * uby);
+          dx3[k] = -a.cd * sp * ubx;
+          dy3[k] = -a.cd * sp * uby;
+        }
+        mh_apply3(dx3, j2d, mx);
+        mh_apply3(dy3, j2d, my);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          acc[0][3 + k] += mx[k];
+          acc[1][3 + k] += my[k];
+        }
+      }
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
+    } else {
+      const double j2d = SD(shf::J2D);
+      double e0[3], j0[3], M0[3][3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) e0[k] = SD(shf::E0 + k);
+      layer_jz(bb, e0, ft, fb, j0);
+      mjz(j0, M0);
+      double mf[2][3] = {{0, 0, 0}, {0, 0, 0}};
+      if constexpr (NC >= 2) {
+        double e1[3], j1[3], M1[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) e1[k] = SD(shf::E1 + k);
+        layer_jz(bb, e1, ft, fb, j1);
+        mjz(j1, M1);
+        const double kk = (KM[0][0] + KM[0][1]) * j2d;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const double F0 = SD(shf::F1 + cc * 3), F1v = SD(shf::F1 + cc * 3 + 1), F2 = SD(shf::F1 + cc * 3 + 2);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) mf[cc][p] = kk * (M1[p][0] * F0 + M1[p][1] * F1v + M1[p][2] * F2);
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double x0[6], m0x[6], o[6];
+        ld6(a.u0c[cc], l, c, L, nt, x0);
+        kron_apply(M0, j2d, x0, m0x);
+#pragma unroll
+        for (int n = 0; n < 6; ++n) {
+          if (NC >= 2 && cc < 2)
+            o[n] = m0x[n] + a.dt * (acc[cc][n] + mf[cc][n % 3]);
+          else
+            o[n] = m0x[n] + a.dt * acc[cc][n];
+        }
+        st6(a.outc[cc], l, c, L, nt, o);
+      }
+    }
+  }
+  if (MODE == 1) {
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) out[(cc * 3 + k) * nt + c] = csum[cc][k];
+  }
+#undef SD
+}
+
 // Coriolis and -M r / rho0 over all prisms (the reference applies them to every row even
 // when `els` restricts the advective part, internal3d.py:745-750)
 __global__ void k_mass_terms(int L, int nt, const double* __restrict__ mass, const double* __restrict__ u,
@@ -1234,7 +1512,17 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, f3d2d
-  DISPATCH_MINB(TUNE_HRHS, k_hrhs, 2, 1)
+  if (tune_get(TUNE_HRHS) >= 8) {
+    const int t = tune_get(TUNE_HRHS);
+    if (t == 9)
+      k_hrhs_s<2, 1, 6><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    else if (t == 10)
+      k_hrhs_s<2, 1, 8><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    else
+      k_hrhs_s<2, 1, 1><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+  } else {
+    DISPATCH_MINB(TUNE_HRHS, k_hrhs, 2, 1)
+  }
 #undef LAUNCH_ARGS
   return check_launch(ctx);
 }
@@ -1318,7 +1606,17 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out_u
-  DISPATCH_MINB(TUNE_HRHS2, k_hrhs, 3, 2)
+  if (tune_get(TUNE_HRHS2) >= 8) {
+    const int t = tune_get(TUNE_HRHS2);
+    if (t == 9)
+      k_hrhs_s<3, 2, 6><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    else if (t == 10)
+      k_hrhs_s<3, 2, 8><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    else
+      k_hrhs_s<3, 2, 1><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+  } else {
+    DISPATCH_MINB(TUNE_HRHS2, k_hrhs, 3, 2)
+  }
 #undef LAUNCH_ARGS
   return check_launch(ctx);
 }

@@ -29,8 +29,10 @@ if __name__ == "__main__":
     st.use_graph = False
     st.step(1)
     res = {}
-    for v in (1, 3, 4):
-        for key in range(6):
+    variants = [int(v) for v in sys.argv[1:]] or [1, 3, 4]
+    keys = [0, 5] if sys.argv[1:] else range(6)
+    for v in variants:
+        for key in keys:
             lib.pdg_tune(key, v)
         res[v] = measure(st)
         print(v, json.dumps({k: round(x, 3) for k, x in res[v].items()}), flush=True)
