@@ -292,8 +292,16 @@ def main():
                   "bytes": b}
     dom = max((k for k in per if per[k]["bytes"]), key=lambda k: per[k]["ms"] * counts[k])
     ach = per[dom]["GBps"]
+    traffic, traffic_src = None, None
+    try:   # DRAM read+write bytes of one launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            tr = json.load(f).get(dom)
+        if tr and args.config == "c4" and world == 1:
+            traffic, traffic_src = tr["dram_bytes"], tr["source"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "peak_kind": peak_kind, "traffic": None,
+                "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                 "bytes_per_launch": per[dom]["bytes"], "launch_ms": per[dom]["ms"],
                 "step_model_M2": {"bytes_per_prism": M2_BYTES_PER_PRISM(case.L, case.m),
                                   "frac": M2_BYTES_PER_PRISM(case.L, case.m) * P / world / (t_ms * 1e-3) / 1e9 / hbm}}
