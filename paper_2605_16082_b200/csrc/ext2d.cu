@@ -193,8 +193,8 @@ __global__ void k_ext2d_eval(DMesh m, Ext2DIn a, const int* __restrict__ els, in
 
 // one SSP-RK3 stage: X = state evaluated, S0 = substep start (3 fields x C3), Y = output.
 // STAGE 0: Y = S0 + dt d(X);  1: Y = 3/4 S0 + 1/4 (X + dt d);  2: Y = S0/3 + 2/3 (X + dt d), qbar += Y.q
-template <int STAGE>
-__global__ void __launch_bounds__(256, 2) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
+template <int STAGE, int BS = 256, int MINB = 2>
+__global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
                                                      double* Y, double dt, double* __restrict__ qbar) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
@@ -396,21 +396,30 @@ int pdg_ext2d_subcycle(pdg_ctx* ctx, double* S, int msub, double dt, double g, d
       cudaSuccess)
     return PDG_ERR_CUDA;
   if (cudaMemsetAsync(qbar, 0, (size_t)6 * nt * sizeof(double), s) != cudaSuccess) return PDG_ERR_CUDA;
-  const int bs = 256, nb = nblocks(ctx->nown, bs);
+  const int variant = tune_get(TUNE_RK);
+  const int bs = variant == 2 || variant == 3 ? 128 : 256, nb = nblocks(ctx->nown, bs);
+#define RK_LAUNCH(ST, ...)                                                              \
+  switch (variant) {                                                                    \
+    case 2: k_rk_stage<ST, 128, 4><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
+    case 3: k_rk_stage<ST, 128, 3><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
+    case 4: k_rk_stage<ST, 256, 1><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
+    default: k_rk_stage<ST, 256, 2><<<nb, bs, 0, s>>>(__VA_ARGS__); break;              \
+  }
   for (int it = 0; it < msub; ++it) {
     const int hb = bc_vals != nullptr;
     Ext2DIn a{S, S + (size_t)3 * nt, S + (size_t)6 * nt, f3d2d, source, patm, hb, hb ? bc_vals[3 * it] : 0.0, g, rho0};
-    k_rk_stage<0><<<nb, bs, 0, s>>>(m, a, S, W1, dt, qbar);
+    RK_LAUNCH(0, m, a, S, W1, dt, qbar)
     if (check_launch(ctx)) return PDG_ERR_CUDA;
     Ext2DIn a1{W1, W1 + (size_t)3 * nt, W1 + (size_t)6 * nt, f3d2d, source, patm, hb,
                hb ? bc_vals[3 * it + 1] : 0.0, g, rho0};
-    k_rk_stage<1><<<nb, bs, 0, s>>>(m, a1, S, W2, dt, qbar);
+    RK_LAUNCH(1, m, a1, S, W2, dt, qbar)
     if (check_launch(ctx)) return PDG_ERR_CUDA;
     Ext2DIn a2{W2, W2 + (size_t)3 * nt, W2 + (size_t)6 * nt, f3d2d, source, patm, hb,
                hb ? bc_vals[3 * it + 2] : 0.0, g, rho0};
-    k_rk_stage<2><<<nb, bs, 0, s>>>(m, a2, S, S, dt, qbar);
+    RK_LAUNCH(2, m, a2, S, S, dt, qbar)
     if (check_launch(ctx)) return PDG_ERR_CUDA;
   }
+#undef RK_LAUNCH
   k_subcycle_final<<<nb, bs, 0, s>>>(m, S, q0, f3d2d, msub, msub * dt, qbar, f2d);
   return check_launch(ctx);
 }
@@ -445,6 +454,7 @@ int pdg_ext2d_rk_stage(pdg_ctx* ctx, int stage, const double* X, const double* S
     k_rk_stage<1><<<nb, bs, 0, s>>>(m, a, S0, Y, dt, qbar);
   else
     k_rk_stage<2><<<nb, bs, 0, s>>>(m, a, S0, Y, dt, qbar);
+  (void)bs;
   return check_launch(ctx);
 }
 

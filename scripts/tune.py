@@ -30,7 +30,7 @@ if __name__ == "__main__":
     st.step(1)
     res = {}
     variants = [int(v) for v in sys.argv[1:]] or [1, 3, 4]
-    keys = [0, 5] if sys.argv[1:] else range(6)
+    keys = [int(k) for k in __import__("os").environ.get("TUNE_KEYS", "0,5").split(",")] if sys.argv[1:] else range(6)
     for v in variants:
         for key in keys:
             lib.pdg_tune(key, v)
