@@ -89,6 +89,10 @@ def lib():
                 continue
             fn.restype = res
             fn.argtypes = args
+        # PDG_TUNE="key=value,..." overrides the measured kernel-variant defaults (A/B runs)
+        for kv in filter(None, os.environ.get("PDG_TUNE", "").split(",")):
+            k, v = kv.split("=")
+            l.pdg_tune(int(k), int(v))
         _lib = l
     return _lib
 

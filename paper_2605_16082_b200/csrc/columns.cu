@@ -852,6 +852,263 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
   }
 }
 
+// ============================================================================ split block Thomas
+// Same elimination as k_vimplicit, but the propagation tile is kept in factored, compact form
+// and the back substitution is its own (low-register, high-occupancy) streaming kernel.
+//
+// The coupling of layer l to layer l+1 is [0; W_l] with W_l = -dt w_l (3x6) and, from
+// vop_blocks, w_l = [Fo + pb MHQ - DV0 cn R_{l+1}, -DV1 cn R_{l+1}] (all 3x3 blocks symmetric).
+// With S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}:
+//     W_l x = S0 x_top - S1 (DV0 x_top + DV1 x_bot)
+// so G_l = Dt_l^-1 [0; W_l] = E_l W_l with E_l = Dt_l^-1 [0; I3] (6x3).  The tile is
+// (E_l 18, S0 6, S1 6) = 30 doubles instead of 36, and forming E_l needs 3 (not 6) solves.
+// Tile layout: [l][30][nt] (one coalesced 8-byte word per lane per element).
+constexpr int VT = 30;
+constexpr int VBLK = 128;
+
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmetric 3x3
+  return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
+}
+
+// FORWARD: assembles M1 - dt A per layer, eliminates, writes the compact tile and g_l (into x).
+// Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
+// (each thread stages and reads only its own words: no barriers), issued two layers ahead;
+// the previous layer's tile lives in shared memory, not in registers or L2.
+template <int NC, int MINB>
+__global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, double dt, const double* rhs,
+                                                        double* __restrict__ Gs, double* x) {
+  
+  constexpr int NE = 6 * NC + 6;  // staged words per layer: rhs, w~
+  extern __shared__ double smem[];
+  double* ring = smem;                       // [3][NE][VBLK]
+  double* tl = smem + 3 * NE * VBLK;         // [VT][VBLK]
+  double* fr = tl + VT * VBLK;               // [L+1]
+  const int t = threadIdx.x;
+  const int c = blockIdx.x * VBLK + t;
+  const int nt = m.nt, L = m.L;
+  for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
+  __syncthreads();
+  if (c >= m.nown) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  auto stage = [&](int l) {
+    if (l < L) {
+      double* s = ring + (l % 3) * NE * VBLK + t;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) cp_async8(s + (cc * 6 + i) * VBLK, rhs + cc * P6 + ((size_t)i * L + l) * nt + c);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cp_async8(s + (6 * NC + i) * VBLK, a.wt + ((size_t)i * L + l) * nt + c);
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  stage(1);
+  Col C;
+  load_col(m, c, C);
+  double eta[3], e0[3], e1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    eta[k] = a.eta_u[k * nt + c];
+    e0[k] = a.eta0[k * nt + c];
+    e1[k] = a.eta1[k * nt + c];
+  }
+  const double j2d = C.j2d;
+  VG Vp, V, Vn;
+  vgeo(C, eta, fr[0], fr[1], V);
+  Vp = V;
+  Vn = V;
+  double gp[6][NC];
+  for (int l = 0; l < L; ++l) {
+    stage(l + 2);
+    cp_async_wait1();  // layers l and l+1 have landed
+    const double* cur = ring + (l % 3) * NE * VBLK + t;
+    const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
+    const double ft = fr[l], fb = fr[l + 1];
+    if (l < L - 1) vgeo(C, eta, fb, fr[l + 2], Vn);
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) wt[i] = cur[(6 * NC + i) * VBLK];
+    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if (l < L - 1) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wtn[k] = nxt[(6 * NC + k) * VBLK];
+    }
+    VPieces P;
+    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
+    double d[6][6], u[3][6], w[3][6];
+    vop_blocks(l, L, Vp, V, Vn, P, P, d, u, w);
+    double jz1[3], M1h[3][3];
+    layer_jz(C.b, e1, ft, fb, jz1);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p; q < 3; ++q) {
+        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+        M1h[p][q] = s;
+        M1h[q][p] = s;
+      }
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) d[i][j] = KM[i / 3][j / 3] * M1h[i % 3][j % 3] - dt * d[i][j];
+    double g[6][NC];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) g[i][cc] = cur[(cc * 6 + i) * VBLK];
+    if (l > 0) {
+      // Dt = D - U G_{l-1} = D - (U E_{l-1}) W_{l-1},  U = -dt u
+      double Pm[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * tl[(k * 3 + j) * VBLK + t];
+          Pm[i][j] = acc;
+        }
+      double S0[3][3], S1h[3][3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double s0 = tl[(18 + sym6(p, q)) * VBLK + t], s1 = tl[(24 + sym6(p, q)) * VBLK + t];
+          S1h[p][q] = DV[1] * s1;                 // W_bot = -DV1 S1  (sign folded below)
+          S0[p][q] = s0 - DV[0] * s1;             // W_top = S0 - DV0 S1
+        }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          double at = 0.0, ab = 0.0;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            at = at + Pm[i][k] * S0[k][j];
+            ab = ab - Pm[i][k] * S1h[k][j];
+          }
+          d[i][j] = d[i][j] - at;
+          d[i][3 + j] = d[i][3 + j] - ab;
+        }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * gp[k][cc];
+          g[i][cc] = g[i][cc] - acc;
+        }
+    }
+    double rp[6];
+    const int bad = lu6r(d, rp);
+    if (bad >= 0) {
+      report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
+      return;
+    }
+    lu6r_solve<NC>(d, rp, g);
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        x[cc * P6 + ((size_t)i * L + l) * nt + c] = g[i][cc];
+        gp[i][cc] = g[i][cc];
+      }
+    if (l < L - 1) {
+      // E = Dt^-1 [0; I3]: forward substitution starts at row 3
+      double* gt = Gs + (size_t)l * VT * nt + c;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double t3 = j == 0 ? 1.0 : 0.0, t4 = j == 1 ? 1.0 : 0.0, t5 = j == 2 ? 1.0 : 0.0;
+        t4 = t4 - d[4][3] * t3;
+        t5 = t5 - d[5][3] * t3 - d[5][4] * t4;
+        double e[6];
+        e[5] = t5 * rp[5];
+        e[4] = (t4 - d[4][5] * e[5]) * rp[4];
+        e[3] = (t3 - d[3][4] * e[4] - d[3][5] * e[5]) * rp[3];
+        e[2] = (0.0 - d[2][3] * e[3] - d[2][4] * e[4] - d[2][5] * e[5]) * rp[2];
+        e[1] = (0.0 - d[1][2] * e[2] - d[1][3] * e[3] - d[1][4] * e[4] - d[1][5] * e[5]) * rp[1];
+        e[0] = (0.0 - d[0][1] * e[1] - d[0][2] * e[2] - d[0][3] * e[3] - d[0][4] * e[4] - d[0][5] * e[5]) * rp[0];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          tl[(i * 3 + j) * VBLK + t] = e[i];
+          gt[(size_t)(i * 3 + j) * nt] = e[i];
+        }
+      }
+      // S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}  (symmetric, packed)
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = p; q < 3; ++q) {
+          const int k = sym6(p, q);
+          const double s0 = -dt * (P.Fo[p][q] + P.pb * MHQ[p][q]);
+          const double s1 = -dt * (P.cn * Vn.R[p][q]);
+          tl[(18 + k) * VBLK + t] = s0;
+          tl[(24 + k) * VBLK + t] = s1;
+          gt[(size_t)(18 + k) * nt] = s0;
+          gt[(size_t)(24 + k) * nt] = s1;
+        }
+    }
+    Vp = V;
+    V = Vn;
+  }
+}
+
+// BACKWARD: x_l = g_l - E_l (W_l x_{l+1}), g_l parked in x by the forward kernel.  Pure
+// streaming (30 + 6 NC words in, 6 NC out per prism), high occupancy.
+template <int NC>
+__global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, const double* __restrict__ Gs,
+                                                  double* x, const pdg_err* err) {
+  const int c = blockIdx.x * VBLK + threadIdx.x;
+  if (c >= nown || err->code == PDG_ERR_ZERO_PIVOT) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  double xn[6][NC];
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = x[cc * P6 + ((size_t)i * L + L - 1) * nt + c];
+  for (int l = L - 2; l >= 0; --l) {
+    const double* gt = Gs + (size_t)l * VT * nt + c;
+    double tv[VT];
+#pragma unroll
+    for (int e = 0; e < VT; ++e) tv[e] = gt[(size_t)e * nt];
+    double gl[6][NC];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      double dz[3], y[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dz[k] = DV[0] * xn[k][cc] + DV[1] * xn[3 + k][cc];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc = acc + tv[18 + sym6(p, q)] * xn[q][cc] - tv[24 + sym6(p, q)] * dz[q];
+        y[p] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double v = gl[i][cc] - (tv[i * 3] * y[0] + tv[i * 3 + 1] * y[1] + tv[i * 3 + 2] * y[2]);
+        x[cc * P6 + ((size_t)i * L + l) * nt + c] = v;
+        xn[i][cc] = v;
+      }
+    }
+  }
+}
+
+inline size_t vimpl_fwd_smem(int nc, int L) { return ((size_t)3 * (6 * nc + 6) * VBLK + VT * VBLK + L + 1) * 8; }
+
 // EXPLICIT: x = M1^-1 (rhs + dt A xin), A applied matrix free; M1^-1 = K^-1 (x) (J2D Mjz)^-1.
 template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, double dt, const double* rhs,
@@ -1159,7 +1416,32 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
-  if (implicit) {
+  if (implicit && tune_get(TUNE_VSPLIT) == 2) {
+    double* Gs = ctx->ws3((size_t)VT * ctx->L * nt);
+    if (!Gs) return PDG_ERR_CUDA;
+    const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
+#define LAUNCH_FWD(NCV, MB)                                                                       \
+  {                                                                                               \
+    static bool attr = false;                                                                     \
+    if (!attr) {                                                                                  \
+      cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                           (int)vimpl_fwd_smem(NCV, 4096));                                       \
+      attr = true;                                                                                \
+    }                                                                                             \
+    k_vimpl_fwd<NCV, MB><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                          \
+  }
+    if (ncomp == 2) {
+      if (tune_get(TUNE_VIMPL) == 2) LAUNCH_FWD(2, 2) else LAUNCH_FWD(2, 1)
+    } else {
+      if (tune_get(TUNE_VIMPL) == 2) LAUNCH_FWD(1, 2) else LAUNCH_FWD(1, 1)
+    }
+#undef LAUNCH_FWD
+    if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+    if (ncomp == 2)
+      k_vimpl_bwd<2><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
+    else
+      k_vimpl_bwd<1><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
+  } else if (implicit) {
     double* Gs = ctx->ws3((size_t)36 * ctx->L * nt);
     if (!Gs) return PDG_ERR_CUDA;
 #define LAUNCH_ARGS m, a, dt, rhs, Gs, x
