@@ -1222,6 +1222,141 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
   }
 }
 
+// EXPLICIT, staged: as k_vexplicit, with the per-layer inputs (rhs, xin, w~) streamed through a
+// 3-deep cp.async ring two layers ahead (each thread stages and reads only its own words).
+template <int NC, int MINB>
+__global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, double dt, const double* rhs,
+                                                     const double* __restrict__ xin, double* x) {
+  constexpr int NE = 12 * NC + 6;  // rhs, xin, w~
+  extern __shared__ double smem[];
+  double* ring = smem;             // [3][NE][VBLK]
+  double* fr = smem + 3 * NE * VBLK;
+  const int t = threadIdx.x;
+  const int c = blockIdx.x * VBLK + t;
+  const int nt = m.nt, L = m.L;
+  for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
+  __syncthreads();
+  if (c >= m.nown) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  auto stage = [&](int l) {
+    if (l < L) {
+      double* s = ring + (l % 3) * NE * VBLK + t;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const size_t o = cc * P6 + ((size_t)i * L + l) * nt + c;
+          cp_async8(s + (cc * 6 + i) * VBLK, rhs + o);
+          cp_async8(s + (6 * NC + cc * 6 + i) * VBLK, xin + o);
+        }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + ((size_t)i * L + l) * nt + c);
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  stage(1);
+  Col C;
+  load_col(m, c, C);
+  double eta[3], e0[3], e1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    eta[k] = a.eta_u[k * nt + c];
+    e0[k] = a.eta0[k * nt + c];
+    e1[k] = a.eta1[k * nt + c];
+  }
+  const double j2d = C.j2d;
+  constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
+  constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
+  VG Vp, V, Vn;
+  vgeo(C, eta, fr[0], fr[1], V);
+  Vp = V;
+  Vn = V;
+  double xa[NC][6], xc[NC][6];
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) xa[cc][k] = 0.0;
+  for (int l = 0; l < L; ++l) {
+    stage(l + 2);
+    cp_async_wait1();
+    const double* cur = ring + (l % 3) * NE * VBLK + t;
+    const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
+    const double ft = fr[l], fb = fr[l + 1];
+    if (l == 0) {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) xc[cc][k] = cur[(6 * NC + cc * 6 + k) * VBLK];
+    }
+    double xb[NC][6];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) xb[cc][k] = l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0;
+    if (l < L - 1) vgeo(C, eta, fb, fr[l + 2], Vn);
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
+    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if (l < L - 1) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wtn[k] = nxt[(12 * NC + k) * VBLK];
+    }
+    VPieces P;
+    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
+    double jz1[3], A1[3][3];
+    layer_jz(C.b, e1, ft, fb, jz1);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p; q < 3; ++q) {
+        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+        A1[p][q] = s;
+        A1[q][p] = s;
+      }
+    const double r0 = 1.0 / A1[0][0];
+    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
+    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
+    const double a22p = A1[2][2] - l20 * A1[0][2];
+    const double r1 = 1.0 / a11;
+    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
+    const double r2 = 1.0 / (a22p - l21 * a12);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      double y[6];
+      vop_apply(l, L, Vp, V, Vn, P, P, xa[cc], xc[cc], xb[cc], y);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) y[k] = cur[(cc * 6 + k) * VBLK] + dt * y[k];
+      double o[6];
+#pragma unroll
+      for (int lev = 0; lev < 2; ++lev) {
+        double z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) z[k] = lev == 0 ? ki00 * y[k] + ki01 * y[3 + k] : ki10 * y[k] + ki11 * y[3 + k];
+        z[1] -= l10 * z[0];
+        z[2] -= l20 * z[0] + l21 * z[1];
+        z[2] *= r2;
+        z[1] = (z[1] - a12 * z[2]) * r1;
+        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
+      }
+      st6(x + cc * P6, l, c, L, nt, o);
+    }
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        xa[cc][k] = xc[cc][k];
+        xc[cc][k] = xb[cc][k];
+      }
+    Vp = V;
+    V = Vn;
+  }
+}
+inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + L + 1) * 8; }
+
 // EXPLICIT stage for momentum (2 comps) AND tracer in one pass: the geometry window, the
 // advective pieces of A and the M1 factorisation are shared; only the diffusion pieces differ.
 template <int MINB>
@@ -1416,7 +1551,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
-  if (implicit && tune_get(TUNE_VSPLIT) == 2) {
+  if (implicit && tune_get(TUNE_VSPLIT) >= 2) {
     double* Gs = ctx->ws3((size_t)VT * ctx->L * nt);
     if (!Gs) return PDG_ERR_CUDA;
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
@@ -1451,6 +1586,22 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
       DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 1)
     }
 #undef LAUNCH_ARGS
+  } else if (!implicit && tune_get(TUNE_VSPLIT) == 3) {
+    const size_t sm = vexpl2_smem(ncomp, ctx->L);
+#define LAUNCH_EX(NCV)                                                                                             \
+  {                                                                                                                \
+    static bool attr = false;                                                                                      \
+    if (!attr) {                                                                                                   \
+      cudaFuncSetAttribute(k_vexpl2<NCV, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
+      attr = true;                                                                                                 \
+    }                                                                                                              \
+    k_vexpl2<NCV, 1><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                              \
+  }
+    if (ncomp == 2)
+      LAUNCH_EX(2)
+    else
+      LAUNCH_EX(1)
+#undef LAUNCH_EX
   } else {
 #define LAUNCH_ARGS m, a, dt, rhs, xin, x
     if (ncomp == 2) {
