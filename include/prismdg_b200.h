@@ -92,7 +92,7 @@ int pdg_last_error(pdg_ctx* ctx, void* stream, int* code, long long* i0, long lo
 const char* pdg_cuda_error_string(void);
 /* occupancy variant of a kernel family (0 F3D->2D, 1 vertical implicit, 2 vertical explicit, 3 r, 4 w~, 5 stage RHS):
  * value = min resident 128-thread blocks per SM (1, 3, 4) or 8/9/10 = shared-memory variant of the
- * F3D->2D / stage-RHS kernels (64-thread blocks); <= 0 queries.  Returns the previous value. */
+ * F3D->2D / stage-RHS kernels (64-thread blocks); < 0 queries.  Returns the previous value. */
 int pdg_tune(int key, int value);
 /* number of kernel launches issued by this context since creation */
 long long pdg_launch_count(pdg_ctx* ctx);

@@ -9,6 +9,16 @@
 
 namespace pdg {
 
+// per-thread asynchronous global -> shared copies (LDGSTS): the staged kernels issue the next
+// layer's words one or two layers ahead and wait for them only when the layer is consumed
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void ld6(const double* __restrict__ f, int l, int c, int L, int nt, double v[6]) {
 #pragma unroll
   for (int k = 0; k < 6; ++k) v[k] = f[((size_t)k * L + l) * nt + c];

@@ -866,12 +866,6 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 constexpr int VT = 30;
 constexpr int VBLK = 128;
 
-__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmetric 3x3
   return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5

@@ -1,12 +1,13 @@
 // Context lifetime, mesh upload (reference (nt,3) host layout -> device SoA), error word.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
 #include "ctx.cuh"
 
 static thread_local char g_errbuf[512] = "";
-static int g_tune[pdg::TUNE_NKEYS] = {1, 1, 1, 3, 4, 8, 2, 3, 0, 0, 0, 0};  // measured: scripts/tune.py
+static int g_tune[pdg::TUNE_NKEYS] = {1, 1, 1, 3, 4, 8, 2, 3, 0, 128, 0, 0};  // measured: scripts/tune.py
 
 namespace pdg {
 int tune_get(int key) { return (key >= 0 && key < TUNE_NKEYS) ? g_tune[key] : 1; }
@@ -72,6 +73,12 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
   rc |= upload_soa3(d->eny, nt, &c->eny);
   rc |= upload_soa3(d->b, nt, &c->b);
   rc |= upload_int3(d->nbr, nt, &c->nbr);
+  c->nbr_host.resize((size_t)3 * nt);
+  c->btag_host.resize((size_t)3 * nt);
+  for (size_t i = 0; i < (size_t)3 * nt; ++i) {
+    c->nbr_host[i] = (int)d->nbr[i];
+    c->btag_host[i] = (int)d->btag[i];
+  }
   rc |= upload_int3(d->nbrk, nt, &c->nbrk);
   rc |= upload_int3(d->btag, nt, &c->btag);
   {
@@ -99,8 +106,8 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
 
 int pdg_ctx_destroy(pdg_ctx* c) {
   if (!c) return PDG_OK;
-  void* ptrs[] = {c->j2d, c->dphx, c->dphy, c->elen, c->enx, c->eny, c->b, c->fracs,
-                  c->nbr, c->nbrk, c->btag, c->ninfo, c->err, c->red, c->ws2d, c->ws3d};
+  void* ptrs[] = {c->j2d, c->dphx, c->dphy, c->elen, c->enx, c->eny, c->b, c->fracs, c->nbr, c->nbrk, c->btag,
+                  c->ninfo, c->err, c->red, c->ws2d, c->ws3d, c->tslot, c->halo, c->hoff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -118,6 +125,65 @@ int pdg_ctx_set_layers(pdg_ctx* c, int L, const double* fracs) {
   c->L = L;
   return PDG_OK;
 }
+
+}  // extern "C"
+
+namespace pdg {
+// Tiles of tw consecutive owned columns.  tslot[k][c] = e2 - c0 when the neighbour across edge k
+// lies in c's own tile, tw + h when it is the tile's h-th halo column (first-seen order), -1 on
+// boundary edges.  A face kernel stages the tile's and the halo's planes of a layer in shared
+// memory and gathers every neighbour trace from there (no atomics, no scattered HBM reads).
+int ensure_tiles(pdg_ctx* c, int tw) {
+  if (c->tile_w == tw && c->tile_nown == c->nown && c->tslot) return PDG_OK;
+  const int nt = c->nt, nown = c->nown, ntile = (nown + tw - 1) / tw;
+  std::vector<int> slot((size_t)3 * nt, -1), halo, hoff(ntile + 1, 0);
+  int nh_max = 0;
+  std::vector<int> seen;
+  for (int b = 0; b < ntile; ++b) {
+    const int c0 = b * tw, c1 = std::min(nown, c0 + tw);
+    seen.clear();
+    for (int e = c0; e < c1; ++e)
+      for (int k = 0; k < 3; ++k) {
+        if (c->btag_host[(size_t)e * 3 + k] != 0) continue;
+        const int e2 = c->nbr_host[(size_t)e * 3 + k];
+        if (e2 >= c0 && e2 < c1) {
+          slot[(size_t)k * nt + e] = e2 - c0;
+          continue;
+        }
+        int h = -1;
+        for (size_t j = 0; j < seen.size(); ++j)
+          if (seen[j] == e2) h = (int)j;
+        if (h < 0) {
+          h = (int)seen.size();
+          seen.push_back(e2);
+        }
+        slot[(size_t)k * nt + e] = tw + h;
+      }
+    halo.insert(halo.end(), seen.begin(), seen.end());
+    hoff[b + 1] = (int)halo.size();
+    nh_max = std::max(nh_max, (int)seen.size());
+  }
+  if (halo.empty()) halo.push_back(0);
+  for (int* p : {c->tslot, c->halo, c->hoff})
+    if (p) cudaFree(p);
+  c->tslot = c->halo = c->hoff = nullptr;
+  int rc = 0;
+  rc |= cudaMalloc(&c->tslot, slot.size() * sizeof(int)) != cudaSuccess;
+  rc |= cudaMalloc(&c->halo, halo.size() * sizeof(int)) != cudaSuccess;
+  rc |= cudaMalloc(&c->hoff, hoff.size() * sizeof(int)) != cudaSuccess;
+  if (rc) return PDG_ERR_CUDA;
+  rc |= cudaMemcpy(c->tslot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  rc |= cudaMemcpy(c->halo, halo.data(), halo.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  rc |= cudaMemcpy(c->hoff, hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  if (rc) return PDG_ERR_CUDA;
+  c->tile_w = tw;
+  c->tile_nown = nown;
+  c->nh_max = nh_max;
+  return PDG_OK;
+}
+}  // namespace pdg
+
+extern "C" {
 
 int pdg_ctx_set_owned(pdg_ctx* c, int nown) {
   if (nown < 0 || nown > c->nt) return PDG_ERR_SHAPE;
@@ -146,7 +212,7 @@ const char* pdg_cuda_error_string(void) { return g_errbuf; }
 int pdg_tune(int key, int value) {
   if (key < 0 || key >= pdg::TUNE_NKEYS) return PDG_ERR_SHAPE;
   int old = g_tune[key];
-  if (value > 0) g_tune[key] = value;
+  if (value >= 0) g_tune[key] = value;
   return old;
 }
 

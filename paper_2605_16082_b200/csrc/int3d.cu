@@ -1265,6 +1265,285 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #undef SD
 }
 
+// ---------------------------------------------------------------------------------------------
+// Tile-staged variant of the stepper flavours (MODE 1 PRED, MODE 2 STAGE).  A block owns TW
+// consecutive (Hilbert-ordered) columns.  Per layer it stages, with per-thread cp.async copies
+// issued one layer ahead into a 2-slot ring, the u (NC x 6) and q (2 x 6) words of its TW columns
+// and of its halo (the out-of-tile neighbours, ctx tile maps); every lateral trace -- own or
+// neighbour -- is then read from shared memory through the precomputed slot map, so the layer
+// loop never waits on a scattered HBM/L2 gather.  Arithmetic is identical to k_hrhs (bitwise).
+// staged planes: word w of a column at layer l is p[w][l * nt + col] (p[w] = plane base + node offset)
+struct StagePlanes {
+  const double* p[30];
+};
+
+template <int NC, int MODE, int TW>
+__global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const __grid_constant__ StagePlanes sp,
+                                                       const int* __restrict__ tslot, const int* __restrict__ halo,
+                                                       const int* __restrict__ hoff, int tj, double* __restrict__ out) {
+  constexpr int NW = 6 * NC + 12;  // staged words per column: u comps, q comps
+  extern __shared__ double sbuf[];  // [2][NW][tj]
+  const int t = threadIdx.x, b = blockIdx.x;
+  const int c = b * TW + t, nt = m.nt, L = m.L;
+  const bool act = c < m.nown;
+  const size_t P6 = (size_t)6 * L * nt;
+  const int h0 = hoff[b], nh = hoff[b + 1] - h0;
+  // halo work split: thread t copies words [w0, w1) of halo column hj (nparts threads per column)
+  const int nparts = nh > 0 ? max(1, TW / nh) : 1;
+  const int wpp = (NW + nparts - 1) / nparts;
+  const int part = nh > 0 ? t / nh : nparts;
+  const int hj = nh > 0 ? t - part * nh : 0;
+  const int hw0 = part < nparts ? part * wpp : NW, hw1 = min(NW, hw0 + wpp);
+  const int hcol = part < nparts ? halo[h0 + hj] : 0;
+  // halo columns beyond TW threads (nh > TW) are covered by a strided fallback
+  auto stage = [&](int l) {
+    double* s = sbuf + (size_t)(l & 1) * NW * tj;
+    const size_t lo = (size_t)l * nt;
+    if (act) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + t, sp.p[w] + lo + c);
+    }
+    for (int w = hw0; w < hw1; ++w) cp_async8(s + w * tj + TW + hj, sp.p[w] + lo + hcol);
+    for (int j = TW + t; j < nh; j += TW) {
+      const int col = halo[h0 + j];
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + TW + j, sp.p[w] + lo + col);
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  Col C;
+  double eta[3];
+  EdgeNb E[3];
+  int sl[3];
+  double mo[2][3], mn[3][2][2];
+  double eta0[3], eta1[3], F1[2][3];
+  if (act) {
+    load_col(m, c, C);
+    load_eta(a.eta_u, c, nt, eta);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      edge_setup(m, C, eta, a.eta_u, k, a.g, E[k]);
+      sl[k] = tslot[k * nt + c];
+      if (MODE == 2) {
+        const double H = eta[k] - C.b[k];
+        mo[0][k] = a.mis[k * nt + c] * H;
+        mo[1][k] = a.mis[(3 + k) * nt + c] * H;
+        if (C.tag[k] == 0) {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            mn[k][cc][0] = a.mis[(cc * 3 + EV0(E[k].k2)) * nt + E[k].e2] * E[k].hn[0];
+            mn[k][cc][1] = a.mis[(cc * 3 + EV1(E[k].k2)) * nt + E[k].e2] * E[k].hn[1];
+          }
+        }
+      }
+    }
+    if (MODE == 2) {
+      load_eta(a.eta0, c, nt, eta0);
+      load_eta(a.eta1, c, nt, eta1);
+      if constexpr (NC >= 2) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double H1 = eta1[k] - C.b[k];
+          F1[0][k] = a.f2d[k * nt + c] / H1;
+          F1[1][k] = a.f2d[(3 + k) * nt + c] / H1;
+        }
+      }
+    }
+  }
+  const double j2d = act ? C.j2d : 0.0;
+  double csum[NC][3];
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
+  cp_async_wait0();
+  __syncthreads();
+  for (int l = 0; l < L; ++l) {
+    if (l + 1 < L) stage(l + 1);
+    const double* S = sbuf + (size_t)(l & 1) * NW * tj;
+    if (act) {
+      const double ft = m.fracs[l], fb = m.fracs[l + 1];
+      const double jm = 0.5 * (fb - ft);
+      double u[NC][6], qv[2][6];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int n = 0; n < 6; ++n) u[cc][n] = S[(cc * 6 + n) * tj + t];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int n = 0; n < 6; ++n) qv[cc][n] = S[(6 * NC + cc * 6 + n) * tj + t];
+      if (MODE == 2) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jm * mo[cc][n % 3];
+      }
+      double acc[NC][6];
+      {
+        double z[2][2][3];
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+          for (int lev = 0; lev < 2; ++lev) mhq_vec(qv[d] + 3 * lev, z[d][lev]);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          double Sm[2][2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            double dot[2][2];
+#pragma unroll
+            for (int l1 = 0; l1 < 2; ++l1)
+#pragma unroll
+              for (int l2 = 0; l2 < 2; ++l2)
+                dot[l1][l2] =
+                    u[cc][3 * l1] * z[d][l2][0] + u[cc][3 * l1 + 1] * z[d][l2][1] + u[cc][3 * l1 + 2] * z[d][l2][2];
+#pragma unroll
+            for (int mm = 0; mm < 2; ++mm)
+              Sm[mm][d] = K3[mm][0][0] * dot[0][0] + K3[mm][0][1] * dot[0][1] + K3[mm][1][0] * dot[1][0] +
+                          K3[mm][1][1] * dot[1][1];
+          }
+#pragma unroll
+          for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+            for (int p = 0; p < 3; ++p) acc[cc][3 * lev + p] = j2d * (C.dx[p] * Sm[lev][0] + C.dy[p] * Sm[lev][1]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (C.tag[k] != 0) continue;
+        const int j = sl[k], k2 = E[k].k2;
+        const int na = EV0(k2), nb = EV1(k2);
+        auto nb4 = [&](int w0, double n4[4]) {
+          n4[0] = S[(w0 + na) * tj + j];
+          n4[1] = S[(w0 + nb) * tj + j];
+          n4[2] = S[(w0 + 3 + na) * tj + j];
+          n4[3] = S[(w0 + 3 + nb) * tj + j];
+        };
+        double f[2][2];
+        {
+          double qn[2][4];
+          nb4(6 * NC, qn[0]);
+          nb4(6 * NC + 6, qn[1]);
+          if (MODE == 2) {
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              qn[cc][0] = qn[cc][0] + jm * mn[k][cc][0];
+              qn[cc][1] = qn[cc][1] + jm * mn[k][cc][1];
+              qn[cc][2] = qn[cc][2] + jm * mn[k][cc][0];
+              qn[cc][3] = qn[cc][3] + jm * mn[k][cc][1];
+            }
+          }
+          lat_factor(C, E[k], k, jm, qv, qn, f);
+        }
+        const double je = -(0.5 * C.el[k]);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          double n4[4], ti[2][2], te[2][2], x[2][2];
+          nb4(cc * 6, n4);
+          tr_own(u[cc], k, ti);
+          tr_nb(n4, te);
+#pragma unroll
+          for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) x[vv][h] = (f[vv][h] >= 0.0 ? ti[vv][h] : te[vv][h]) * f[vv][h];
+          lat_add(acc[cc], k, x, je);
+        }
+      }
+      if constexpr (NC >= 2) {
+        double rr[2][6];
+        ld6(a.r, l, c, L, nt, rr[0]);
+        ld6(a.r + P6, l, c, L, nt, rr[1]);
+        double jz[3], Mu[3][3];
+        layer_jz(C.b, eta, ft, fb, jz);
+        mjz(jz, Mu);
+        const double ir = 1.0 / a.rho0;
+        double y0[6], y1[6], m0[6], m1[6];
+#pragma unroll
+        for (int n = 0; n < 6; ++n) {
+          y0[n] = a.f * u[1][n] - rr[0][n] * ir;
+          y1[n] = -a.f * u[0][n] - rr[1][n] * ir;
+        }
+        kron_apply(Mu, j2d, y0, m0);
+        kron_apply(Mu, j2d, y1, m1);
+#pragma unroll
+        for (int n = 0; n < 6; ++n) {
+          acc[0][n] += m0[n];
+          acc[1][n] += m1[n];
+        }
+        if (l == 0) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            acc[0][k] += j2d / 6.0 * a.tsx;
+            acc[1][k] += j2d / 6.0 * a.tsy;
+          }
+        }
+        if (l == L - 1 && a.cd != 0.0) {
+          double dx3[3], dy3[3], mx[3], my[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double ubx = u[0][3 + k], uby = u[1][3 + k];
+            const double sp = sqrt(ubx * ubx + uby * uby);
+            dx3[k] = -a.cd * sp * ubx;
+            dy3[k] = -a.cd * sp * uby;
+          }
+          mh_apply3(dx3, j2d, mx);
+          mh_apply3(dy3, j2d, my);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            acc[0][3 + k] += mx[k];
+            acc[1][3 + k] += my[k];
+          }
+        }
+      }
+      if (MODE == 1) {
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
+      } else {
+        double j0[3], M0[3][3];
+        layer_jz(C.b, eta0, ft, fb, j0);
+        mjz(j0, M0);
+        double mf[2][3] = {{0, 0, 0}, {0, 0, 0}};
+        if constexpr (NC >= 2) {
+          double j1[3], M1[3][3];
+          layer_jz(C.b, eta1, ft, fb, j1);
+          mjz(j1, M1);
+          const double kk = (KM[0][0] + KM[0][1]) * j2d;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+              mf[cc][p] = kk * (M1[p][0] * F1[cc][0] + M1[p][1] * F1[cc][1] + M1[p][2] * F1[cc][2]);
+        }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          double x0[6], m0x[6], o[6];
+          ld6(a.u0c[cc], l, c, L, nt, x0);
+          kron_apply(M0, j2d, x0, m0x);
+#pragma unroll
+          for (int n = 0; n < 6; ++n) {
+            if (NC >= 2 && cc < 2)
+              o[n] = m0x[n] + a.dt * (acc[cc][n] + mf[cc][n % 3]);
+            else
+              o[n] = m0x[n] + a.dt * acc[cc][n];
+          }
+          st6(a.outc[cc], l, c, L, nt, o);
+        }
+      }
+    }
+    cp_async_wait0();
+    __syncthreads();
+  }
+  if (MODE == 1 && act) {
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) out[(cc * 3 + k) * nt + c] = csum[cc][k];
+  }
+}
+
 // Coriolis and -M r / rho0 over all prisms (the reference applies them to every row even
 // when `els` restricts the advective part, internal3d.py:745-750)
 __global__ void k_mass_terms(int L, int nt, const double* __restrict__ mass, const double* __restrict__ u,
@@ -1349,6 +1628,23 @@ using namespace pdg;
 
 #define COLS(els, n) Cols{els, (els) ? (n) : ctx->nown}
 #define GRID1(nn) nblocks((nn), 128), 128, 0, (cudaStream_t)stream
+
+template <int NC, int MODE, int TW>
+static void launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t s) {
+  const int tj = TW + ctx->nh_max;
+  const size_t sm = (size_t)2 * (6 * NC + 12) * tj * sizeof(double);
+  static size_t attr = 0;
+  if (sm > attr) {
+    cudaFuncSetAttribute(k_hrhs_t<NC, MODE, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+  StagePlanes sp{};
+  const size_t P6 = (size_t)6 * ctx->L * ctx->nt, LN = (size_t)ctx->L * ctx->nt;
+  for (int w = 0; w < 6 * NC + 12; ++w)
+    sp.p[w] = (w < 6 * NC ? a.uc[w / 6] : a.qa + (size_t)((w - 6 * NC) / 6) * P6) + (size_t)(w % 6) * LN;
+  k_hrhs_t<NC, MODE, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), a, sp, ctx->tslot, ctx->halo, ctx->hoff,
+                                                              tj, out);
+}
 
 extern "C" {
 
@@ -1512,7 +1808,13 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, f3d2d
-  if (tune_get(TUNE_HRHS) >= 8) {
+  if (const int tw = tune_get(TUNE_TILE_PRED); tw == 64 || tw == 128) {
+    if (ensure_tiles(ctx, tw)) return PDG_ERR_CUDA;
+    if (tw == 64)
+      launch_tile<2, 1, 64>(ctx, a, f3d2d, strm);
+    else
+      launch_tile<2, 1, 128>(ctx, a, f3d2d, strm);
+  } else if (tune_get(TUNE_HRHS) >= 8) {
     const int t = tune_get(TUNE_HRHS);
     if (t == 9)
       k_hrhs_s<2, 1, 6><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
@@ -1606,7 +1908,13 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out_u
-  if (tune_get(TUNE_HRHS2) >= 8) {
+  if (const int tw = tune_get(TUNE_TILE_STAGE); tw == 64 || tw == 128) {
+    if (ensure_tiles(ctx, tw)) return PDG_ERR_CUDA;
+    if (tw == 64)
+      launch_tile<3, 2, 64>(ctx, a, out_u, strm);
+    else
+      launch_tile<3, 2, 128>(ctx, a, out_u, strm);
+  } else if (tune_get(TUNE_HRHS2) >= 8) {
     const int t = tune_get(TUNE_HRHS2);
     if (t == 9)
       k_hrhs_s<3, 2, 6><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
