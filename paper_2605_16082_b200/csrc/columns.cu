@@ -317,12 +317,28 @@ struct VG {
   double m2a, m2b; // |m_h/m_z|^2 at the two vertical points (kappa_i = kv + kh m2, internal3d.py:838)
   double tt, bb;   // |grad z_top|^2, |grad z_bot|^2                               (:875-876)
   double hgt;      // 2 mean(Jz)                                                   (:888)
+  double rhgt;     // 1 / hgt (the penalty's 1/min(L_a, L_b) = max(1/L_a, 1/L_b))
   double nz;       // 1/sqrt(1 + |grad z_top|^2)                                   (:891)
 };
 
+// KH0: kh == 0 (the stepper: explicit horizontal diffusion is out of scope), so the slope terms
+// m2a, m2b, bb only ever multiply zero and are not formed
+template <bool KH0 = false>
 __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double ft, double fb, VG& V) {
   LGeo G;
-  layer_geo(C, eta, ft, fb, G);
+  if constexpr (KH0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double H = __dsub_rn(eta[i], C.b[i]);
+      G.zt[i] = __dsub_rn(eta[i], __dmul_rn(ft, H));
+      G.zb[i] = __dsub_rn(eta[i], __dmul_rn(fb, H));
+      G.jz[i] = __dmul_rn(0.5, __dsub_rn(G.zt[i], G.zb[i]));
+    }
+    G.dztop[0] = dot3_rn(G.zt, C.dx);
+    G.dztop[1] = dot3_rn(G.zt, C.dy);
+  } else {
+    layer_geo(C, eta, ft, fb, G);
+  }
   double jzq[6], ij[6];
   hq(G.jz, jzq);
 #pragma unroll
@@ -337,23 +353,27 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
       V.R[a][b] = s;
       V.R[b][a] = s;
     }
-  {
+  if constexpr (KH0) {
+    V.m2a = V.m2b = V.bb = 0.0;
+  } else {
     const double mx = G.dzmid[0] + ZQP[0] * G.djz[0], my = G.dzmid[1] + ZQP[0] * G.djz[1];
     V.m2a = mx * mx + my * my;
     const double nx = G.dzmid[0] + ZQP[1] * G.djz[0], ny = G.dzmid[1] + ZQP[1] * G.djz[1];
     V.m2b = nx * nx + ny * ny;
+    V.bb = G.dzbot[0] * G.dzbot[0] + G.dzbot[1] * G.dzbot[1];
   }
   const double tt = G.dztop[0] * G.dztop[0] + G.dztop[1] * G.dztop[1];
   V.tt = tt;
-  V.bb = G.dzbot[0] * G.dzbot[0] + G.dzbot[1] * G.dzbot[1];
-  V.hgt = 2.0 * (((G.jz[0] + G.jz[1]) + G.jz[2]) / 3.0);
-  V.nz = 1.0 / sqrt(1.0 + tt);
+  V.hgt = ((G.jz[0] + G.jz[1]) + G.jz[2]) * (2.0 / 3.0);
+  V.rhgt = 1.0 / V.hgt;
+  V.nz = rsqrt(1.0 + tt);
 }
 
-__device__ __forceinline__ double pen_sigma(double la, double lb, double n0, int order, pdg_err* err) {
-  const double lmin = fmin(la, lb);
+// interior penalty sigma (dg.py:161-173) with L = min(L_a, L_b): n0 (p+1)(p+3) / (2 3 L)
+__device__ __forceinline__ double pen_sigma(const VG& A, const VG& B, double n0, int order, pdg_err* err) {
+  const double lmin = fmin(A.hgt, B.hgt);
   if (lmin <= 0.0) report(err, PDG_ERR_NONPOS_LENGTH, 0, 0, lmin);
-  return n0 * (order + 1.0) * (order + 3.0) / (2.0 * 3.0 * lmin);
+  return n0 * ((order + 1.0) * (order + 3.0) / 6.0) * fmax(A.rhgt, B.rhgt);
 }
 
 // F(x) for x at the 6 points, symmetric
@@ -455,8 +475,8 @@ __device__ __forceinline__ void vop_dif(double j2d, int l, int L, const VG& Vp, 
   P.ca = 0.5 * j2d * kbp;
   P.cb = 0.5 * j2d * kb;
   P.cn = 0.5 * j2d * ktn;
-  P.pt = l > 0 ? 0.5 * (pen_sigma(V.hgt, Vp.hgt, n0, order, err) * fmax(kt, kbp) * V.nz * j2d) : 0.0;
-  P.pb = l < L - 1 ? 0.5 * (pen_sigma(Vn.hgt, V.hgt, n0, order, err) * fmax(ktn, kb) * Vn.nz * j2d) : 0.0;
+  P.pt = l > 0 ? 0.5 * (pen_sigma(V, Vp, n0, order, err) * fmax(kt, kbp) * V.nz * j2d) : 0.0;
+  P.pb = l < L - 1 ? 0.5 * (pen_sigma(Vn, V, n0, order, err) * fmax(ktn, kb) * Vn.nz * j2d) : 0.0;
 }
 
 __device__ __forceinline__ void vop_pieces(double j2d, int l, int L, const VG& Vp, const VG& V, const VG& Vn,
@@ -573,7 +593,7 @@ struct VopArgs {
   const double* wm;     // w_m (P6) when given explicitly (API); else from eta0/eta1
   const double* eta0;   // fused: mesh velocity (z(eta1) - z(eta0)) / dtm
   const double* eta1;   //        and M1 = mass(eta1)
-  double dtm;
+  double dtm, rdtm;     // mesh-velocity step and its reciprocal
   double kh, kv, n0;
   int order;
 };
@@ -590,8 +610,8 @@ __device__ __forceinline__ void wm_layer(const VopArgs& a, const double b[3], co
     const double H0 = __dsub_rn(e0[i], b[i]), H1 = __dsub_rn(e1[i], b[i]);
     const double zt0 = __dsub_rn(e0[i], __dmul_rn(ft, H0)), zt1 = __dsub_rn(e1[i], __dmul_rn(ft, H1));
     const double zb0 = __dsub_rn(e0[i], __dmul_rn(fb, H0)), zb1 = __dsub_rn(e1[i], __dmul_rn(fb, H1));
-    wm[i] = (zt1 - zt0) / a.dtm;
-    wm[3 + i] = (zb1 - zb0) / a.dtm;
+    wm[i] = (zt1 - zt0) * a.rdtm;
+    wm[3 + i] = (zb1 - zb0) * a.rdtm;
   }
 }
 
@@ -875,7 +895,7 @@ __device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmet
 // Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
 // (each thread stages and reads only its own words: no barriers), issued two layers ahead;
 // the previous layer's tile lives in shared memory, not in registers or L2.
-template <int NC, int MINB>
+template <int NC, int MINB, bool KH0>
 __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, double dt, const double* rhs,
                                                         double* __restrict__ Gs, double* x) {
   
@@ -916,7 +936,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   }
   const double j2d = C.j2d;
   VG Vp, V, Vn;
-  vgeo(C, eta, fr[0], fr[1], V);
+  vgeo<KH0>(C, eta, fr[0], fr[1], V);
   Vp = V;
   Vn = V;
   double gp[6][NC];
@@ -926,7 +946,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     const double* cur = ring + (l % 3) * NE * VBLK + t;
     const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
     const double ft = fr[l], fb = fr[l + 1];
-    if (l < L - 1) vgeo(C, eta, fb, fr[l + 2], Vn);
+    if (l < L - 1) vgeo<KH0>(C, eta, fb, fr[l + 2], Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(6 * NC + i) * VBLK];
@@ -1218,7 +1238,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
 
 // EXPLICIT, staged: as k_vexplicit, with the per-layer inputs (rhs, xin, w~) streamed through a
 // 3-deep cp.async ring two layers ahead (each thread stages and reads only its own words).
-template <int NC, int MINB>
+template <int NC, int MINB, bool KH0>
 __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, double dt, const double* rhs,
                                                      const double* __restrict__ xin, double* x) {
   constexpr int NE = 12 * NC + 6;  // rhs, xin, w~
@@ -1263,7 +1283,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
   constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
   VG Vp, V, Vn;
-  vgeo(C, eta, fr[0], fr[1], V);
+  vgeo<KH0>(C, eta, fr[0], fr[1], V);
   Vp = V;
   Vn = V;
   double xa[NC][6], xc[NC][6];
@@ -1288,7 +1308,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
     for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
       for (int k = 0; k < 6; ++k) xb[cc][k] = l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0;
-    if (l < L - 1) vgeo(C, eta, fb, fr[l + 2], Vn);
+    if (l < L - 1) vgeo<KH0>(C, eta, fb, fr[l + 2], Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
@@ -1531,7 +1551,7 @@ int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, c
                           void* stream) {
   const int n = els ? n_els : ctx->nown;
   if (n == 0) return PDG_OK;
-  VopArgs a{eta_g, wt, wm, nullptr, nullptr, 1.0, kh, kv, n0, order};
+  VopArgs a{eta_g, wt, wm, nullptr, nullptr, 1.0, 1.0, kh, kv, n0, order};
   k_vop<<<nblocks(n, 128), 128, 0, (cudaStream_t)stream>>>(ctx->view(), a, els, n, d, u, w);
   return check_launch(ctx);
 }
@@ -1540,7 +1560,7 @@ int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, c
 int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
                       const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
                       double dt, const double* rhs, const double* xin, double* x, void* stream) {
-  VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, kh, kv, n0, order};
+  VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, 1.0 / dt_mesh, kh, kv, n0, order};
   const int nt = ctx->nt;
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
@@ -1553,11 +1573,16 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   {                                                                                               \
     static bool attr = false;                                                                     \
     if (!attr) {                                                                                  \
-      cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+      cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)vimpl_fwd_smem(NCV, 4096));                                       \
+      cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)vimpl_fwd_smem(NCV, 4096));                                       \
       attr = true;                                                                                \
     }                                                                                             \
-    k_vimpl_fwd<NCV, MB><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                          \
+    if (a.kh == 0.0)                                                                              \
+      k_vimpl_fwd<NCV, MB, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                  \
+    else                                                                                          \
+      k_vimpl_fwd<NCV, MB, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                 \
   }
     if (ncomp == 2) {
       if (tune_get(TUNE_VIMPL) == 2) LAUNCH_FWD(2, 2) else LAUNCH_FWD(2, 1)
@@ -1586,10 +1611,14 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   {                                                                                                                \
     static bool attr = false;                                                                                      \
     if (!attr) {                                                                                                   \
-      cudaFuncSetAttribute(k_vexpl2<NCV, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
+      cudaFuncSetAttribute(k_vexpl2<NCV, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
+      cudaFuncSetAttribute(k_vexpl2<NCV, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
       attr = true;                                                                                                 \
     }                                                                                                              \
-    k_vexpl2<NCV, 1><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                              \
+    if (a.kh == 0.0)                                                                                               \
+      k_vexpl2<NCV, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                      \
+    else                                                                                                           \
+      k_vexpl2<NCV, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                     \
   }
     if (ncomp == 2)
       LAUNCH_EX(2)
@@ -1613,7 +1642,7 @@ int pdg_step_vertical_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, 
                          const double* wt, double kh_u, double kv_u, double kh_T, double kv_T, double n0, int order,
                          double dt, const double* rhs_u, const double* xin_u, double* x_u, const double* rhs_T,
                          const double* xin_T, double* x_T, void* stream) {
-  VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, kh_u, kv_u, n0, order};
+  VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, 1.0 / dt_mesh, kh_u, kv_u, n0, order};
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, kh_T, kv_T, dt, rhs_u, xin_u, x_u, rhs_T, xin_T, x_T
