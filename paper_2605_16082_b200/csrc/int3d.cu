@@ -672,6 +672,297 @@ __global__ void __launch_bounds__(128, MINB) k_compute_wtilde(DMesh m, const dou
   }
 }
 
+// staged planes: word w of a column at layer l is p[w][l * nt + col] (p[w] = plane base + node offset)
+struct StagePlanes {
+  const double* p[30];
+};
+
+// ---------------------------------------------------------------------------------------------
+// Tile staging shared by the tiled column kernels: NW words per column of layer l (word w at
+// sp.p[w][l nt + col]) for the block's TW columns and its halo, copied with per-thread cp.async
+// into smem laid out [NW][tj] (tj = TW + max halo).  The halo copies are split so that every
+// thread issues about the same number of them.
+template <int NW, int TW>
+struct TileStage {
+  int t, c, nh, h0, hj, hw0, hw1, hcol;
+  bool act;
+  __device__ __forceinline__ void init(const DMesh& m, const int* __restrict__ halo, const int* __restrict__ hoff) {
+    t = threadIdx.x;
+    c = blockIdx.x * TW + t;
+    act = c < m.nown;
+    h0 = hoff[blockIdx.x];
+    nh = hoff[blockIdx.x + 1] - h0;
+    const int nparts = nh > 0 ? max(1, TW / nh) : 1;
+    const int wpp = (NW + nparts - 1) / nparts;
+    const int part = nh > 0 ? t / nh : nparts;
+    hj = nh > 0 ? t - part * nh : 0;
+    hw0 = part < nparts ? part * wpp : NW;
+    hw1 = min(NW, hw0 + wpp);
+    hcol = part < nparts ? halo[h0 + hj] : 0;
+  }
+  __device__ __forceinline__ void issue(double* s, int tj, const StagePlanes& sp, size_t lo,
+                                        const int* __restrict__ halo) const {
+    if (act) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + t, sp.p[w] + lo + c);
+    }
+    for (int w = hw0; w < hw1; ++w) cp_async8(s + w * tj + TW + hj, sp.p[w] + lo + hcol);
+    for (int j = TW + t; j < nh; j += TW) {
+      const int col = halo[h0 + j];
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + TW + j, sp.p[w] + lo + col);
+    }
+    cp_async_commit();
+  }
+};
+
+// the 4 lateral nodes (t0, t1, b0, b1) of the neighbour across local edge k2, staged word base w0
+__device__ __forceinline__ void nb4_s(const double* S, int tj, int w0, int k2, int j, double n4[4]) {
+  const int a = EV0(k2), b = EV1(k2);
+  n4[0] = S[(w0 + a) * tj + j];
+  n4[1] = S[(w0 + b) * tj + j];
+  n4[2] = S[(w0 + 3 + a) * tj + j];
+  n4[3] = S[(w0 + 3 + b) * tj + j];
+}
+
+// tiled baroclinic head (k_compute_r<FROM_T> with T / rho' staged: 6 words per column)
+template <bool FROM_T, int TW>
+__global__ void __launch_bounds__(TW) k_compute_r_t(DMesh m, const double* __restrict__ eta_g, double alpha,
+                                                   double tref, double g, const __grid_constant__ StagePlanes sp,
+                                                   const int* __restrict__ tslot, const int* __restrict__ halo,
+                                                   const int* __restrict__ hoff, int tj, double* __restrict__ r) {
+  extern __shared__ double sbuf[];  // [2][6][tj]
+  TileStage<6, TW> ts;
+  ts.init(m, halo, hoff);
+  const int c = ts.c, nt = m.nt, L = m.L, t = ts.t;
+  const size_t P6 = (size_t)6 * L * nt;
+  ts.issue(sbuf, tj, sp, 0, halo);
+  Col C;
+  double eta[3], ex = 0.0, ey = 0.0;
+  EdgeNb E[3];
+  int sl[3];
+  if (ts.act) {
+    load_col(m, c, C);
+    load_eta(eta_g, c, nt, eta);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      edge_setup(m, C, eta, eta_g, k, g, E[k]);
+      sl[k] = tslot[k * nt + c];
+    }
+    ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
+    ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
+  }
+  const double j2d = ts.act ? C.j2d : 0.0;
+  double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  double prevb[3] = {0, 0, 0};
+  cp_async_wait0();
+  __syncthreads();
+  for (int l = 0; l < L; ++l) {
+    if (l + 1 < L) ts.issue(sbuf + (size_t)((l + 1) & 1) * 6 * tj, tj, sp, (size_t)(l + 1) * nt, halo);
+    const double* S = sbuf + (size_t)(l & 1) * 6 * tj;
+    if (ts.act) {
+      const double ft = m.fracs[l], fb = m.fracs[l + 1];
+      const double jm = 0.5 * (fb - ft);
+      LGeo G;
+      layer_geo(C, eta, ft, fb, G);
+      double rho[6];
+#pragma unroll
+      for (int n = 0; n < 6; ++n) rho[n] = S[n * tj + t];
+      if (FROM_T) {
+#pragma unroll
+        for (int n = 0; n < 6; ++n) rho[n] = -alpha * (rho[n] - tref);
+      }
+      double acc[2][6];
+      {
+        double gi[2][2], A[3], B[3], dzn[3];
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev) {
+          gi[lev][0] = (rho[3 * lev] * C.dx[0] + rho[3 * lev + 1] * C.dx[1]) + rho[3 * lev + 2] * C.dx[2];
+          gi[lev][1] = (rho[3 * lev] * C.dy[0] + rho[3 * lev + 1] * C.dy[1]) + rho[3 * lev + 2] * C.dy[2];
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) dzn[a] = 0.5 * (rho[a] - rho[3 + a]);
+        mhq_vec(G.jz, A);
+        mhq_vec(dzn, B);
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          double tt[2][3];
+#pragma unroll
+          for (int vv = 0; vv < 2; ++vv) {
+            const double gv = VS[vv][0] * gi[0][d] + VS[vv][1] * gi[1][d];
+            const double md = d == 0 ? G.dzmid[0] + ZQP[vv] * G.djz[0] : G.dzmid[1] + ZQP[vv] * G.djz[1];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) tt[vv][a] = gv * A[a] - md * B[a];
+          }
+#pragma unroll
+          for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+              acc[d][3 * lev + a] = -(g * j2d) * (VS[0][lev] * tt[0][a] + VS[1][lev] * tt[1][a]);
+        }
+      }
+      if (l > 0) {
+        double dr[3], fi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) dr[a] = 0.5 * (rho[a] - prevb[a]);
+        const double sdr = (dr[0] + dr[1]) + dr[2];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) fi[a] = (dr[a] + sdr) / 24.0;
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) acc[d][a] += 2.0 * g * j2d * (-G.dztop[d]) * fi[a];
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (C.tag[k] != 0) continue;
+        double n4[4], dj[2][2];
+        nb4_s(S, tj, 0, E[k].k2, sl[k], n4);
+        if (FROM_T) {
+#pragma unroll
+          for (int n = 0; n < 4; ++n) n4[n] = -alpha * (n4[n] - tref);
+        }
+        tr_jump(rho, k, n4, dj);
+        double xx[2][2], xy[2][2];
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double x = dj[vv][h] * (jm * E[k].hm[h]);
+            xx[vv][h] = C.nx[k] * x;
+            xy[vv][h] = C.ny[k] * x;
+          }
+        const double je = 0.5 * C.el[k];
+        lat_add(acc[0], k, xx, g * je);
+        lat_add(acc[1], k, xy, g * je);
+      }
+      if (l == 0) {
+        double mr[3];
+        mh_apply3(rho, j2d, mr);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          acc[0][a] -= g * mr[a] * ex;
+          acc[1][a] -= g * mr[a] * ey;
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        double gt[3], gb[3], out[6];
+        mh_inv3(acc[d], j2d, gt);
+        mh_inv3(acc[d] + 3, j2d, gb);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          s[d][a] = s[d][a] + (gt[a] + gb[a]);
+          out[a] = -s[d][a] + 2.0 * gb[a];
+          out[3 + a] = -s[d][a];
+        }
+        st6(r + d * P6, l, c, L, nt, out);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) prevb[a] = rho[3 + a];
+    }
+    cp_async_wait0();
+    __syncthreads();
+  }
+}
+
+// tiled fused w~ (k_compute_wtilde<true> with q staged: 12 words per column), bottom-up
+template <int TW>
+__global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* __restrict__ eta_g,
+                                                        const double* __restrict__ mis, double g,
+                                                        const __grid_constant__ StagePlanes sp,
+                                                        const int* __restrict__ tslot, const int* __restrict__ halo,
+                                                        const int* __restrict__ hoff, int tj, double* __restrict__ w) {
+  extern __shared__ double sbuf[];  // [2][12][tj]
+  TileStage<12, TW> ts;
+  ts.init(m, halo, hoff);
+  const int c = ts.c, nt = m.nt, L = m.L, t = ts.t;
+  ts.issue(sbuf + (size_t)((L - 1) & 1) * 12 * tj, tj, sp, (size_t)(L - 1) * nt, halo);
+  Col C;
+  double eta[3];
+  EdgeNb E[3];
+  int sl[3];
+  double mo[2][3], mn[3][2][2];
+  if (ts.act) {
+    load_col(m, c, C);
+    load_eta(eta_g, c, nt, eta);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      edge_setup(m, C, eta, eta_g, k, g, E[k]);
+      sl[k] = tslot[k * nt + c];
+      mo[0][k] = mis[k * nt + c] * (eta[k] - C.b[k]);
+      mo[1][k] = mis[(3 + k) * nt + c] * (eta[k] - C.b[k]);
+      if (C.tag[k] == 0) {
+        const int e2 = E[k].e2, k2 = E[k].k2;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          mn[k][cc][0] = mis[(cc * 3 + EV0(k2)) * nt + e2] * E[k].hn[0];
+          mn[k][cc][1] = mis[(cc * 3 + EV1(k2)) * nt + e2] * E[k].hn[1];
+        }
+      }
+    }
+  }
+  const double j2d = ts.act ? C.j2d : 0.0;
+  double s[3] = {0, 0, 0};
+  cp_async_wait0();
+  __syncthreads();
+  for (int l = L - 1; l >= 0; --l) {
+    if (l > 0) ts.issue(sbuf + (size_t)((l - 1) & 1) * 12 * tj, tj, sp, (size_t)(l - 1) * nt, halo);
+    const double* S = sbuf + (size_t)(l & 1) * 12 * tj;
+    if (ts.act) {
+      const double jm = 0.5 * (m.fracs[l + 1] - m.fracs[l]);
+      double qv[2][6];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int n = 0; n < 6; ++n) qv[cc][n] = S[(cc * 6 + n) * tj + t] + jm * mo[cc][n % 3];
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      {
+        double wq[2][2];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int lev = 0; lev < 2; ++lev)
+            wq[cc][lev] = W1[0] * qv[cc][3 * lev] + W1[1] * qv[cc][3 * lev + 1] + W1[2] * qv[cc][3 * lev + 2];
+        double Sm[2][2];
+#pragma unroll
+        for (int mm = 0; mm < 2; ++mm) {
+          Sm[mm][0] = KM[mm][0] * wq[0][0] + KM[mm][1] * wq[0][1];
+          Sm[mm][1] = KM[mm][0] * wq[1][0] + KM[mm][1] * wq[1][1];
+        }
+        iso_add(C, Sm, acc);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (C.tag[k] != 0) continue;
+        double f[2][2], qn[2][4];
+        nb4_s(S, tj, 0, E[k].k2, sl[k], qn[0]);
+        nb4_s(S, tj, 6, E[k].k2, sl[k], qn[1]);
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          qn[cc][0] = qn[cc][0] + jm * mn[k][cc][0];
+          qn[cc][1] = qn[cc][1] + jm * mn[k][cc][1];
+          qn[cc][2] = qn[cc][2] + jm * mn[k][cc][0];
+          qn[cc][3] = qn[cc][3] + jm * mn[k][cc][1];
+        }
+        lat_factor(C, E[k], k, jm, qv, qn, f);
+        lat_add(acc, k, f, -(0.5 * C.el[k]));
+      }
+      double gt[3], gb[3], out[6];
+      mh_inv3(acc, j2d, gt);
+      mh_inv3(acc + 3, j2d, gb);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        out[3 + a] = s[a] + gb[a] - gt[a];
+        out[a] = s[a] + gb[a] + gt[a];
+        s[a] = out[a];
+      }
+      st6(w, l, c, L, nt, out);
+    }
+    cp_async_wait0();
+    __syncthreads();
+  }
+}
+
 // ============================================================================ horizontal RHS
 // internal3d.py:695-751 (momentum, NC=2) and :754-792 (tracer, NC=1), kappa = nu = 0.
 // MODE 0 (API):   explicit q_adv / factor / mass arrays; out = F (P6N); Coriolis and -M r/rho0
@@ -1272,10 +1563,6 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 // and of its halo (the out-of-tile neighbours, ctx tile maps); every lateral trace -- own or
 // neighbour -- is then read from shared memory through the precomputed slot map, so the layer
 // loop never waits on a scattered HBM/L2 gather.  Arithmetic is identical to k_hrhs (bitwise).
-// staged planes: word w of a column at layer l is p[w][l * nt + col] (p[w] = plane base + node offset)
-struct StagePlanes {
-  const double* p[30];
-};
 
 template <int NC, int MODE, int TW>
 __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const __grid_constant__ StagePlanes sp,
@@ -1646,7 +1933,48 @@ static void launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t 
                                                               tj, out);
 }
 
+// planes of an NC-component prism field: word cc*6+node -> base + cc P6 + node L nt
+static StagePlanes planes_of(const double* base, int nc, const pdg_ctx* ctx) {
+  StagePlanes sp{};
+  const size_t P6 = (size_t)6 * ctx->L * ctx->nt, LN = (size_t)ctx->L * ctx->nt;
+  for (int w = 0; w < 6 * nc; ++w) sp.p[w] = base + (size_t)(w / 6) * P6 + (size_t)(w % 6) * LN;
+  return sp;
+}
+template <typename K>
+static void set_smem(K kernel, size_t sm, size_t& attr) {
+  if (sm > attr) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+}
+template <bool FROM_T, int TW>
+static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, double alpha, double tref, double g,
+                         double* r, cudaStream_t s) {
+  if (ensure_tiles(ctx, TW)) return PDG_ERR_CUDA;
+  const int tj = TW + ctx->nh_max;
+  const size_t sm = (size_t)2 * 6 * tj * sizeof(double);
+  static size_t attr = 0;
+  set_smem(k_compute_r_t<FROM_T, TW>, sm, attr);
+  k_compute_r_t<FROM_T, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, alpha, tref, g,
+                                                                 planes_of(rho, 1, ctx), ctx->tslot, ctx->halo,
+                                                                 ctx->hoff, tj, r);
+  return PDG_OK;
+}
+template <int TW>
+static int launch_wt_tile(pdg_ctx* ctx, const double* eta_g, const double* qb, const double* mis, double g, double* w,
+                          cudaStream_t s) {
+  if (ensure_tiles(ctx, TW)) return PDG_ERR_CUDA;
+  const int tj = TW + ctx->nh_max;
+  const size_t sm = (size_t)2 * 12 * tj * sizeof(double);
+  static size_t attr = 0;
+  set_smem(k_compute_wtilde_t<TW>, sm, attr);
+  k_compute_wtilde_t<TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, mis, g, planes_of(qb, 2, ctx),
+                                                              ctx->tslot, ctx->halo, ctx->hoff, tj, w);
+  return PDG_OK;
+}
+
 extern "C" {
+
 
 int pdg_prism_mass(pdg_ctx* ctx, const double* eta_g, const int* els, int n_els, double* out, void* stream) {
   Cols cs = COLS(els, n_els);
@@ -1705,6 +2033,17 @@ int pdg_compute_r(pdg_ctx* ctx, const double* eta_g, const double* rho_or_T, int
   if (cs.n == 0) return PDG_OK;
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
+  if (const int tw = tune_get(TUNE_TILE_COL); !els && (tw == 64 || tw == 128)) {
+    int rc;
+    if (tw == 64)
+      rc = from_T ? launch_r_tile<true, 64>(ctx, eta_g, rho_or_T, alpha, tref, g, r, strm)
+                  : launch_r_tile<false, 64>(ctx, eta_g, rho_or_T, alpha, tref, g, r, strm);
+    else
+      rc = from_T ? launch_r_tile<true, 128>(ctx, eta_g, rho_or_T, alpha, tref, g, r, strm)
+                  : launch_r_tile<false, 128>(ctx, eta_g, rho_or_T, alpha, tref, g, r, strm);
+    if (rc) return rc;
+    return check_launch(ctx);
+  }
 #define LAUNCH_ARGS ctx->view(), eta_g, rho_or_T, alpha, tref, g, cs, r
   if (from_T) {
     DISPATCH_MINB(TUNE_R, k_compute_r, true)
@@ -1729,6 +2068,12 @@ int pdg_compute_wtilde(pdg_ctx* ctx, const double* eta_g, const double* qb, cons
   if (cs.n == 0) return PDG_OK;
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
+  if (const int tw = tune_get(TUNE_TILE_COL); !els && mis && (tw == 64 || tw == 128)) {
+    const int rc = tw == 64 ? launch_wt_tile<64>(ctx, eta_g, qb, mis, g, w, strm)
+                            : launch_wt_tile<128>(ctx, eta_g, qb, mis, g, w, strm);
+    if (rc) return rc;
+    return check_launch(ctx);
+  }
 #define LAUNCH_ARGS ctx->view(), eta_g, qb, fac, mis, g, cs, w
   if (mis) {
     DISPATCH_MINB(TUNE_WT, k_compute_wtilde, true)
