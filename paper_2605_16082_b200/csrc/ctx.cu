@@ -107,7 +107,8 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
 int pdg_ctx_destroy(pdg_ctx* c) {
   if (!c) return PDG_OK;
   void* ptrs[] = {c->j2d, c->dphx, c->dphy, c->elen, c->enx, c->eny, c->b, c->fracs, c->nbr, c->nbrk, c->btag,
-                  c->ninfo, c->err, c->red, c->ws2d, c->ws3d, c->tslot, c->halo, c->hoff};
+                  c->ninfo, c->err, c->red, c->ws2d, c->ws3d, c->tiles[0].tslot, c->tiles[0].halo,
+                  c->tiles[0].hoff, c->tiles[1].tslot, c->tiles[1].halo, c->tiles[1].hoff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -133,8 +134,10 @@ namespace pdg {
 // lies in c's own tile, tw + h when it is the tile's h-th halo column (first-seen order), -1 on
 // boundary edges.  A face kernel stages the tile's and the halo's planes of a layer in shared
 // memory and gathers every neighbour trace from there (no atomics, no scattered HBM reads).
-int ensure_tiles(pdg_ctx* c, int tw) {
-  if (c->tile_w == tw && c->tile_nown == c->nown && c->tslot) return PDG_OK;
+const pdg_ctx::TileMap* ensure_tiles(pdg_ctx* c, int tw) {
+  if (tw != 64 && tw != 128) return nullptr;
+  pdg_ctx::TileMap& T = c->tiles[tw == 64 ? 0 : 1];
+  if (T.tw == tw && T.nown == c->nown && T.tslot) return &T;
   const int nt = c->nt, nown = c->nown, ntile = (nown + tw - 1) / tw;
   std::vector<int> slot((size_t)3 * nt, -1), halo, hoff(ntile + 1, 0);
   int nh_max = 0;
@@ -164,22 +167,23 @@ int ensure_tiles(pdg_ctx* c, int tw) {
     nh_max = std::max(nh_max, (int)seen.size());
   }
   if (halo.empty()) halo.push_back(0);
-  for (int* p : {c->tslot, c->halo, c->hoff})
+  for (int* p : {T.tslot, T.halo, T.hoff})
     if (p) cudaFree(p);
-  c->tslot = c->halo = c->hoff = nullptr;
+  T.tslot = T.halo = T.hoff = nullptr;
+  T.tw = 0;
   int rc = 0;
-  rc |= cudaMalloc(&c->tslot, slot.size() * sizeof(int)) != cudaSuccess;
-  rc |= cudaMalloc(&c->halo, halo.size() * sizeof(int)) != cudaSuccess;
-  rc |= cudaMalloc(&c->hoff, hoff.size() * sizeof(int)) != cudaSuccess;
-  if (rc) return PDG_ERR_CUDA;
-  rc |= cudaMemcpy(c->tslot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
-  rc |= cudaMemcpy(c->halo, halo.data(), halo.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
-  rc |= cudaMemcpy(c->hoff, hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
-  if (rc) return PDG_ERR_CUDA;
-  c->tile_w = tw;
-  c->tile_nown = nown;
-  c->nh_max = nh_max;
-  return PDG_OK;
+  rc |= cudaMalloc(&T.tslot, slot.size() * sizeof(int)) != cudaSuccess;
+  rc |= cudaMalloc(&T.halo, halo.size() * sizeof(int)) != cudaSuccess;
+  rc |= cudaMalloc(&T.hoff, hoff.size() * sizeof(int)) != cudaSuccess;
+  if (rc) return nullptr;
+  rc |= cudaMemcpy(T.tslot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  rc |= cudaMemcpy(T.halo, halo.data(), halo.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  rc |= cudaMemcpy(T.hoff, hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess;
+  if (rc) return nullptr;
+  T.tw = tw;
+  T.nown = nown;
+  T.nh_max = nh_max;
+  return &T;
 }
 }  // namespace pdg
 

@@ -20,11 +20,14 @@ struct pdg_ctx {
   size_t ws3d_doubles = 0;
   long long launches = 0;
   std::vector<double> fracs_host;
-  // tile maps of the shared-memory-staged face kernels (int3d.cu k_hrhs_t): for tiles of `tile_w`
-  // consecutive owned columns, the neighbour slot of every (edge, column) and each tile's halo
+  // tile maps of the shared-memory-staged face kernels (int3d.cu k_*_t): for tiles of tw
+  // consecutive owned columns, the neighbour slot of every (edge, column) and each tile's halo;
+  // one map per tile width (64, 128)
   std::vector<int> nbr_host, btag_host;   // (nt,3) row-major host copies
-  int tile_w = 0, tile_nown = -1, nh_max = 0;
-  int *tslot = nullptr, *halo = nullptr, *hoff = nullptr;
+  struct TileMap {
+    int tw = 0, nown = -1, nh_max = 0;
+    int *tslot = nullptr, *halo = nullptr, *hoff = nullptr;
+  } tiles[2];
 
   pdg::DMesh view() const {
     pdg::DMesh m;
@@ -62,7 +65,8 @@ struct pdg_ctx {
 };
 
 namespace pdg {
-int ensure_tiles(pdg_ctx* ctx, int tw);   // builds / reuses the tile maps (host, never during capture)
+// builds / reuses the tile map of width tw (64 or 128; host work, never during capture); nullptr on failure
+const pdg_ctx::TileMap* ensure_tiles(pdg_ctx* ctx, int tw);
 int check_launch(pdg_ctx* ctx);  // returns PDG_OK or PDG_ERR_CUDA and counts the launch
 int check_launch_noctx();
 }  // namespace pdg

@@ -1556,6 +1556,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #undef SD
 }
 
+
 // ---------------------------------------------------------------------------------------------
 // Tile-staged variant of the stepper flavours (MODE 1 PRED, MODE 2 STAGE).  A block owns TW
 // consecutive (Hilbert-ordered) columns.  Per layer it stages, with per-thread cp.async copies
@@ -1917,8 +1918,10 @@ using namespace pdg;
 #define GRID1(nn) nblocks((nn), 128), 128, 0, (cudaStream_t)stream
 
 template <int NC, int MODE, int TW>
-static void launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t s) {
-  const int tj = TW + ctx->nh_max;
+static int launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t s) {
+  const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
+  if (!tm) return PDG_ERR_CUDA;
+  const int tj = TW + tm->nh_max;
   const size_t sm = (size_t)2 * (6 * NC + 12) * tj * sizeof(double);
   static size_t attr = 0;
   if (sm > attr) {
@@ -1929,8 +1932,9 @@ static void launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t 
   const size_t P6 = (size_t)6 * ctx->L * ctx->nt, LN = (size_t)ctx->L * ctx->nt;
   for (int w = 0; w < 6 * NC + 12; ++w)
     sp.p[w] = (w < 6 * NC ? a.uc[w / 6] : a.qa + (size_t)((w - 6 * NC) / 6) * P6) + (size_t)(w % 6) * LN;
-  k_hrhs_t<NC, MODE, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), a, sp, ctx->tslot, ctx->halo, ctx->hoff,
+  k_hrhs_t<NC, MODE, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), a, sp, tm->tslot, tm->halo, tm->hoff,
                                                               tj, out);
+  return PDG_OK;
 }
 
 // planes of an NC-component prism field: word cc*6+node -> base + cc P6 + node L nt
@@ -1950,28 +1954,31 @@ static void set_smem(K kernel, size_t sm, size_t& attr) {
 template <bool FROM_T, int TW>
 static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, double alpha, double tref, double g,
                          double* r, cudaStream_t s) {
-  if (ensure_tiles(ctx, TW)) return PDG_ERR_CUDA;
-  const int tj = TW + ctx->nh_max;
+  const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
+  if (!tm) return PDG_ERR_CUDA;
+  const int tj = TW + tm->nh_max;
   const size_t sm = (size_t)2 * 6 * tj * sizeof(double);
   static size_t attr = 0;
   set_smem(k_compute_r_t<FROM_T, TW>, sm, attr);
   k_compute_r_t<FROM_T, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, alpha, tref, g,
-                                                                 planes_of(rho, 1, ctx), ctx->tslot, ctx->halo,
-                                                                 ctx->hoff, tj, r);
+                                                                 planes_of(rho, 1, ctx), tm->tslot, tm->halo,
+                                                                 tm->hoff, tj, r);
   return PDG_OK;
 }
 template <int TW>
 static int launch_wt_tile(pdg_ctx* ctx, const double* eta_g, const double* qb, const double* mis, double g, double* w,
                           cudaStream_t s) {
-  if (ensure_tiles(ctx, TW)) return PDG_ERR_CUDA;
-  const int tj = TW + ctx->nh_max;
+  const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
+  if (!tm) return PDG_ERR_CUDA;
+  const int tj = TW + tm->nh_max;
   const size_t sm = (size_t)2 * 12 * tj * sizeof(double);
   static size_t attr = 0;
   set_smem(k_compute_wtilde_t<TW>, sm, attr);
   k_compute_wtilde_t<TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, mis, g, planes_of(qb, 2, ctx),
-                                                              ctx->tslot, ctx->halo, ctx->hoff, tj, w);
+                                                              tm->tslot, tm->halo, tm->hoff, tj, w);
   return PDG_OK;
 }
+
 
 extern "C" {
 
@@ -2154,11 +2161,8 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, f3d2d
   if (const int tw = tune_get(TUNE_TILE_PRED); tw == 64 || tw == 128) {
-    if (ensure_tiles(ctx, tw)) return PDG_ERR_CUDA;
-    if (tw == 64)
-      launch_tile<2, 1, 64>(ctx, a, f3d2d, strm);
-    else
-      launch_tile<2, 1, 128>(ctx, a, f3d2d, strm);
+    if ((tw == 64 ? launch_tile<2, 1, 64>(ctx, a, f3d2d, strm) : launch_tile<2, 1, 128>(ctx, a, f3d2d, strm)))
+      return PDG_ERR_CUDA;
   } else if (tune_get(TUNE_HRHS) >= 8) {
     const int t = tune_get(TUNE_HRHS);
     if (t == 9)
@@ -2254,11 +2258,8 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out_u
   if (const int tw = tune_get(TUNE_TILE_STAGE); tw == 64 || tw == 128) {
-    if (ensure_tiles(ctx, tw)) return PDG_ERR_CUDA;
-    if (tw == 64)
-      launch_tile<3, 2, 64>(ctx, a, out_u, strm);
-    else
-      launch_tile<3, 2, 128>(ctx, a, out_u, strm);
+    if ((tw == 64 ? launch_tile<3, 2, 64>(ctx, a, out_u, strm) : launch_tile<3, 2, 128>(ctx, a, out_u, strm)))
+      return PDG_ERR_CUDA;
   } else if (tune_get(TUNE_HRHS2) >= 8) {
     const int t = tune_get(TUNE_HRHS2);
     if (t == 9)
