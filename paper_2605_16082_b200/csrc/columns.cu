@@ -1585,9 +1585,9 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
       k_vimpl_fwd<NCV, MB, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                 \
   }
     if (ncomp == 2) {
-      if (tune_get(TUNE_VIMPL) == 2) LAUNCH_FWD(2, 2) else LAUNCH_FWD(2, 1)
+      if (tune_get(TUNE_VIMPL) == 3) LAUNCH_FWD(2, 3) else LAUNCH_FWD(2, 1)
     } else {
-      if (tune_get(TUNE_VIMPL) == 2) LAUNCH_FWD(1, 2) else LAUNCH_FWD(1, 1)
+      if (tune_get(TUNE_VIMPL) == 3) LAUNCH_FWD(1, 3) else LAUNCH_FWD(1, 1)
     }
 #undef LAUNCH_FWD
     if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
@@ -1607,23 +1607,24 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
 #undef LAUNCH_ARGS
   } else if (!implicit && tune_get(TUNE_VSPLIT) == 3) {
     const size_t sm = vexpl2_smem(ncomp, ctx->L);
-#define LAUNCH_EX(NCV)                                                                                             \
+#define LAUNCH_EX(NCV, MB)                                                                                           \
   {                                                                                                                \
     static bool attr = false;                                                                                      \
     if (!attr) {                                                                                                   \
-      cudaFuncSetAttribute(k_vexpl2<NCV, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
-      cudaFuncSetAttribute(k_vexpl2<NCV, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
+      cudaFuncSetAttribute(k_vexpl2<NCV, MB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
+      cudaFuncSetAttribute(k_vexpl2<NCV, MB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
       attr = true;                                                                                                 \
     }                                                                                                              \
     if (a.kh == 0.0)                                                                                               \
-      k_vexpl2<NCV, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                      \
+      k_vexpl2<NCV, MB, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                      \
     else                                                                                                           \
-      k_vexpl2<NCV, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                     \
+      k_vexpl2<NCV, MB, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                     \
   }
-    if (ncomp == 2)
-      LAUNCH_EX(2)
-    else
-      LAUNCH_EX(1)
+    if (ncomp == 2) {
+      if (tune_get(TUNE_VEXPL) == 3) LAUNCH_EX(2, 3) else LAUNCH_EX(2, 1)
+    } else {
+      if (tune_get(TUNE_VEXPL) == 3) LAUNCH_EX(1, 3) else LAUNCH_EX(1, 1)
+    }
 #undef LAUNCH_EX
   } else {
 #define LAUNCH_ARGS m, a, dt, rhs, xin, x

@@ -397,12 +397,14 @@ int pdg_ext2d_subcycle(pdg_ctx* ctx, double* S, int msub, double dt, double g, d
     return PDG_ERR_CUDA;
   if (cudaMemsetAsync(qbar, 0, (size_t)6 * nt * sizeof(double), s) != cudaSuccess) return PDG_ERR_CUDA;
   const int variant = tune_get(TUNE_RK);
-  const int bs = variant == 2 || variant == 3 ? 128 : 256, nb = nblocks(ctx->nown, bs);
+  const int bs = variant == 2 || variant == 3 || variant == 5 || variant == 6 ? 128 : 256, nb = nblocks(ctx->nown, bs);
 #define RK_LAUNCH(ST, ...)                                                              \
   switch (variant) {                                                                    \
     case 2: k_rk_stage<ST, 128, 4><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
     case 3: k_rk_stage<ST, 128, 3><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
     case 4: k_rk_stage<ST, 256, 1><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
+    case 5: k_rk_stage<ST, 128, 6><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
+    case 6: k_rk_stage<ST, 128, 8><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
     default: k_rk_stage<ST, 256, 2><<<nb, bs, 0, s>>>(__VA_ARGS__); break;              \
   }
   for (int it = 0; it < msub; ++it) {
