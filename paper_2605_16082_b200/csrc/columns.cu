@@ -342,7 +342,7 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
   double jzq[6], ij[6];
   hq(G.jz, jzq);
 #pragma unroll
-  for (int q = 0; q < 6; ++q) ij[q] = QW[q] / jzq[q];
+  for (int q = 0; q < 6; ++q) ij[q] = KH0 ? QW[q] * drcp(jzq[q]) : QW[q] / jzq[q];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -365,7 +365,7 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
   const double tt = G.dztop[0] * G.dztop[0] + G.dztop[1] * G.dztop[1];
   V.tt = tt;
   V.hgt = ((G.jz[0] + G.jz[1]) + G.jz[2]) * (2.0 / 3.0);
-  V.rhgt = 1.0 / V.hgt;
+  V.rhgt = KH0 ? drcp(V.hgt) : 1.0 / V.hgt;
   V.nz = rsqrt(1.0 + tt);
 }
 
@@ -675,6 +675,24 @@ __device__ __forceinline__ int lu6r(double a[6][6], double rp[6]) {
     }
   }
   return -1;
+}
+// the same elimination without early exit and with branch-free reciprocals; returns the first
+// zero pivot or -1 (the caller reports it and abandons the column)
+__device__ __forceinline__ int lu6r_bf(double a[6][6], double rp[6]) {
+  int bad = -1;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    bad = (bad < 0 && a[k][k] == 0.0) ? k : bad;
+    const double inv = drcp(a[k][k]);
+    rp[k] = inv;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      a[i][k] = a[i][k] * inv;
+#pragma unroll
+      for (int j = k + 1; j < 6; ++j) a[i][j] = a[i][j] - a[i][k] * a[k][j];
+    }
+  }
+  return bad;
 }
 template <int NR>
 __device__ __forceinline__ void lu6r_solve(const double a[6][6], const double rp[6], double b[6][NR]) {
@@ -1023,7 +1041,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
         }
     }
     double rp[6];
-    const int bad = lu6r(d, rp);
+    const int bad = lu6r_bf(d, rp);
     if (bad >= 0) {
       report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
       return;
@@ -1329,13 +1347,13 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
         A1[p][q] = s;
         A1[q][p] = s;
       }
-    const double r0 = 1.0 / A1[0][0];
+    const double r0 = drcp(A1[0][0]);
     const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
     const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
     const double a22p = A1[2][2] - l20 * A1[0][2];
-    const double r1 = 1.0 / a11;
+    const double r1 = drcp(a11);
     const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
-    const double r2 = 1.0 / (a22p - l21 * a12);
+    const double r2 = drcp(a22p - l21 * a12);
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
       double y[6];

@@ -146,6 +146,16 @@ __device__ __forceinline__ void load_col2(const DMesh& m, int c, Col2& C) {
 }
 
 // ---------------------------------------------------------------- small helpers
+// branch-free double reciprocal: MUFU seed + two Newton steps (within 1 ulp of 1/x for normal
+// finite x; no IEEE slow-path call, so the scheduler can interleave it with independent work)
+__device__ __forceinline__ double drcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 // values at the 6 horizontal points of a corner field (c3 @ BARY.T)
 __device__ __forceinline__ void hq(const double c3[3], double out[6]) {
 #pragma unroll
