@@ -90,6 +90,28 @@ struct DMesh {
   pdg_err* err;
 };
 
+// branch-free double reciprocal: MUFU seed + two Newton steps (within 1 ulp of 1/x for normal
+// finite x; no IEEE slow-path call, so the scheduler can interleave it with independent work)
+__device__ __forceinline__ double drcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+// branch-free double square root of x > 0: rsqrt seed, two Newton steps, one Heron correction
+// (within 1 ulp of sqrt(x); the dry-cell checks reject x <= 0 before it matters)
+__device__ __forceinline__ double dsqrt_bf(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  r = r * fma(-hx * r, r, 1.5);
+  const double s0 = x * r;
+  return fma(0.5 * r, fma(-s0, s0, x), s0);
+}
+
 // per-column 2D data held in registers for a whole column
 struct Col {
   double j2d, dx[3], dy[3], el[3], nx[3], ny[3], b[3];
@@ -136,7 +158,7 @@ __device__ __forceinline__ void load_col2(const DMesh& m, int c, Col2& C) {
     C.nk[k] = (info >> 2) & 3;
     C.nb[k] = info >> 4;
   }
-  const double inv = 1.0 / C.j2d;
+  const double inv = drcp(C.j2d);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const int k = i == 2 ? 0 : i + 1;
@@ -146,16 +168,6 @@ __device__ __forceinline__ void load_col2(const DMesh& m, int c, Col2& C) {
 }
 
 // ---------------------------------------------------------------- small helpers
-// branch-free double reciprocal: MUFU seed + two Newton steps (within 1 ulp of 1/x for normal
-// finite x; no IEEE slow-path call, so the scheduler can interleave it with independent work)
-__device__ __forceinline__ double drcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 // values at the 6 horizontal points of a corner field (c3 @ BARY.T)
 __device__ __forceinline__ void hq(const double c3[3], double out[6]) {
 #pragma unroll
@@ -168,6 +180,12 @@ __device__ __forceinline__ void mh_apply3(const double v[3], double j2d, double 
   const double f = j2d / 24.0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) out[i] = (v[i] + s) * f;
+}
+// (6/J2D)(4 v - sum v) with f6 = 6/J2D precomputed
+__device__ __forceinline__ void mh_inv3f(const double v[3], double f6, double out[3]) {
+  const double s = (v[0] + v[1]) + v[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) out[i] = (4.0 * v[i] - s) * f6;
 }
 // (6/J2D)(4 v - sum v)  (columns.py:59-69)
 __device__ __forceinline__ void mh_inv3(const double v[3], double j2d, double out[3]) {

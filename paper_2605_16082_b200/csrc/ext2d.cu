@@ -20,7 +20,7 @@ struct Ext2DIn {
 };
 
 // residuals (before Mh^-1) of the free-surface and depth-momentum equations for column c
-template <class ColT>
+template <class ColT, bool FAST = false>
 __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, int c, const Ext2DIn& a,
                                                double re[3], double rx[3], double ry[3]) {
   const int nt = m.nt;
@@ -129,7 +129,7 @@ __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, in
     for (int h = 0; h < 2; ++h) {
       const double hi = ei[h] - bi[h], he = ee[h] - be[h];
       if (hi <= 0.0 || he <= 0.0) report(m.err, PDG_ERR_DRY, -1, 0, fmin(hi, he));
-      const double cel = sqrt(g * fmax(hi, he));   // == max(sqrt(g hi), sqrt(g he)) exactly
+      const double cel = FAST ? dsqrt_bf(g * fmax(hi, he)) : sqrt(g * fmax(hi, he));  // max(sqrt(g h))
       const double fe = nx * 0.5 * (xi[h] + xe[h]) + ny * 0.5 * (yi[h] + ye[h]) + cel * 0.5 * (ei[h] - ee[h]);
       const double hm = 0.5 * (hi + he);
       const double de = 0.5 * (ei[h] - ee[h]);
@@ -215,13 +215,14 @@ __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const
   Col2 C;
   load_col2(m, c, C);
   double r[3][3];
-  ext2d_residual(m, C, c, a, r[0], r[1], r[2]);
+  ext2d_residual<Col2, true>(m, C, c, a, r[0], r[1], r[2]);
   const double* X = nullptr;
   (void)X;
+  const double f6 = 6.0 * drcp(C.j2d);
 #pragma unroll
   for (int f = 0; f < 3; ++f) {
     double d[3];
-    mh_inv3(r[f], C.j2d, d);
+    mh_inv3f(r[f], f6, d);
     const double* Xf = f == 0 ? a.eta : (f == 1 ? a.qx : a.qy);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const
       } else if (STAGE == 1) {
         y = 0.75 * s0[f][k] + 0.25 * (Xf[k * nt + c] + dt * d[k]);
       } else {
-        y = s0[f][k] / 3.0 + (2.0 / 3.0) * (Xf[k * nt + c] + dt * d[k]);
+        y = s0[f][k] * (1.0 / 3.0) + (2.0 / 3.0) * (Xf[k * nt + c] + dt * d[k]);
       }
       Y[o] = y;
       if (STAGE == 2 && f > 0) qbar[(size_t)((f - 1) * 3 + k) * nt + c] = qb[f - 1][k] + y;
