@@ -366,7 +366,7 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
   V.tt = tt;
   V.hgt = ((G.jz[0] + G.jz[1]) + G.jz[2]) * (2.0 / 3.0);
   V.rhgt = KH0 ? drcp(V.hgt) : 1.0 / V.hgt;
-  V.nz = rsqrt(1.0 + tt);
+  V.nz = KH0 ? drsqrt(1.0 + tt) : rsqrt(1.0 + tt);
 }
 
 // interior penalty sigma (dg.py:161-173) with L = min(L_a, L_b): n0 (p+1)(p+3) / (2 3 L)

@@ -112,6 +112,15 @@ __device__ __forceinline__ double dsqrt_bf(double x) {
   return fma(0.5 * r, fma(-s0, s0, x), s0);
 }
 
+// branch-free 1/sqrt(x), x > 0: MUFU seed + two Newton steps (within ~1 ulp)
+__device__ __forceinline__ double drsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  return r * fma(-hx * r, r, 1.5);
+}
+
 // per-column 2D data held in registers for a whole column
 struct Col {
   double j2d, dx[3], dy[3], el[3], nx[3], ny[3], b[3];

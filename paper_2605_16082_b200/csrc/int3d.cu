@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
   const double ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
   const double ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
   const double j2d = C.j2d;
+  const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
   double prevb[3] = {0, 0, 0};
   for (int l = 0; l < L; ++l) {
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
       for (int a = 0; a < 3; ++a) dr[a] = 0.5 * (rho[a] - prevb[a]);
       const double sdr = (dr[0] + dr[1]) + dr[2];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) fi[a] = (dr[a] + sdr) / 24.0;
+      for (int a = 0; a < 3; ++a) fi[a] = (dr[a] + sdr) * (1.0 / 24.0);
 #pragma unroll
       for (int d = 0; d < 2; ++d)
 #pragma unroll
@@ -395,8 +396,8 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
       double gt[3], gb[3], out[6];
-      mh_inv3(acc[d], j2d, gt);
-      mh_inv3(acc[d] + 3, j2d, gb);
+      mh_inv3f(acc[d], f6, gt);
+      mh_inv3f(acc[d] + 3, f6, gb);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         s[d][a] = s[d][a] + (gt[a] + gb[a]);
@@ -425,6 +426,7 @@ __global__ void __launch_bounds__(128) k_compute_w(DMesh m, const double* __rest
   double eta[3];
   load_eta(eta_g, c, nt, eta);
   const double j2d = C.j2d;
+  const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[3] = {0, 0, 0};
   double ut_below[6][2];  // top-face q/Jz of layer l+1 at the 6 horizontal points
   for (int l = L - 1; l >= 0; --l) {
@@ -559,8 +561,8 @@ __global__ void __launch_bounds__(128) k_compute_w(DMesh m, const double* __rest
       for (int a = 0; a < 3; ++a) acc[3 + a] += mw[a];
     }
     double gt[3], gb[3], out[6];
-    mh_inv3(acc, j2d, gt);
-    mh_inv3(acc + 3, j2d, gb);
+    mh_inv3f(acc, f6, gt);
+    mh_inv3f(acc + 3, f6, gb);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       out[3 + a] = s[a] + gb[a] - gt[a];
@@ -606,6 +608,7 @@ __global__ void __launch_bounds__(128, MINB) k_compute_wtilde(DMesh m, const dou
     }
   }
   const double j2d = C.j2d;
+  const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[3] = {0, 0, 0};
   for (int l = L - 1; l >= 0; --l) {
     const double jm = 0.5 * (m.fracs[l + 1] - m.fracs[l]);
@@ -660,8 +663,8 @@ __global__ void __launch_bounds__(128, MINB) k_compute_wtilde(DMesh m, const dou
       lat_add(acc, k, f, -(0.5 * C.el[k]));
     }
     double gt[3], gb[3], out[6];
-    mh_inv3(acc, j2d, gt);
-    mh_inv3(acc + 3, j2d, gb);
+    mh_inv3f(acc, f6, gt);
+    mh_inv3f(acc + 3, f6, gb);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       out[3 + a] = s[a] + gb[a] - gt[a];
@@ -752,6 +755,7 @@ __global__ void __launch_bounds__(TW) k_compute_r_t(DMesh m, const double* __res
     ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
   }
   const double j2d = ts.act ? C.j2d : 0.0;
+  const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
   double prevb[3] = {0, 0, 0};
   cp_async_wait0();
@@ -806,7 +810,7 @@ __global__ void __launch_bounds__(TW) k_compute_r_t(DMesh m, const double* __res
         for (int a = 0; a < 3; ++a) dr[a] = 0.5 * (rho[a] - prevb[a]);
         const double sdr = (dr[0] + dr[1]) + dr[2];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) fi[a] = (dr[a] + sdr) / 24.0;
+        for (int a = 0; a < 3; ++a) fi[a] = (dr[a] + sdr) * (1.0 / 24.0);
 #pragma unroll
         for (int d = 0; d < 2; ++d)
 #pragma unroll
@@ -847,8 +851,8 @@ __global__ void __launch_bounds__(TW) k_compute_r_t(DMesh m, const double* __res
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
         double gt[3], gb[3], out[6];
-        mh_inv3(acc[d], j2d, gt);
-        mh_inv3(acc[d] + 3, j2d, gb);
+        mh_inv3f(acc[d], f6, gt);
+        mh_inv3f(acc[d] + 3, f6, gb);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           s[d][a] = s[d][a] + (gt[a] + gb[a]);
@@ -902,6 +906,7 @@ __global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* 
     }
   }
   const double j2d = ts.act ? C.j2d : 0.0;
+  const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[3] = {0, 0, 0};
   cp_async_wait0();
   __syncthreads();
@@ -948,8 +953,8 @@ __global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* 
         lat_add(acc, k, f, -(0.5 * C.el[k]));
       }
       double gt[3], gb[3], out[6];
-      mh_inv3(acc, j2d, gt);
-      mh_inv3(acc + 3, j2d, gb);
+      mh_inv3f(acc, f6, gt);
+      mh_inv3f(acc + 3, f6, gb);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         out[3 + a] = s[a] + gb[a] - gt[a];
