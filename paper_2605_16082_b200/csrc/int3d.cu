@@ -1308,7 +1308,9 @@ __device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, d
   }
 }
 
-template <int NC, int MODE, int MINB>
+// SAME: the stage values are the step-start values (stage 1: u == u0, T == T0), so M0 u0 reuses
+// the u words already loaded for the fluxes instead of loading them again
+template <int NC, int MODE, int MINB, bool SAME = false>
 __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
   __shared__ double sdm[shf::N * 64];
   __shared__ int sim[9 * 64];
@@ -1539,7 +1541,12 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double x0[6], m0x[6], o[6];
-        ld6(a.u0c[cc], l, c, L, nt, x0);
+        if (SAME) {
+#pragma unroll
+          for (int n = 0; n < 6; ++n) x0[n] = u[cc][n];
+        } else {
+          ld6(a.u0c[cc], l, c, L, nt, x0);
+        }
         kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
@@ -2271,6 +2278,8 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
       k_hrhs_s<3, 2, 6><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
     else if (t == 10)
       k_hrhs_s<3, 2, 8><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    else if (a.u0c[0] == a.uc[0] && a.u0c[1] == a.uc[1] && a.u0c[2] == a.uc[2])
+      k_hrhs_s<3, 2, 1, true><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
     else
       k_hrhs_s<3, 2, 1><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
   } else {
