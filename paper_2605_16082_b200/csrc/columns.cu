@@ -913,7 +913,7 @@ __device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmet
 // Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
 // (each thread stages and reads only its own words: no barriers), issued two layers ahead;
 // the previous layer's tile lives in shared memory, not in registers or L2.
-template <int NC, int MINB, bool KH0>
+template <int NC, int MINB, bool KH0, bool CT = false>
 __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, double dt, const double* rhs,
                                                         double* __restrict__ Gs, double* x) {
   
@@ -1056,7 +1056,8 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
       }
     if (l < L - 1) {
       // E = Dt^-1 [0; I3]: forward substitution starts at row 3
-      double* gt = Gs + (size_t)l * VT * nt + c;
+      constexpr int GT = CT ? 18 : VT;   // global tile words (CT: S0, S1 rebuilt by k_vimpl_bwd_r)
+      double* gt = Gs + (size_t)l * GT * nt + c;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         double t3 = j == 0 ? 1.0 : 0.0, t4 = j == 1 ? 1.0 : 0.0, t5 = j == 2 ? 1.0 : 0.0;
@@ -1085,8 +1086,10 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
           const double s1 = -dt * (P.cn * Vn.R[p][q]);
           tl[(18 + k) * VBLK + t] = s0;
           tl[(24 + k) * VBLK + t] = s1;
-          gt[(size_t)(18 + k) * nt] = s0;
-          gt[(size_t)(24 + k) * nt] = s1;
+          if (!CT) {
+            gt[(size_t)(18 + k) * nt] = s0;
+            gt[(size_t)(24 + k) * nt] = s1;
+          }
         }
     }
     Vp = V;
@@ -1136,6 +1139,99 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, con
         xn[i][cc] = v;
       }
     }
+  }
+}
+
+// BACKWARD with the coupling rebuilt: the tile holds only E_l (18 words); S0 = -dt (Fo + pb MHQ)
+// and S1 = -dt cn R_{l+1} are recomputed from the sigma geometry, w~ (top nodes of layer l+1) and
+// the mesh velocity with the forward kernel's own functions -- 12 fewer words written and read
+// per prism for ~200 FP64 operations in a kernel whose FP64 pipe is otherwise idle.
+template <int NC>
+__global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double dt, const double* __restrict__ Gs,
+                                                    double* x) {
+  const int c = blockIdx.x * VBLK + threadIdx.x;
+  const int nt = m.nt, L = m.L;
+  if (c >= m.nown || m.err->code == PDG_ERR_ZERO_PIVOT) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  Col C;
+  load_col(m, c, C);
+  double eta[3], e0[3], e1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    eta[k] = a.eta_u[k * nt + c];
+    e0[k] = a.eta0[k * nt + c];
+    e1[k] = a.eta1[k * nt + c];
+  }
+  const double j2d = C.j2d;
+  VG Vu;  // geometry of layer l + 1
+  vgeo<true>(C, eta, m.fracs[L - 1], m.fracs[L], Vu);
+  double xn[6][NC];
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = x[cc * P6 + ((size_t)i * L + L - 1) * nt + c];
+  for (int l = L - 2; l >= 0; --l) {
+    const double* gt = Gs + (size_t)l * 18 * nt + c;
+    double E[18];
+#pragma unroll
+    for (int e = 0; e < 18; ++e) E[e] = gt[(size_t)e * nt];
+    double gl[6][NC];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c];
+    double wtn[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    VG Vl;
+    vgeo<true>(C, eta, ft, fb, Vl);
+    double wm[6];
+    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    // Fo (vop_adv, bottom face of layer l) and the diffusion pieces cn, pb (vop_dif)
+    double Fo[3][3];
+    {
+      double a3[6], b3[6], sout[6];
+      hq(wtn, a3);
+      hq(wm + 3, b3);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double sb = a3[q] - b3[q];
+        sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
+      }
+      face3(sout, Fo);
+    }
+    const double kb = a.kv + a.kh * Vl.bb, ktn = a.kv + a.kh * Vu.tt;
+    const double cn = 0.5 * j2d * ktn;
+    const double pb = 0.5 * (pen_sigma(Vu, Vl, a.n0, a.order, m.err) * fmax(ktn, kb) * Vu.nz * j2d);
+    double S0[3][3], S1[3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        S0[p][q] = -dt * (Fo[p][q] + pb * MHQ[p][q]);
+        S1[p][q] = -dt * (cn * Vu.R[p][q]);
+      }
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      double dz[3], y[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dz[k] = DV[0] * xn[k][cc] + DV[1] * xn[3 + k][cc];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc = acc + S0[p][q] * xn[q][cc] - S1[p][q] * dz[q];
+        y[p] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double v = gl[i][cc] - (E[i * 3] * y[0] + E[i * 3 + 1] * y[1] + E[i * 3 + 2] * y[2]);
+        x[cc * P6 + ((size_t)i * L + l) * nt + c] = v;
+        xn[i][cc] = v;
+      }
+    }
+    Vu = Vl;
   }
 }
 
@@ -1583,7 +1679,28 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
-  if (implicit && tune_get(TUNE_VSPLIT) >= 2) {
+  if (implicit && tune_get(TUNE_VSPLIT) == 4 && kh == 0.0) {
+    double* Gs = ctx->ws3((size_t)18 * ctx->L * nt);
+    if (!Gs) return PDG_ERR_CUDA;
+    const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)vimpl_fwd_smem(2, 4096));
+      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)vimpl_fwd_smem(1, 4096));
+      attr = true;
+    }
+    if (ncomp == 2) {
+      k_vimpl_fwd<2, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+      if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+      k_vimpl_bwd_r<2><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
+    } else {
+      k_vimpl_fwd<1, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+      if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+      k_vimpl_bwd_r<1><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
+    }
+  } else if (implicit && tune_get(TUNE_VSPLIT) >= 2) {
     double* Gs = ctx->ws3((size_t)VT * ctx->L * nt);
     if (!Gs) return PDG_ERR_CUDA;
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
@@ -1623,7 +1740,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
       DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 1)
     }
 #undef LAUNCH_ARGS
-  } else if (!implicit && tune_get(TUNE_VSPLIT) == 3) {
+  } else if (!implicit && tune_get(TUNE_VSPLIT) >= 3) {
     const size_t sm = vexpl2_smem(ncomp, ctx->L);
 #define LAUNCH_EX(NCV, MB)                                                                                           \
   {                                                                                                                \

@@ -3,7 +3,8 @@
 The defaults (csrc/ctx.cu g_tune) are the measured-fastest variants; the alternatives stay in the
 library for A/B runs (scripts/ab_tune.py) and must keep producing the same answer:
   key 7  vertical stage: 1 fused block Thomas (36-double tiles), 2 split factored Thomas with the
-         unstaged explicit kernel, 3 split Thomas + cp.async-staged explicit kernel
+         unstaged explicit kernel, 3 split Thomas + cp.async-staged explicit kernel, 4 as 3 with
+         the coupling blocks S0, S1 rebuilt in the back substitution (18-double tiles)
   key 9  F3D->2D: 0 register kernel, 64 / 128 tile-staged (shared-memory neighbour traces)
   key 11 r / w~: 0 register kernels, 64 / 128 tile-staged
   key 5  stage RHS: 1 register kernel (128-thread blocks), 8 shared-memory column constants
@@ -53,7 +54,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("setting,tol", [
-    ({7: 1}, 1e-11), ({7: 2}, 1e-11),
+    ({7: 1}, 1e-11), ({7: 2}, 1e-11), ({7: 3}, 1e-13),
     ({9: 0}, 0.0), ({9: 64}, 0.0),
     ({11: 0}, 0.0), ({11: 64}, 0.0),
     ({5: 1}, 1e-12), ({10: 128}, 1e-12),
