@@ -14,8 +14,8 @@ KEYS = {
     "f3d2d": ["k_hrhs_t<2, 1"],
     "wtilde": ["k_compute_wtilde_t"],
     "rhs_uT": ["k_hrhs_s<3, 2"],
-    "vertical_u_impl": ["k_vimpl_fwd<2", "k_vimpl_bwd<2"],
-    "vertical_T_impl": ["k_vimpl_fwd<1", "k_vimpl_bwd<1"],
+    "vertical_u_impl": ["k_vimpl_fwd<2", "k_vimpl_bwd_r<2"],
+    "vertical_T_impl": ["k_vimpl_fwd<1", "k_vimpl_bwd_r<1"],
     "vertical_u_expl": ["k_vexpl2<2"],
     "vertical_T_expl": ["k_vexpl2<1"],
     "rk_stage": ["k_rk_stage<1"],
