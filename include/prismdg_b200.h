@@ -120,6 +120,11 @@ int pdg_ext2d_subcycle_begin(pdg_ctx* ctx, const double* state, double g, double
 int pdg_ext2d_rk_stage(pdg_ctx* ctx, int stage, const double* X, const double* S0, double* Y, double dt, double g,
                        double rho0, const double* f3d2d, const double* source, const double* patm, int has_bc,
                        double eta_bc, double* qbar, void* stream);
+/* one RK stage over the columns els[0..n_els) only (partitioned runs: the columns next to ghost
+ * columns first, then the interior while the halo exchange of the boundary values is in flight) */
+int pdg_ext2d_rk_stage_cols(pdg_ctx* ctx, int stage, const double* X, const double* S0, double* Y, double dt,
+                            double g, double rho0, const double* f3d2d, double* qbar, const int* els, int n_els,
+                            void* stream);
 int pdg_ext2d_subcycle_end(pdg_ctx* ctx, const double* state, const double* f3d2d, int m, double dt, double* qbar,
                            double* f2d, void* stream);
 /* check_cfl on device; writes the ratio to ratio_dev[0] (device) and the error word */

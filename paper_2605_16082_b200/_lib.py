@@ -36,6 +36,7 @@ _SIGS = {
     "pdg_ext2d_subcycle_begin": (I, [P, P, D, D, I, P, P]),
     "pdg_ext2d_rk_stage": (I, [P, I, P, P, P, D, D, D, P, P, P, I, D, P, P]),
     "pdg_ext2d_subcycle_end": (I, [P, P, P, I, D, P, P, P]),
+    "pdg_ext2d_rk_stage_cols": (I, [P, I, P, P, P, D, D, D, P, P, P, I, P]),
     "pdg_halo_pack": (I, [P, LL, I, P, I, P, P]),
     "pdg_halo_unpack": (I, [P, LL, I, P, I, P, P]),
     "pdg_ext2d_eval": (I, [P, P, P, P, P, P, P, I, D, D, D, P, I, I, P, P, P, P]),

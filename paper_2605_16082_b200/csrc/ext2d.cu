@@ -193,12 +193,16 @@ __global__ void k_ext2d_eval(DMesh m, Ext2DIn a, const int* __restrict__ els, in
 
 // one SSP-RK3 stage: X = state evaluated, S0 = substep start (3 fields x C3), Y = output.
 // STAGE 0: Y = S0 + dt d(X);  1: Y = 3/4 S0 + 1/4 (X + dt d);  2: Y = S0/3 + 2/3 (X + dt d), qbar += Y.q
+// els (optional): the columns to update (partitioned runs split owned columns into those next to
+// ghost columns and the interior, so the halo exchange overlaps the interior update)
 template <int STAGE, int BS = 256, int MINB = 2>
 __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
-                                                     double* Y, double dt, double* __restrict__ qbar) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+                                                     double* Y, double dt, double* __restrict__ qbar,
+                                                     const int* __restrict__ els = nullptr, int n_els = 0) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
-  if (c >= m.nown) return;
+  if (i >= (els ? n_els : m.nown)) return;
+  const int c = els ? els[i] : i;
   // issue the substep-start and Qbar loads first: they are independent of the flux work below,
   // so their latency overlaps it instead of being exposed at the end (stages 1, 2)
   double s0[3][3], qb[2][3];
@@ -458,6 +462,25 @@ int pdg_ext2d_rk_stage(pdg_ctx* ctx, int stage, const double* X, const double* S
   else
     k_rk_stage<2><<<nb, bs, 0, s>>>(m, a, S0, Y, dt, qbar);
   (void)bs;
+  return check_launch(ctx);
+}
+
+// the same stage over an explicit column list (partitioned runs: boundary / interior columns)
+int pdg_ext2d_rk_stage_cols(pdg_ctx* ctx, int stage, const double* X, const double* S0, double* Y, double dt,
+                            double g, double rho0, const double* f3d2d, double* qbar, const int* els, int n_els,
+                            void* stream) {
+  if (n_els <= 0) return PDG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nt = ctx->nt;
+  DMesh m = ctx->view();
+  const int nb = nblocks(n_els, 128);
+  Ext2DIn a{X, X + (size_t)3 * nt, X + (size_t)6 * nt, f3d2d, nullptr, nullptr, 0, 0.0, g, rho0};
+  if (stage == 0)
+    k_rk_stage<0, 128, 4><<<nb, 128, 0, s>>>(m, a, S0, Y, dt, qbar, els, n_els);
+  else if (stage == 1)
+    k_rk_stage<1, 128, 4><<<nb, 128, 0, s>>>(m, a, S0, Y, dt, qbar, els, n_els);
+  else
+    k_rk_stage<2, 128, 4><<<nb, 128, 0, s>>>(m, a, S0, Y, dt, qbar, els, n_els);
   return check_launch(ctx);
 }
 

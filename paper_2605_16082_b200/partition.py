@@ -171,6 +171,12 @@ class DistHalo:
         self.host_staging = dist.is_initialized() and dist.get_backend() == "gloo" and device.type == "cuda"
 
     def exchange(self, fields):
+        self.start(fields)
+        self.finish(fields)
+
+    def start(self, fields):
+        """Pack the owned boundary values and post the sends / receives (asynchronous: with NCCL the
+        transfer runs on its own stream while the caller launches interior work)."""
         import torch
         import torch.distributed as dist
         tot = sum(f.numel() // self.nt for f in fields)
@@ -187,12 +193,18 @@ class DistHalo:
                 ops.append(dist.P2POp(dist.isend, sends[peer], peer))
             if peer in recvs:
                 ops.append(dist.P2POp(dist.irecv, recvs[peer], peer))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+        works = dist.batch_isend_irecv(ops) if ops else []
+        self._pending = (sends, recvs, works)
+
+    def finish(self, fields):
+        """Wait for the posted transfers (a stream dependency with NCCL) and fill the ghost slots."""
+        sends, recvs, works = self._pending
+        for w in works:
+            w.wait()
         for peer, idx in self.maps.recv.items():
             buf = recvs[peer].to(self.device) if self.host_staging else recvs[peer]
             _unpack(fields, self.nt, idx, buf)
+        self._pending = None
         self.exchanges += 1
 
 
@@ -274,17 +286,22 @@ class PartitionedRun:
             if self.group is not None:
                 gens = {r: st._step_gen(st.t) for r, st in self.st.items()}
                 while True:
-                    fields, done = [], 0
+                    fields, phases, done = [], set(), 0
                     for r in self.ranks:          # every rank runs the same phase, then one exchange
                         try:
-                            fields.append(next(gens[r]))
+                            ph, f = next(gens[r])
+                            phases.add(ph)
+                            fields.append(f)
                         except StopIteration:
                             done += 1
                     if done:
                         if done != len(self.ranks):
                             raise MapMismatch("ranks reached different exchange points")
                         break
-                    self.group.exchange_all(fields)
+                    if len(phases) != 1:
+                        raise MapMismatch(f"ranks at different exchange phases {phases}")
+                    if phases != {"start"}:       # one device: the copies happen at "finish"
+                        self.group.exchange_all(fields)
             else:
                 for st in self.st.values():
                     st._launch_step(st.t)

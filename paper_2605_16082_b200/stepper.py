@@ -68,6 +68,12 @@ class ImexStepper:
         self.qsum, self.htot, self.f3d2d = z(2, 3, nt), z(3, nt), z(2, 3, nt)
         self.qbar, self.f2d, self.mis = z(2, 3, nt), z(2, 3, nt), z(2, 3, nt)
         self.W12 = (z(3, 3, nt), z(3, 3, nt)) if part is not None else None   # RK stage states (partitioned)
+        self.cols2d = None     # (boundary, interior) owned columns of a partition, device int32
+        if part is not None:
+            nb = np.asarray(mesh.nbr)[:part.n_own]
+            nxt = (nb >= part.n_own).any(axis=1)          # reads a ghost column
+            self.cols2d = tuple(torch.as_tensor(np.flatnonzero(sel).astype(np.int32), device=self.dev)
+                                for sel in (nxt, ~nxt))
         self.cur = 0
         self.t = 0.0
         self.graphs = {}
@@ -127,7 +133,7 @@ class ImexStepper:
         tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
            ptr(self.qsum), ptr(self.htot), s)
         if part:
-            yield [self.q]
+            yield ("all", [self.q])
         tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
         Sw.copy_(self.S)
@@ -138,17 +144,22 @@ class ImexStepper:
         else:
             tm("sub_begin", lb.pdg_ext2d_subcycle_begin, h, ptr(Sw), p.g, dt2, 1, ptr(self.qbar), s)
             W1, W2 = self.W12
+            bnd, intr = self.cols2d
             for _ in range(m_s):
                 for k, (X, Y) in enumerate(((Sw, W1), (W1, W2), (W2, Sw))):
-                    tm(f"rk{k}", lb.pdg_ext2d_rk_stage, h, k, ptr(X), ptr(Sw), ptr(Y), dt2, p.g, p.rho0,
-                       ptr(self.f3d2d), None, None, 0, 0.0, ptr(self.qbar), s)
-                    yield [Y]
+                    # columns next to ghosts first; their values travel while the interior updates
+                    tm(f"rk{k}", lb.pdg_ext2d_rk_stage_cols, h, k, ptr(X), ptr(Sw), ptr(Y), dt2, p.g, p.rho0,
+                       ptr(self.f3d2d), ptr(self.qbar), ptr(bnd), bnd.numel(), s)
+                    yield ("start", [Y])
+                    tm(f"rk{k}", lb.pdg_ext2d_rk_stage_cols, h, k, ptr(X), ptr(Sw), ptr(Y), dt2, p.g, p.rho0,
+                       ptr(self.f3d2d), ptr(self.qbar), ptr(intr), intr.numel(), s)
+                    yield ("finish", [Y])
             tm("sub_end", lb.pdg_ext2d_subcycle_end, h, ptr(Sw), ptr(self.f3d2d), m_s, dt2, ptr(self.qbar),
                ptr(self.f2d), s)
         eta1 = Sw[0]
         tm("mismatch", lb.pdg_mismatch, h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s)
         if part:
-            yield [self.mis]
+            yield ("all", [self.mis])
         tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
            ptr(self.wt), s)
         if self.fuse_rhs:
@@ -166,14 +177,14 @@ class ImexStepper:
                p.kappa_h, self.kv, p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u),
                ptr(out_T), ptr(T), ptr(out_T), s)
             if part:
-                yield [out_u, out_T]
+                yield ("all", [out_u, out_T])
             return eta1
         tm(f"vertical_u_{tag}", lb.pdg_step_vertical, h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
         tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
         if part:
-            yield [out_u, out_T]
+            yield ("all", [out_u, out_T])
         return eta1
 
     def _step_gen(self, t0):
@@ -187,8 +198,13 @@ class ImexStepper:
         self.S.copy_(self.Sw[1])
 
     def _launch_step(self, t0):
-        for fields in self._step_gen(t0):
-            self.halo.exchange(fields)
+        for phase, fields in self._step_gen(t0):
+            if phase == "all":
+                self.halo.exchange(fields)
+            elif phase == "start":
+                self.halo.start(fields)
+            else:
+                self.halo.finish(fields)
 
     def _advance(self):
         self.cur = (self.cur + 2) % 3
