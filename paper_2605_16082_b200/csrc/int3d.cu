@@ -729,7 +729,7 @@ __device__ __forceinline__ void nb4_s(const double* S, int tj, int w0, int k2, i
 
 // tiled baroclinic head (k_compute_r<FROM_T> with T / rho' staged: 6 words per column)
 template <bool FROM_T, int TW>
-__global__ void __launch_bounds__(TW) k_compute_r_t(DMesh m, const double* __restrict__ eta_g, double alpha,
+__global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const double* __restrict__ eta_g, double alpha,
                                                    double tref, double g, const __grid_constant__ StagePlanes sp,
                                                    const int* __restrict__ tslot, const int* __restrict__ halo,
                                                    const int* __restrict__ hoff, int tj, double* __restrict__ r) {
