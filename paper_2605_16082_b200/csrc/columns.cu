@@ -909,6 +909,38 @@ __device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmet
   return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
 }
 
+// Per-thread column constants parked in shared memory and re-read (volatile) inside the layer
+// loop: J2D, grad phi, bed and the three free surfaces are used every layer but would otherwise
+// pin ~40 registers for the whole loop and get spilled to local memory by the 255-register
+// vertical kernels (the spill reloads were their main long-scoreboard stall).
+constexpr int NCS = 19;
+__device__ __forceinline__ void cs_put(double* cs, int t, const Col& C, const double eta[3], const double e0[3],
+                                       const double e1[3]) {
+  cs[t] = C.j2d;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    cs[(1 + k) * VBLK + t] = C.dx[k];
+    cs[(4 + k) * VBLK + t] = C.dy[k];
+    cs[(7 + k) * VBLK + t] = C.b[k];
+    cs[(10 + k) * VBLK + t] = eta[k];
+    cs[(13 + k) * VBLK + t] = e0[k];
+    cs[(16 + k) * VBLK + t] = e1[k];
+  }
+}
+__device__ __forceinline__ void cs_get(const double* csp, int t, Col& C, double eta[3], double e0[3], double e1[3]) {
+  const volatile double* cs = csp;
+  C.j2d = cs[t];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    C.dx[k] = cs[(1 + k) * VBLK + t];
+    C.dy[k] = cs[(4 + k) * VBLK + t];
+    C.b[k] = cs[(7 + k) * VBLK + t];
+    eta[k] = cs[(10 + k) * VBLK + t];
+    e0[k] = cs[(13 + k) * VBLK + t];
+    e1[k] = cs[(16 + k) * VBLK + t];
+  }
+}
+
 // FORWARD: assembles M1 - dt A per layer, eliminates, writes the compact tile and g_l (into x).
 // Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
 // (each thread stages and reads only its own words: no barriers), issued two layers ahead;
@@ -921,7 +953,8 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   extern __shared__ double smem[];
   double* ring = smem;                       // [3][NE][VBLK]
   double* tl = smem + 3 * NE * VBLK;         // [VT][VBLK]
-  double* fr = tl + VT * VBLK;               // [L+1]
+  double* cst = tl + VT * VBLK;              // [NCS][VBLK] column constants
+  double* fr = cst + NCS * VBLK;             // [L+1]
   const int t = threadIdx.x;
   const int c = blockIdx.x * VBLK + t;
   const int nt = m.nt, L = m.L;
@@ -952,13 +985,15 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     e0[k] = a.eta0[k * nt + c];
     e1[k] = a.eta1[k * nt + c];
   }
-  const double j2d = C.j2d;
+  cs_put(cst, t, C, eta, e0, e1);
   VG Vp, V, Vn;
   vgeo<KH0>(C, eta, fr[0], fr[1], V);
   Vp = V;
   Vn = V;
   double gp[6][NC];
   for (int l = 0; l < L; ++l) {
+    cs_get(cst, t, C, eta, e0, e1);
+    const double j2d = C.j2d;
     stage(l + 2);
     cp_async_wait1();  // layers l and l+1 have landed
     const double* cur = ring + (l % 3) * NE * VBLK + t;
@@ -1235,7 +1270,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
   }
 }
 
-inline size_t vimpl_fwd_smem(int nc, int L) { return ((size_t)3 * (6 * nc + 6) * VBLK + VT * VBLK + L + 1) * 8; }
+inline size_t vimpl_fwd_smem(int nc, int L) { return ((size_t)3 * (6 * nc + 6) * VBLK + (VT + NCS) * VBLK + L + 1) * 8; }
 
 // EXPLICIT: x = M1^-1 (rhs + dt A xin), A applied matrix free; M1^-1 = K^-1 (x) (J2D Mjz)^-1.
 template <int NC, int MINB>
@@ -1358,7 +1393,8 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   constexpr int NE = 12 * NC + 6;  // rhs, xin, w~
   extern __shared__ double smem[];
   double* ring = smem;             // [3][NE][VBLK]
-  double* fr = smem + 3 * NE * VBLK;
+  double* cst = smem + 3 * NE * VBLK;  // [NCS][VBLK] column constants
+  double* fr = cst + NCS * VBLK;
   const int t = threadIdx.x;
   const int c = blockIdx.x * VBLK + t;
   const int nt = m.nt, L = m.L;
@@ -1393,7 +1429,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
     e0[k] = a.eta0[k * nt + c];
     e1[k] = a.eta1[k * nt + c];
   }
-  const double j2d = C.j2d;
+  cs_put(cst, t, C, eta, e0, e1);
   constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
   constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
   VG Vp, V, Vn;
@@ -1406,6 +1442,8 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
 #pragma unroll
     for (int k = 0; k < 6; ++k) xa[cc][k] = 0.0;
   for (int l = 0; l < L; ++l) {
+    cs_get(cst, t, C, eta, e0, e1);
+    const double j2d = C.j2d;
     stage(l + 2);
     cp_async_wait1();
     const double* cur = ring + (l % 3) * NE * VBLK + t;
@@ -1483,7 +1521,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
     V = Vn;
   }
 }
-inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + L + 1) * 8; }
+inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1) * 8; }
 
 // EXPLICIT stage for momentum (2 comps) AND tracer in one pass: the geometry window, the
 // advective pieces of A and the M1 factorisation are shared; only the diffusion pieces differ.
