@@ -63,9 +63,13 @@ __global__ void k_project(DMesh m, const double* __restrict__ eta_g, const doubl
 #pragma unroll
   for (int k = 0; k < 3; ++k) b[k] = ldg(m.b + k * nt + c);
   double st[2][3] = {{0, 0, 0}, {0, 0, 0}}, sb[2][3] = {{0, 0, 0}, {0, 0, 0}}, hs[3] = {0, 0, 0};
+  double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
   for (int l = 0; l < L; ++l) {
+    const double ft = fcur, fb = fnext;
+    fcur = fnext;
+    fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
     double jz[3], jzq[6];
-    layer_jz(b, eta, m.fracs[l], m.fracs[l + 1], jz);
+    layer_jz(b, eta, ft, fb, jz);
     hq(jz, jzq);
     double u[2][6];
     ld6(ux, l, c, L, nt, u[0]);
@@ -760,11 +764,14 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
   double prevb[3] = {0, 0, 0};
   cp_async_wait0();
   __syncthreads();
+  double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
   for (int l = 0; l < L; ++l) {
     if (l + 1 < L) ts.issue(sbuf + (size_t)((l + 1) & 1) * 6 * tj, tj, sp, (size_t)(l + 1) * nt, halo);
     const double* S = sbuf + (size_t)(l & 1) * 6 * tj;
+    const double ft = fcur, fb = fnext;
+    fcur = fnext;
+    fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
     if (ts.act) {
-      const double ft = m.fracs[l], fb = m.fracs[l + 1];
       const double jm = 0.5 * (fb - ft);
       LGeo G;
       layer_geo(C, eta, ft, fb, G);
@@ -1377,8 +1384,11 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
   for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
     for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
+  double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
   for (int l = 0; l < L; ++l) {
-    const double ft = m.fracs[l], fb = m.fracs[l + 1];
+    const double ft = fcur, fb = fnext;
+    fcur = fnext;
+    fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
     const double jm = 0.5 * (fb - ft);
     double u[NC][6], qv[2][6];
 #pragma unroll
@@ -1658,11 +1668,14 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
     for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
   cp_async_wait0();
   __syncthreads();
+  double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
   for (int l = 0; l < L; ++l) {
     if (l + 1 < L) stage(l + 1);
     const double* S = sbuf + (size_t)(l & 1) * NW * tj;
+    const double ft = fcur, fb = fnext;
+    fcur = fnext;
+    fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
     if (act) {
-      const double ft = m.fracs[l], fb = m.fracs[l + 1];
       const double jm = 0.5 * (fb - ft);
       double u[NC][6], qv[2][6];
 #pragma unroll
