@@ -1436,7 +1436,11 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   vgeo<KH0>(C, eta, fr[0], fr[1], V);
   Vp = V;
   Vn = V;
-  double xa[NC][6], xc[NC][6];
+  // xin of layers l-1 (registers: its ring slot is refilled at the top of iteration l), l and
+  // l+1 (read from the ring where they are used)
+  // (NC == 1 keeps all three in registers: no pressure there, and the smem reads cost more)
+  constexpr bool XR = NC >= 2;
+  double xa[NC][6], xcr[NC][6];
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
@@ -1444,22 +1448,31 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   for (int l = 0; l < L; ++l) {
     cs_get(cst, t, C, eta, e0, e1);
     const double j2d = C.j2d;
+    if (XR && l > 0) {
+      const double* prv = ring + ((l + 2) % 3) * NE * VBLK + t;   // slot of layer l-1
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) xa[cc][k] = prv[(6 * NC + cc * 6 + k) * VBLK];
+    }
     stage(l + 2);
     cp_async_wait1();
     const double* cur = ring + (l % 3) * NE * VBLK + t;
     const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
     const double ft = fr[l], fb = fr[l + 1];
-    if (l == 0) {
+    if (!XR && l == 0) {
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) xc[cc][k] = cur[(6 * NC + cc * 6 + k) * VBLK];
+        for (int k = 0; k < 6; ++k) xcr[cc][k] = cur[(6 * NC + cc * 6 + k) * VBLK];
     }
-    double xb[NC][6];
+    double xbr[NC][6];
+    if (!XR) {
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc)
+      for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-      for (int k = 0; k < 6; ++k) xb[cc][k] = l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0;
+        for (int k = 0; k < 6; ++k) xbr[cc][k] = l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0;
+    }
     if (l < L - 1) vgeo<KH0>(C, eta, fb, fr[l + 2], Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
@@ -1490,8 +1503,13 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
     const double r2 = drcp(a22p - l21 * a12);
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
-      double y[6];
-      vop_apply(l, L, Vp, V, Vn, P, P, xa[cc], xc[cc], xb[cc], y);
+      double y[6], xc[6], xb[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        xc[k] = XR ? cur[(6 * NC + cc * 6 + k) * VBLK] : xcr[cc][k];
+        xb[k] = XR ? (l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0) : xbr[cc][k];
+      }
+      vop_apply(l, L, Vp, V, Vn, P, P, xa[cc], xc, xb, y);
 #pragma unroll
       for (int k = 0; k < 6; ++k) y[k] = cur[(cc * 6 + k) * VBLK] + dt * y[k];
       double o[6];
@@ -1510,13 +1528,15 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
       }
       st6(x + cc * P6, l, c, L, nt, o);
     }
+    if (!XR) {
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc)
+      for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        xa[cc][k] = xc[cc][k];
-        xc[cc][k] = xb[cc][k];
-      }
+        for (int k = 0; k < 6; ++k) {
+          xa[cc][k] = xcr[cc][k];
+          xcr[cc][k] = xbr[cc][k];
+        }
+    }
     Vp = V;
     V = Vn;
   }
