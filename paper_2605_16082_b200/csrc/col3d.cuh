@@ -18,6 +18,11 @@ __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// TMA bulk prefetch of a contiguous global range into L2 (16-byte aligned, size a multiple of 16):
+// one instruction warms a whole plane segment of a block's columns for the next layer
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ void ld6(const double* __restrict__ f, int l, int c, int L, int nt, double v[6]) {
 #pragma unroll

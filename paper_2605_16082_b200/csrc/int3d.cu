@@ -998,6 +998,7 @@ struct HArgs {
   const double* f2d;     // STAGE momentum: [2][3][nt]
   double g, f, rho0, tsx, tsy, cd, dt;
   int mass_terms;
+  int bulkpf;            // 1: L2 bulk prefetch of the tile's next-layer r planes (F3D->2D; nt even only)
   // per-component planes (momentum x, y[, tracer]); filled from u / u0 / out by the entry points
   const double* uc[3];
   const double* u0c[3];
@@ -1670,7 +1671,14 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
   __syncthreads();
   double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
   for (int l = 0; l < L; ++l) {
-    if (l + 1 < L) stage(l + 1);
+    if (l + 1 < L) {
+      stage(l + 1);
+      if (NC >= 2 && a.bulkpf && t < 12) {   // r is read per layer from global: warm it in L2
+        const int c0 = b * TW;
+        const unsigned segb = (unsigned)(min(TW, m.nown - c0) * 8 + 15) & ~15u;
+        bulk_prefetch_l2(a.r + (size_t)(t / 6) * P6 + ((size_t)(t % 6) * L + l + 1) * nt + c0, segb);
+      }
+    }
     const double* S = sbuf + (size_t)(l & 1) * NW * tj;
     const double ft = fcur, fb = fnext;
     fcur = fnext;
@@ -2181,6 +2189,7 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   a.tsx = tsx;
   a.tsy = tsy;
   a.cd = cd;
+  a.bulkpf = (tune_get(TUNE_BULKPF) & 1) && ctx->nt % 2 == 0;
   Cols cs{nullptr, ctx->nown};
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;

@@ -31,7 +31,7 @@ if __name__ == "__main__":
     c = make_case(name, with_state=(name != "c4"))
     st = S.ImexStepper(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v)
     lib = _lib.lib()
-    defaults = {k: lib.pdg_tune(k, -1) for k in range(12)}
+    defaults = {k: lib.pdg_tune(k, -1) for k in range(16)}
 
     def reset():
         st.cur, st.t = 0, 0.0
