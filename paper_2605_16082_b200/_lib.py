@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libprismdg_b200.so")
+# PDG_LIB selects an alternative in-tree build (A/B experiments); default: the in-tree library
+LIB_PATH = os.environ.get("PDG_LIB") or os.path.join(_HERE, "libprismdg_b200.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int

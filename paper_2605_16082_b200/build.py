@@ -28,10 +28,11 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(verbose=False, force=False, extra=()):
-    if not force and not needs_build():
+def build(verbose=False, force=False, extra=(), out=None):
+    """out: alternative library path (A/B builds with extra -D flags); default the in-tree library."""
+    if out is None and not force and not needs_build():
         return LIB
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" if out is None else "obj_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -44,15 +45,15 @@ def build(verbose=False, force=False, extra=()):
         objs.append(obj)
     failed = False
     for src, p in procs:
-        out = p.communicate()[0].decode()
+        log = p.communicate()[0].decode()
         if p.returncode != 0 or verbose:
-            sys.stderr.write(out)
+            sys.stderr.write(log)
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    cmd = ["nvcc", *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = ["nvcc", *ARCH, "-shared", "-o", out or LIB, *objs, "-lcudart"]
     subprocess.check_call(cmd)
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":

@@ -429,39 +429,52 @@ __device__ __forceinline__ void vop_adv(double j2d, int l, int L, const double w
         P.Sa[mm][b][a] = s;
       }
   }
-  // top face of the layer: surface keeps the interior trace; interior faces split by sign
-  double sp[6], spos[6], sneg[6];
+  // The sign-split parts sum to the whole (P1) speed whose face mass is exact in closed form, so
+  // only the positive parts are integrated point-wise: F(neg) = F(whole) - F(pos).
   {
+    double sp[6], spos[6];
     double d3[3] = {wt[0] - wm[0], wt[1] - wm[1], wt[2] - wm[2]};
     hq(d3, sp);
-  }
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    spos[q] = j2d * (l == 0 ? sp[q] : (sp[q] >= 0.0 ? sp[q] : 0.0));
-    sneg[q] = j2d * (l == 0 ? 0.0 : (sp[q] < 0.0 ? sp[q] : 0.0));
-  }
-  face3(spos, P.Ft);
-  face3(sneg, P.Fn);
-  if (l < L - 1) {
-    double a3[6], b3[6], sin_[6], sout[6];
-    hq(wtn, a3);
-    hq(wm + 3, b3);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double sb = a3[q] - b3[q];
-      sin_[q] = j2d * (sb <= 0.0 ? sb : 0.0);
-      sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
-    }
-    face3(sin_, P.Fi);
-    face3(sout, P.Fo);
-  } else {
+    for (int q = 0; q < 6; ++q) spos[q] = j2d * (l == 0 ? sp[q] : (sp[q] >= 0.0 ? sp[q] : 0.0));
+    face3(spos, P.Ft);
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        P.Fi[a][b] = 0.0;
-        P.Fo[a][b] = 0.0;
+      for (int b = a; b < 3; ++b) {
+        const double w = l == 0 ? P.Ft[a][b] : j2d * (T3[a][b][0] * d3[0] + T3[a][b][1] * d3[1] + T3[a][b][2] * d3[2]);
+        P.Fn[a][b] = w - P.Ft[a][b];
+        P.Fn[b][a] = P.Fn[a][b];
       }
+    if (l < L - 1) {
+      double a3[6], b3[6], sout[6], e3[3];
+      hq(wtn, a3);
+      hq(wm + 3, b3);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double sb = a3[q] - b3[q];
+        sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
+      }
+      face3(sout, P.Fo);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) e3[c] = wtn[c] - wm[3 + c];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b) {
+          const double w = j2d * (T3[a][b][0] * e3[0] + T3[a][b][1] * e3[1] + T3[a][b][2] * e3[2]);
+          P.Fi[a][b] = w - P.Fo[a][b];
+          P.Fi[b][a] = P.Fi[a][b];
+        }
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          P.Fi[a][b] = 0.0;
+          P.Fo[a][b] = 0.0;
+        }
+    }
   }
 }
 
