@@ -737,23 +737,26 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
                                                    double tref, double g, const __grid_constant__ StagePlanes sp,
                                                    const int* __restrict__ tslot, const int* __restrict__ halo,
                                                    const int* __restrict__ hoff, int tj, double* __restrict__ r) {
-  extern __shared__ double sbuf[];  // [2][6][tj]
+  extern __shared__ double sbuf[];  // [2][6][tj], then the sigma fractions [L + 1], then ints [6][TW]
   TileStage<6, TW> ts;
   ts.init(m, halo, hoff);
   const int c = ts.c, nt = m.nt, L = m.L, t = ts.t;
+  double* frs = sbuf + (size_t)2 * 6 * tj;
+  int* nsl = reinterpret_cast<int*>(frs + L + 1);   // [k][t] neighbour slot, [3 + k][t] its local edge
+  for (int i2 = t; i2 <= L; i2 += TW) frs[i2] = m.fracs[i2];
   const size_t P6 = (size_t)6 * L * nt;
   ts.issue(sbuf, tj, sp, 0, halo);
   Col C;
   double eta[3], ex = 0.0, ey = 0.0;
   EdgeNb E[3];
-  int sl[3];
   if (ts.act) {
     load_col(m, c, C);
     load_eta(eta_g, c, nt, eta);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       edge_setup(m, C, eta, eta_g, k, g, E[k]);
-      sl[k] = tslot[k * nt + c];
+      nsl[k * TW + t] = tslot[k * nt + c];
+      nsl[(3 + k) * TW + t] = E[k].k2;
     }
     ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
     ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
@@ -764,13 +767,10 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
   double prevb[3] = {0, 0, 0};
   cp_async_wait0();
   __syncthreads();
-  double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
   for (int l = 0; l < L; ++l) {
     if (l + 1 < L) ts.issue(sbuf + (size_t)((l + 1) & 1) * 6 * tj, tj, sp, (size_t)(l + 1) * nt, halo);
     const double* S = sbuf + (size_t)(l & 1) * 6 * tj;
-    const double ft = fcur, fb = fnext;
-    fcur = fnext;
-    fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
+    const double ft = frs[l], fb = frs[l + 1];
     if (ts.act) {
       const double jm = 0.5 * (fb - ft);
       LGeo G;
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
       for (int k = 0; k < 3; ++k) {
         if (C.tag[k] != 0) continue;
         double n4[4], dj[2][2];
-        nb4_s(S, tj, 0, E[k].k2, sl[k], n4);
+        nb4_s(S, tj, 0, nsl[(3 + k) * TW + t], nsl[k * TW + t], n4);
         if (FROM_T) {
 #pragma unroll
           for (int n = 0; n < 4; ++n) n4[n] = -alpha * (n4[n] - tref);
@@ -883,10 +883,12 @@ __global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* 
                                                         const __grid_constant__ StagePlanes sp,
                                                         const int* __restrict__ tslot, const int* __restrict__ halo,
                                                         const int* __restrict__ hoff, int tj, double* __restrict__ w) {
-  extern __shared__ double sbuf[];  // [2][12][tj]
+  extern __shared__ double sbuf[];  // [2][12][tj], then the sigma fractions [L + 1]
   TileStage<12, TW> ts;
   ts.init(m, halo, hoff);
   const int c = ts.c, nt = m.nt, L = m.L, t = ts.t;
+  double* frs = sbuf + (size_t)2 * 12 * tj;
+  for (int i2 = t; i2 <= L; i2 += TW) frs[i2] = m.fracs[i2];
   ts.issue(sbuf + (size_t)((L - 1) & 1) * 12 * tj, tj, sp, (size_t)(L - 1) * nt, halo);
   Col C;
   double eta[3];
@@ -921,7 +923,7 @@ __global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* 
     if (l > 0) ts.issue(sbuf + (size_t)((l - 1) & 1) * 12 * tj, tj, sp, (size_t)(l - 1) * nt, halo);
     const double* S = sbuf + (size_t)(l & 1) * 12 * tj;
     if (ts.act) {
-      const double jm = 0.5 * (m.fracs[l + 1] - m.fracs[l]);
+      const double jm = 0.5 * (frs[l + 1] - frs[l]);
       double qv[2][6];
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
@@ -1990,7 +1992,7 @@ static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, d
   const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
-  const size_t sm = (size_t)2 * 6 * tj * sizeof(double);
+  const size_t sm = ((size_t)2 * 6 * tj + ctx->L + 1) * sizeof(double) + (size_t)6 * TW * sizeof(int);
   static size_t attr = 0;
   set_smem(k_compute_r_t<FROM_T, TW>, sm, attr);
   k_compute_r_t<FROM_T, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, alpha, tref, g,
@@ -2004,7 +2006,7 @@ static int launch_wt_tile(pdg_ctx* ctx, const double* eta_g, const double* qb, c
   const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
-  const size_t sm = (size_t)2 * 12 * tj * sizeof(double);
+  const size_t sm = ((size_t)2 * 12 * tj + ctx->L + 1) * sizeof(double);
   static size_t attr = 0;
   set_smem(k_compute_wtilde_t<TW>, sm, attr);
   k_compute_wtilde_t<TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, mis, g, planes_of(qb, 2, ctx),
