@@ -22,7 +22,8 @@ struct Ext2DIn {
 // residuals (before Mh^-1) of the free-surface and depth-momentum equations for column c
 template <class ColT, bool FAST = false>
 __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, int c, const Ext2DIn& a,
-                                               double re[3], double rx[3], double ry[3]) {
+                                               double re[3], double rx[3], double ry[3],
+                                               double* own = nullptr) {  // optional: the own state [3][3]
   const int nt = m.nt;
   const double g = a.g;
   double e[3], x[3], y[3];
@@ -31,6 +32,14 @@ __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, in
     e[i] = a.eta[i * nt + c];
     x[i] = a.qx[i * nt + c];
     y[i] = a.qy[i * nt + c];
+  }
+  if (own) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      own[i] = e[i];
+      own[3 + i] = x[i];
+      own[6 + i] = y[i];
+    }
   }
   // ---- volume terms (external2d.py:145-148, 204-218)
   double xq = 0.0, yq = 0.0;
@@ -218,8 +227,8 @@ __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const
   }
   Col2 C;
   load_col2(m, c, C);
-  double r[3][3];
-  ext2d_residual<Col2, true>(m, C, c, a, r[0], r[1], r[2]);
+  double r[3][3], xo[9];
+  ext2d_residual<Col2, true>(m, C, c, a, r[0], r[1], r[2], xo);
   const double* X = nullptr;
   (void)X;
   const double f6 = 6.0 * drcp(C.j2d);
@@ -227,17 +236,16 @@ __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const
   for (int f = 0; f < 3; ++f) {
     double d[3];
     mh_inv3f(r[f], f6, d);
-    const double* Xf = f == 0 ? a.eta : (f == 1 ? a.qx : a.qy);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const size_t o = (size_t)(f * 3 + k) * nt + c;
       double y;
       if (STAGE == 0) {
-        y = S0[o] + dt * d[k];        // X == S0: this value is already in L1
+        y = xo[f * 3 + k] + dt * d[k];   // X == S0
       } else if (STAGE == 1) {
-        y = 0.75 * s0[f][k] + 0.25 * (Xf[k * nt + c] + dt * d[k]);
+        y = 0.75 * s0[f][k] + 0.25 * (xo[f * 3 + k] + dt * d[k]);
       } else {
-        y = s0[f][k] * (1.0 / 3.0) + (2.0 / 3.0) * (Xf[k * nt + c] + dt * d[k]);
+        y = s0[f][k] * (1.0 / 3.0) + (2.0 / 3.0) * (xo[f * 3 + k] + dt * d[k]);
       }
       Y[o] = y;
       if (STAGE == 2 && f > 0) qbar[(size_t)((f - 1) * 3 + k) * nt + c] = qb[f - 1][k] + y;
