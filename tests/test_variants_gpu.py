@@ -8,7 +8,7 @@ library for A/B runs (scripts/ab_tune.py) and must keep producing the same answe
   key 9  F3D->2D: 0 register kernel, 64 / 128 tile-staged (shared-memory neighbour traces)
   key 11 r / w~: 0 register kernels, 64 / 128 tile-staged
   key 5  stage RHS: 1 register kernel (128-thread blocks), 8 shared-memory column constants
-  key 6  2D RK stage occupancy variant
+  key 6  2D RK stage occupancy variant (register allocation can change FMA contraction)
 Tile-staged and register kernels do the same arithmetic (bitwise equal); the split Thomas and the
 branch-free reciprocals of the staged vertical kernels differ at rounding level.
 """
@@ -58,7 +58,7 @@ def rel(a, b):
     ({9: 0}, 0.0), ({9: 64}, 0.0),
     ({11: 0}, 0.0), ({11: 64}, 0.0),
     ({5: 1}, 1e-12), ({10: 128}, 1e-12),
-    ({6: 0}, 0.0), ({6: 3}, 0.0),
+    ({6: 0}, 1e-12), ({6: 3}, 1e-12),
 ])
 def test_variant_matches_default(case, setting, tol):
     pdg, c, lib, defaults = case
