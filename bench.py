@@ -362,8 +362,10 @@ def main():
                "config": {"workload": f"{args.config}: {case.mesh.nt} tri x {case.L} layers = {P} prisms, "
                                       f"m={case.m}, dt2d={case.dt2d} s, momentum+tracer, FP64",
                           "nt": case.mesh.nt, "L": case.L, "m": case.m, "prism_dof_per_step": dof_per_step,
-                          "parallelism": (f"column partition x{world} (Hilbert ranges, one-ring ghosts, NCCL "
-                                          "halo send/recv)") if world > 1 else "single GPU",
+                          "parallelism": (f"column partition x{world} (Hilbert ranges, one-ring ghosts, "
+                                          f"{'NCCL' if args.backend == 'nccl' else 'gloo host-staged'} halo "
+                                          "send/recv, 2D halos overlapped with interior columns)")
+                          if world > 1 else "single GPU",
                           "l2": "inputs larger than L2 (~48 GB resident fields)"},
                "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
