@@ -33,6 +33,19 @@ __device__ __forceinline__ void st6(double* __restrict__ f, int l, int c, int L,
   for (int k = 0; k < 6; ++k) f[((size_t)k * L + l) * nt + c] = v[k];
 }
 
+// read-only-path (ld.global.nc) variants for kernels whose inputs never alias their outputs
+__device__ __forceinline__ void ld6g(const double* f, int l, int c, int L, int nt, double v[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = __ldg(f + ((size_t)k * L + l) * nt + c);
+}
+__device__ __forceinline__ void ld_nb4g(const double* f, int k2, int e2, int l, int L, int nt, double n4[4]) {
+  const int a = EV0(k2), b = EV1(k2);
+  n4[0] = __ldg(f + ((size_t)a * L + l) * nt + e2);
+  n4[1] = __ldg(f + ((size_t)b * L + l) * nt + e2);
+  n4[2] = __ldg(f + ((size_t)(3 + a) * L + l) * nt + e2);
+  n4[3] = __ldg(f + ((size_t)(3 + b) * L + l) * nt + e2);
+}
+
 // L1 prefetch of the 6 node planes of layer l (issued one layer ahead: the thread-per-column
 // kernels run at ~8 warps/SM, too few to hide HBM latency, and have no registers to spare for
 // software pipelining -- a prefetch costs no register)

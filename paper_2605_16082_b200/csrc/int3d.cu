@@ -1395,9 +1395,9 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
     const double jm = 0.5 * (fb - ft);
     double u[NC][6], qv[2][6];
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) ld6(a.uc[cc], l, c, L, nt, u[cc]);
-    ld6(a.qa, l, c, L, nt, qv[0]);
-    ld6(a.qa + P6, l, c, L, nt, qv[1]);
+    for (int cc = 0; cc < NC; ++cc) ld6g(a.uc[cc], l, c, L, nt, u[cc]);
+    ld6g(a.qa, l, c, L, nt, qv[0]);
+    ld6g(a.qa + P6, l, c, L, nt, qv[1]);
     if (MODE == 2) {
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
@@ -1442,8 +1442,8 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
       double f[2][2];
       {
         double qn[2][4];
-        ld_nb4(a.qa, k2, e2, l, L, nt, qn[0]);
-        ld_nb4(a.qa + P6, k2, e2, l, L, nt, qn[1]);
+        ld_nb4g(a.qa, k2, e2, l, L, nt, qn[0]);
+        ld_nb4g(a.qa + P6, k2, e2, l, L, nt, qn[1]);
         if (MODE == 2) {
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
@@ -1461,7 +1461,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double n4[4], ti[2][2], te[2][2], x[2][2];
-        ld_nb4(a.uc[cc], k2, e2, l, L, nt, n4);
+        ld_nb4g(a.uc[cc], k2, e2, l, L, nt, n4);
         tr_own(u[cc], k, ti);
         tr_nb(n4, te);
 #pragma unroll
@@ -1479,8 +1479,8 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
     }
     if constexpr (NC >= 2) {
       double rr[2][6];
-      ld6(a.r, l, c, L, nt, rr[0]);
-      ld6(a.r + P6, l, c, L, nt, rr[1]);
+      ld6g(a.r, l, c, L, nt, rr[0]);
+      ld6g(a.r + P6, l, c, L, nt, rr[1]);
       double jz[3], Mu[3][3];
       layer_jz(bb, eta, ft, fb, jz);
       mjz(jz, Mu);
@@ -1558,7 +1558,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
           for (int n = 0; n < 6; ++n) x0[n] = u[cc][n];
         } else {
-          ld6(a.u0c[cc], l, c, L, nt, x0);
+          ld6g(a.u0c[cc], l, c, L, nt, x0);
         }
         kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
@@ -1775,8 +1775,8 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
       }
       if constexpr (NC >= 2) {
         double rr[2][6];
-        ld6(a.r, l, c, L, nt, rr[0]);
-        ld6(a.r + P6, l, c, L, nt, rr[1]);
+        ld6g(a.r, l, c, L, nt, rr[0]);
+        ld6g(a.r + P6, l, c, L, nt, rr[1]);
         double jz[3], Mu[3][3];
         layer_jz(C.b, eta, ft, fb, jz);
         mjz(jz, Mu);
@@ -1843,7 +1843,7 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
           double x0[6], m0x[6], o[6];
-          ld6(a.u0c[cc], l, c, L, nt, x0);
+          ld6g(a.u0c[cc], l, c, L, nt, x0);
           kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
           for (int n = 0; n < 6; ++n) {
