@@ -29,9 +29,9 @@ __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, in
   double e[3], x[3], y[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    e[i] = a.eta[i * nt + c];
-    x[i] = a.qx[i * nt + c];
-    y[i] = a.qy[i * nt + c];
+    e[i] = __ldg(a.eta + i * nt + c);
+    x[i] = __ldg(a.qx + i * nt + c);
+    y[i] = __ldg(a.qy + i * nt + c);
   }
   if (own) {
 #pragma unroll
@@ -106,8 +106,8 @@ __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, in
     if (C.tag[k] == 0) {
       const int e2 = C.nb[k], k2 = C.nk[k];
       const int n0 = EV0(k2) * nt + e2, n1 = EV1(k2) * nt + e2;
-      const double ea = a.eta[n0], eb = a.eta[n1], xa = a.qx[n0], xb = a.qx[n1];
-      const double ya = a.qy[n0], yb = a.qy[n1], ba = ldg(m.b + n0), bb = ldg(m.b + n1);
+      const double ea = __ldg(a.eta + n0), eb = __ldg(a.eta + n1), xa = __ldg(a.qx + n0), xb = __ldg(a.qx + n1);
+      const double ya = __ldg(a.qy + n0), yb = __ldg(a.qy + n1), ba = ldg(m.b + n0), bb = ldg(m.b + n1);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         ee[h] = ea * ES[h][1] + eb * ES[h][0];
@@ -156,8 +156,8 @@ __device__ __forceinline__ void ext2d_residual(const DMesh& m, const ColT& C, in
   if (a.f3d2d) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      rx[i] += a.f3d2d[i * nt + c];
-      ry[i] += a.f3d2d[(3 + i) * nt + c];
+      rx[i] += __ldg(a.f3d2d + i * nt + c);
+      ry[i] += __ldg(a.f3d2d + (3 + i) * nt + c);
     }
   }
   if (a.source) {
