@@ -169,36 +169,51 @@ class DistHalo:
         # gloo cannot send CUDA tensors: stage the packed messages through host memory (lets the
         # multi-process path run -- and be tested -- with several ranks sharing one GPU)
         self.host_staging = dist.is_initialized() and dist.get_backend() == "gloo" and device.type == "cuda"
+        self._plans = {}   # planes per column -> (send buffers, recv buffers, P2P ops), reused every step
 
     def exchange(self, fields):
         self.start(fields)
         self.finish(fields)
 
+    def _plan(self, tot):
+        """Message buffers and the P2P op list for `tot` planes per column, allocated once: an
+        exchange is always finished before the next one starts, so reuse is stream-ordered."""
+        import torch
+        import torch.distributed as dist
+        plan = self._plans.get(tot)
+        if plan is None:
+            sends = {p: torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
+                     for p, idx in self.maps.send.items()}
+            recvs = {p: torch.empty(tot * idx.numel(), dtype=torch.float64,
+                                    device="cpu" if self.host_staging else self.device)
+                     for p, idx in self.maps.recv.items()}
+            hsend = {p: torch.empty(b.numel(), dtype=torch.float64, pin_memory=True) for p, b in sends.items()} \
+                if self.host_staging else sends
+            ops = []
+            for peer in sorted(set(sends) | set(recvs)):
+                if peer in sends:
+                    ops.append(dist.P2POp(dist.isend, hsend[peer], peer))
+                if peer in recvs:
+                    ops.append(dist.P2POp(dist.irecv, recvs[peer], peer))
+            plan = self._plans[tot] = (sends, hsend, recvs, ops)
+        return plan
+
     def start(self, fields):
         """Pack the owned boundary values and post the sends / receives (asynchronous: with NCCL the
         transfer runs on its own stream while the caller launches interior work)."""
-        import torch
         import torch.distributed as dist
         tot = sum(f.numel() // self.nt for f in fields)
-        sends, recvs, ops = {}, {}, []
+        sends, hsend, recvs, ops = self._plan(tot)
         for peer, idx in self.maps.send.items():
-            buf = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
-            _pack(fields, self.nt, idx, buf)
-            sends[peer] = buf.cpu() if self.host_staging else buf
-        for peer, idx in self.maps.recv.items():
-            recvs[peer] = torch.empty(tot * idx.numel(), dtype=torch.float64,
-                                      device="cpu" if self.host_staging else self.device)
-        for peer in sorted(set(sends) | set(recvs)):
-            if peer in sends:
-                ops.append(dist.P2POp(dist.isend, sends[peer], peer))
-            if peer in recvs:
-                ops.append(dist.P2POp(dist.irecv, recvs[peer], peer))
+            _pack(fields, self.nt, idx, sends[peer])
+            if self.host_staging:
+                hsend[peer].copy_(sends[peer])
         works = dist.batch_isend_irecv(ops) if ops else []
-        self._pending = (sends, recvs, works)
+        self._pending = (recvs, works)
 
     def finish(self, fields):
         """Wait for the posted transfers (a stream dependency with NCCL) and fill the ghost slots."""
-        sends, recvs, works = self._pending
+        recvs, works = self._pending
         for w in works:
             w.wait()
         for peer, idx in self.maps.recv.items():
