@@ -49,3 +49,40 @@ def maps(nbr, weights, P):
             recv[r].setdefault(s, []).append(n_own + pos)
             send[s].setdefault(r, []).append(g - bounds[s])
     return bounds, ghosts, send, recv
+
+
+def deep_maps(nbr, weights, P, depth):
+    """Ghost rings by breadth-first layers (ring k+1 = edge neighbours of ring k not yet local),
+    all ghosts ascending; recv/send over all rings and restricted to ring 1 (plain loops)."""
+    own, bounds = owners(weights, P)
+    ghosts, rings = [], []
+    for r in range(P):
+        lo, hi = bounds[r], bounds[r + 1]
+        local = set(range(lo, hi))
+        front = list(range(lo, hi))
+        ring_of = {}
+        for k in range(1, depth + 1):
+            nxt = set()
+            for c in front:
+                for e in nbr[c]:
+                    if e >= 0 and e not in local:
+                        nxt.add(int(e))
+            for e in nxt:
+                ring_of[e] = k
+            local |= nxt
+            front = sorted(nxt)
+        gs = sorted(ring_of)
+        ghosts.append(gs)
+        rings.append([ring_of[g] for g in gs])
+    send, recv = [dict() for _ in range(P)], [dict() for _ in range(P)]
+    send1, recv1 = [dict() for _ in range(P)], [dict() for _ in range(P)]
+    for r in range(P):
+        n_own = bounds[r + 1] - bounds[r]
+        for pos, g in enumerate(ghosts[r]):
+            s = own[g]
+            recv[r].setdefault(s, []).append(n_own + pos)
+            send[s].setdefault(r, []).append(g - bounds[s])
+            if rings[r][pos] == 1:
+                recv1[r].setdefault(s, []).append(n_own + pos)
+                send1[s].setdefault(r, []).append(g - bounds[s])
+    return bounds, ghosts, rings, send, recv, send1, recv1

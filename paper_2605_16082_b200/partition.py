@@ -23,6 +23,8 @@ import numpy as np
 
 from .errors import MapMismatch, TooManyRanks
 
+GHOST_DEPTH = 3   # ghost rings of a partition: the 2D sub-cycle exchanges once per substep
+
 
 @dataclass
 class Part:
@@ -30,9 +32,12 @@ class Part:
     nparts: int
     lo: int                     # owned global range [lo, hi)
     hi: int
-    ghosts: np.ndarray          # global ids of ghost columns (ascending)
-    send: dict = field(default_factory=dict)   # peer -> local indices (owned) to send
-    recv: dict = field(default_factory=dict)   # peer -> local indices (ghost slots) to fill
+    ghosts: np.ndarray          # global ids of ghost columns (ascending; all rings)
+    send: dict = field(default_factory=dict)   # peer -> local indices (owned) to send (all rings)
+    recv: dict = field(default_factory=dict)   # peer -> local indices (ghost slots) to fill (all rings)
+    ring: np.ndarray = None     # ring (1..depth) of every ghost
+    send1: dict = field(default_factory=dict)  # the same restricted to ring-1 ghosts (3D exchanges)
+    recv1: dict = field(default_factory=dict)
 
     @property
     def n_own(self) -> int:
@@ -64,8 +69,12 @@ def split_ranges(weights, P):
     return np.asarray(bounds, dtype=np.int64)
 
 
-def decompose(mesh, P: int, layers=None):
-    """list of Part for ranks 0..P-1."""
+def decompose(mesh, P: int, layers=None, depth: int = 1):
+    """list of Part for ranks 0..P-1.
+
+    depth > 1 adds ghost rings: ring k+1 = the edge neighbours of ring k not already local.  The
+    2D sub-cycle then exchanges once per substep (its three RK stages run redundantly on rings
+    1-2 and 1) while the 3D fields only ever need ring 1 (send1 / recv1)."""
     nt = mesh.nt
     weights = np.ones(nt, np.int64) if layers is None else np.asarray(layers, np.int64)
     b = split_ranges(weights, P)
@@ -74,16 +83,33 @@ def decompose(mesh, P: int, layers=None):
     nbr = np.asarray(mesh.nbr)
     for r in range(P):
         lo, hi = int(b[r]), int(b[r + 1])
-        nb = nbr[lo:hi].ravel()
-        nb = nb[nb >= 0]
-        ghosts = np.unique(nb[(nb < lo) | (nb >= hi)])
-        parts.append(Part(r, P, lo, hi, ghosts))
+        local = np.zeros(nt, bool)
+        local[lo:hi] = True
+        front = np.arange(lo, hi)
+        rings = []
+        for _ in range(depth):
+            nb = nbr[front].ravel()
+            nb = np.unique(nb[nb >= 0])
+            nb = nb[~local[nb]]
+            local[nb] = True
+            rings.append(nb)
+            front = nb
+        ghosts = np.concatenate(rings) if rings else np.zeros(0, np.int64)
+        ring = np.concatenate([np.full(g.size, k + 1, np.int32) for k, g in enumerate(rings)]) if rings else \
+            np.zeros(0, np.int32)
+        order = np.argsort(ghosts, kind="stable")
+        parts.append(Part(r, P, lo, hi, ghosts[order], ring=ring[order]))
     for r, p in enumerate(parts):
         for s in np.unique(owner[p.ghosts]) if p.ghosts.size else []:
             s = int(s)
-            sel = p.ghosts[owner[p.ghosts] == s]                      # ascending global ids
-            p.recv[s] = (p.n_own + np.searchsorted(p.ghosts, sel)).astype(np.int32)
+            mine = owner[p.ghosts] == s
+            sel = p.ghosts[mine]                                      # ascending global ids
+            p.recv[s] = (p.n_own + np.flatnonzero(mine)).astype(np.int32)
             parts[s].send[r] = (sel - parts[s].lo).astype(np.int32)
+            one = mine & (p.ring == 1)
+            if one.any():
+                p.recv1[s] = (p.n_own + np.flatnonzero(one)).astype(np.int32)
+                parts[s].send1[r] = (p.ghosts[one] - parts[s].lo).astype(np.int32)
     for p in parts:
         for s, idx in p.recv.items():
             if parts[s].send.get(p.rank) is None or parts[s].send[p.rank].size != idx.size:
@@ -112,13 +138,14 @@ def local_mesh(mesh, part: Part):
 # ----------------------------------------------------------------------------- exchange
 
 class _Maps:
-    """Device copies of one rank's send / recv index lists."""
+    """Device copies of one rank's send / recv index lists (all rings, and ring 1 only)."""
 
-    def __init__(self, part: Part, device):
+    def __init__(self, part: Part, device, deep=True):
         import torch
         self.part = part
-        self.send = {s: torch.as_tensor(v, device=device) for s, v in sorted(part.send.items())}
-        self.recv = {s: torch.as_tensor(v, device=device) for s, v in sorted(part.recv.items())}
+        src_s, src_r = (part.send, part.recv) if deep else (part.send1, part.recv1)
+        self.send = {s: torch.as_tensor(v, device=device) for s, v in sorted(src_s.items())}
+        self.recv = {s: torch.as_tensor(v, device=device) for s, v in sorted(src_r.items())}
 
 
 def _pack(fields, nt, idx, buf):
@@ -158,35 +185,37 @@ def _unpack(fields, nt, idx, buf):
 
 
 class DistHalo:
-    """One rank of a torch.distributed job (NCCL on GPUs, gloo on CPU for the host-side tests)."""
+    """One rank of a torch.distributed job (NCCL on GPUs, gloo on CPU for the host-side tests).
+    `deep` messages fill every ghost ring (2D sub-cycle state and forcing), the others ring 1."""
 
     def __init__(self, part: Part, nt_local: int, device):
         import torch.distributed as dist
-        self.maps = _Maps(part, device)
+        self.maps = {True: _Maps(part, device, True), False: _Maps(part, device, False)}
         self.nt = nt_local
         self.device = device
         self.exchanges = 0
         # gloo cannot send CUDA tensors: stage the packed messages through host memory (lets the
         # multi-process path run -- and be tested -- with several ranks sharing one GPU)
         self.host_staging = dist.is_initialized() and dist.get_backend() == "gloo" and device.type == "cuda"
-        self._plans = {}   # planes per column -> (send buffers, recv buffers, P2P ops), reused every step
+        self._plans = {}   # (planes per column, deep) -> (buffers, P2P ops), reused every step
 
-    def exchange(self, fields):
-        self.start(fields)
-        self.finish(fields)
+    def exchange(self, fields, deep=False):
+        self.start(fields, deep)
+        self.finish(fields, deep)
 
-    def _plan(self, tot):
+    def _plan(self, tot, deep):
         """Message buffers and the P2P op list for `tot` planes per column, allocated once: an
         exchange is always finished before the next one starts, so reuse is stream-ordered."""
         import torch
         import torch.distributed as dist
-        plan = self._plans.get(tot)
+        plan = self._plans.get((tot, deep))
         if plan is None:
+            mp = self.maps[deep]
             sends = {p: torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
-                     for p, idx in self.maps.send.items()}
+                     for p, idx in mp.send.items()}
             recvs = {p: torch.empty(tot * idx.numel(), dtype=torch.float64,
                                     device="cpu" if self.host_staging else self.device)
-                     for p, idx in self.maps.recv.items()}
+                     for p, idx in mp.recv.items()}
             hsend = {p: torch.empty(b.numel(), dtype=torch.float64, pin_memory=True) for p, b in sends.items()} \
                 if self.host_staging else sends
             ops = []
@@ -195,28 +224,28 @@ class DistHalo:
                     ops.append(dist.P2POp(dist.isend, hsend[peer], peer))
                 if peer in recvs:
                     ops.append(dist.P2POp(dist.irecv, recvs[peer], peer))
-            plan = self._plans[tot] = (sends, hsend, recvs, ops)
+            plan = self._plans[(tot, deep)] = (sends, hsend, recvs, ops)
         return plan
 
-    def start(self, fields):
+    def start(self, fields, deep=True):
         """Pack the owned boundary values and post the sends / receives (asynchronous: with NCCL the
         transfer runs on its own stream while the caller launches interior work)."""
         import torch.distributed as dist
         tot = sum(f.numel() // self.nt for f in fields)
-        sends, hsend, recvs, ops = self._plan(tot)
-        for peer, idx in self.maps.send.items():
+        sends, hsend, recvs, ops = self._plan(tot, deep)
+        for peer, idx in self.maps[deep].send.items():
             _pack(fields, self.nt, idx, sends[peer])
             if self.host_staging:
                 hsend[peer].copy_(sends[peer])
         works = dist.batch_isend_irecv(ops) if ops else []
-        self._pending = (recvs, works)
+        self._pending = (recvs, works, deep)
 
-    def finish(self, fields):
+    def finish(self, fields, deep=True):
         """Wait for the posted transfers (a stream dependency with NCCL) and fill the ghost slots."""
-        recvs, works = self._pending
+        recvs, works, deep = self._pending
         for w in works:
             w.wait()
-        for peer, idx in self.maps.recv.items():
+        for peer, idx in self.maps[deep].recv.items():
             buf = recvs[peer].to(self.device) if self.host_staging else recvs[peer]
             _unpack(fields, self.nt, idx, buf)
         self._pending = None
@@ -227,21 +256,22 @@ class VirtualGroup:
     """P ranks in one process on one device: halo messages are device-to-device copies."""
 
     def __init__(self, parts, nts, device):
-        self.maps = [_Maps(p, device) for p in parts]
+        self.maps = {d: [_Maps(p, device, d) for p in parts] for d in (True, False)}
         self.nts = nts
         self.device = device
         self.exchanges = 0
 
-    def exchange_all(self, fields_per_rank):
+    def exchange_all(self, fields_per_rank, deep=False):
         import torch
         msgs = {}
-        for r, (mp, fields) in enumerate(zip(self.maps, fields_per_rank)):
+        maps = self.maps[deep]
+        for r, (mp, fields) in enumerate(zip(maps, fields_per_rank)):
             tot = sum(f.numel() // self.nts[r] for f in fields)
             for peer, idx in mp.send.items():
                 buf = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
                 _pack(fields, self.nts[r], idx, buf)
                 msgs[(r, peer)] = buf
-        for r, (mp, fields) in enumerate(zip(self.maps, fields_per_rank)):
+        for r, (mp, fields) in enumerate(zip(maps, fields_per_rank)):
             for peer, idx in mp.recv.items():
                 _unpack(fields, self.nts[r], idx, msgs[(peer, r)])
         self.exchanges += 1
@@ -258,7 +288,7 @@ class PartitionedRun:
         import torch
         from .stepper import ImexStepper
         self.mesh, self.L, self.P = mesh, L, P
-        self.parts = decompose(mesh, P, np.full(mesh.nt, L))
+        self.parts = decompose(mesh, P, np.full(mesh.nt, L), depth=GHOST_DEPTH)
         self.local = [local_mesh(mesh, p) for p in self.parts]
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         ranks = range(P) if transport == "virtual" else [rank]
@@ -315,8 +345,9 @@ class PartitionedRun:
                         break
                     if len(phases) != 1:
                         raise MapMismatch(f"ranks at different exchange phases {phases}")
-                    if phases != {"start"}:       # one device: the copies happen at "finish"
-                        self.group.exchange_all(fields)
+                    ph = phases.pop()
+                    if ph != "start":             # one device: the copies happen at "finish"
+                        self.group.exchange_all(fields, deep=ph in ("finish", "deep"))
             else:
                 for st in self.st.values():
                     st._launch_step(st.t)

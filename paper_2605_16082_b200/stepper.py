@@ -68,12 +68,21 @@ class ImexStepper:
         self.qsum, self.htot, self.f3d2d = z(2, 3, nt), z(3, nt), z(2, 3, nt)
         self.qbar, self.f2d, self.mis = z(2, 3, nt), z(2, 3, nt), z(2, 3, nt)
         self.W12 = (z(3, 3, nt), z(3, 3, nt)) if part is not None else None   # RK stage states (partitioned)
-        self.cols2d = None     # (boundary, interior) owned columns of a partition, device int32
+        # partitions (>= 3 ghost rings): the RK stages of a substep run on owned + rings 1-2, owned +
+        # ring 1 and owned columns, so the 2D state is exchanged once per substep; the last stage
+        # updates the columns other ranks receive first and the rest while the exchange is in flight
+        self.cols2d = None
         if part is not None:
-            nb = np.asarray(mesh.nbr)[:part.n_own]
-            nxt = (nb >= part.n_own).any(axis=1)          # reads a ghost column
-            self.cols2d = tuple(torch.as_tensor(np.flatnonzero(sel).astype(np.int32), device=self.dev)
-                                for sel in (nxt, ~nxt))
+            if part.ring is None or part.ring.size and part.ring.max() < 3:
+                raise ValueError("partitioned stepping needs 3 ghost rings (partition.decompose depth=3)")
+            n_own = part.n_own
+            ring = np.concatenate([np.zeros(n_own, np.int32), part.ring])
+            sent = np.zeros(n_own, bool)
+            for idx in part.send.values():
+                sent[idx] = True
+            sets = (np.flatnonzero(ring <= 2), np.flatnonzero(ring <= 1), np.flatnonzero(sent),
+                    np.flatnonzero(~sent))
+            self.cols2d = tuple(torch.as_tensor(x.astype(np.int32), device=self.dev) for x in sets)
         self.cur = 0
         self.t = 0.0
         self.graphs = {}
@@ -136,6 +145,8 @@ class ImexStepper:
             yield ("all", [self.q])
         tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
+        if part:
+            yield ("deep", [self.f3d2d])   # the ring columns' RK stages need their forcing
         Sw.copy_(self.S)
         dt2 = dt_s / m_s
         if not part:
@@ -144,16 +155,17 @@ class ImexStepper:
         else:
             tm("sub_begin", lb.pdg_ext2d_subcycle_begin, h, ptr(Sw), p.g, dt2, 1, ptr(self.qbar), s)
             W1, W2 = self.W12
-            bnd, intr = self.cols2d
+            c012, c01, bnd, intr = self.cols2d
             for _ in range(m_s):
-                for k, (X, Y) in enumerate(((Sw, W1), (W1, W2), (W2, Sw))):
-                    # columns next to ghosts first; their values travel while the interior updates
+                for k, (X, Y, cols) in enumerate(((Sw, W1, c012), (W1, W2, c01))):
                     tm(f"rk{k}", lb.pdg_ext2d_rk_stage_cols, h, k, ptr(X), ptr(Sw), ptr(Y), dt2, p.g, p.rho0,
-                       ptr(self.f3d2d), ptr(self.qbar), ptr(bnd), bnd.numel(), s)
-                    yield ("start", [Y])
-                    tm(f"rk{k}", lb.pdg_ext2d_rk_stage_cols, h, k, ptr(X), ptr(Sw), ptr(Y), dt2, p.g, p.rho0,
-                       ptr(self.f3d2d), ptr(self.qbar), ptr(intr), intr.numel(), s)
-                    yield ("finish", [Y])
+                       ptr(self.f3d2d), ptr(self.qbar), ptr(cols), cols.numel(), s)
+                tm("rk2", lb.pdg_ext2d_rk_stage_cols, h, 2, ptr(W2), ptr(Sw), ptr(Sw), dt2, p.g, p.rho0,
+                   ptr(self.f3d2d), ptr(self.qbar), ptr(bnd), bnd.numel(), s)
+                yield ("start", [Sw])
+                tm("rk2", lb.pdg_ext2d_rk_stage_cols, h, 2, ptr(W2), ptr(Sw), ptr(Sw), dt2, p.g, p.rho0,
+                   ptr(self.f3d2d), ptr(self.qbar), ptr(intr), intr.numel(), s)
+                yield ("finish", [Sw])
             tm("sub_end", lb.pdg_ext2d_subcycle_end, h, ptr(Sw), ptr(self.f3d2d), m_s, dt2, ptr(self.qbar),
                ptr(self.f2d), s)
         eta1 = Sw[0]
@@ -199,12 +211,12 @@ class ImexStepper:
 
     def _launch_step(self, t0):
         for phase, fields in self._step_gen(t0):
-            if phase == "all":
-                self.halo.exchange(fields)
+            if phase in ("all", "deep"):
+                self.halo.exchange(fields, deep=phase == "deep")
             elif phase == "start":
-                self.halo.start(fields)
+                self.halo.start(fields, True)
             else:
-                self.halo.finish(fields)
+                self.halo.finish(fields, True)
 
     def _advance(self):
         self.cur = (self.cur + 2) % 3

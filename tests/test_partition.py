@@ -30,6 +30,26 @@ def test_maps_bit_exact_vs_oracle(nx, ny, P):
         assert {k: v.tolist() for k, v in p.send.items()} == send[r]
 
 
+@pytest.mark.parametrize("nx,ny,P", [(8, 6, 3), (32, 32, 4), (16, 9, 7), (5, 5, 8)])
+def test_deep_ring_maps_bit_exact_vs_oracle(nx, ny, P):
+    """3 ghost rings (the partitioned stepper's 2D sub-cycle): rings, all-ring and ring-1 maps."""
+    m = basin(nx, ny)
+    parts = PP.decompose(m, P, depth=3)
+    bounds, ghosts, rings, send, recv, send1, recv1 = OP.deep_maps(m.nbr.tolist(), [1] * m.nt, P, 3)
+    assert [p.lo for p in parts] + [parts[-1].hi] == bounds
+    for r, p in enumerate(parts):
+        assert p.ghosts.tolist() == ghosts[r]
+        assert p.ring.tolist() == rings[r]
+        assert {k: v.tolist() for k, v in p.recv.items()} == recv[r]
+        assert {k: v.tolist() for k, v in p.send.items()} == send[r]
+        assert {k: v.tolist() for k, v in p.recv1.items()} == recv1[r]
+        assert {k: v.tolist() for k, v in p.send1.items()} == send1[r]
+    one = PP.decompose(m, P)                        # ring 1 of the deep partition == the one-ring one
+    for p, q in zip(parts, one):
+        gl = p.ghosts[p.ring == 1]
+        assert gl.tolist() == q.ghosts.tolist()
+
+
 def test_partition_properties():
     m = basin(32, 32)
     parts = PP.decompose(m, 4)

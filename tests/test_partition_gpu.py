@@ -29,4 +29,4 @@ def test_partition_invariance_bitwise(pdg, P):
     s = run.get_state()
     for k in ("eta", "qx", "qy", "ux", "uy", "T"):
         assert np.array_equal(s[k], g[k]), (P, k, float(np.abs(s[k] - g[k]).max()))
-    assert run.group.exchanges == 3 * (2 * 3 + 3 * (c.m // 2 + c.m))   # q, mis, u/T per stage + 2D per RK stage
+    assert run.group.exchanges == 3 * (2 * 4 + (c.m // 2 + c.m))   # q, F3D->2D, mis, u/T per stage + 2D per substep
