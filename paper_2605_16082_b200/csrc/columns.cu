@@ -1222,7 +1222,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
     const double* gt = Gs + (size_t)l * 18 * nt + c;
     double E[18];
 #pragma unroll
-    for (int e = 0; e < 18; ++e) E[e] = gt[(size_t)e * nt];
+    for (int e = 0; e < 18; ++e) E[e] = __ldg(gt + (size_t)e * nt);
     double gl[6][NC];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
@@ -1230,7 +1230,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
       for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c];
     double wtn[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+    for (int k = 0; k < 3; ++k) wtn[k] = __ldg(a.wt + ((size_t)k * L + l + 1) * nt + c);
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     VG Vl;
     vgeo<true>(C, eta, ft, fb, Vl);

@@ -72,8 +72,8 @@ __global__ void k_project(DMesh m, const double* __restrict__ eta_g, const doubl
     layer_jz(b, eta, ft, fb, jz);
     hq(jz, jzq);
     double u[2][6];
-    ld6(ux, l, c, L, nt, u[0]);
-    ld6(uy, l, c, L, nt, u[1]);
+    ld6g(ux, l, c, L, nt, u[0]);
+    ld6g(uy, l, c, L, nt, u[1]);
     double out[2][6];
     if (MASS_GIVEN) {
       double a[6][6], rhs[6][2];
