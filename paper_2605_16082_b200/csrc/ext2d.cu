@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const
 #pragma unroll
   for (int f = 0; f < 3; ++f)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) s0[f][k] = STAGE == 0 ? 0.0 : S0[(size_t)(f * 3 + k) * nt + c];
+    for (int k = 0; k < 3; ++k)
+      s0[f][k] = STAGE == 0 ? 0.0 : STAGE == 1 ? __ldg(S0 + (size_t)(f * 3 + k) * nt + c) : S0[(size_t)(f * 3 + k) * nt + c];
   if (STAGE == 2) {
 #pragma unroll
     for (int f = 0; f < 2; ++f)
