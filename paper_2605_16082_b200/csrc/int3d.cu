@@ -1090,9 +1090,9 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
     const double jm = 0.5 * (fb - ft);
     double u[NC][6], qv[2][6];
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) ld6(a.uc[cc], l, c, L, nt, u[cc]);
-    ld6(a.qa, l, c, L, nt, qv[0]);
-    ld6(a.qa + P6, l, c, L, nt, qv[1]);
+    for (int cc = 0; cc < NC; ++cc) ld6g(a.uc[cc], l, c, L, nt, u[cc]);
+    ld6g(a.qa, l, c, L, nt, qv[0]);
+    ld6g(a.qa + P6, l, c, L, nt, qv[1]);
     if (MODE == 2) {
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
@@ -1138,8 +1138,8 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
         ld_fac(a.fac, k, l, c, L, nt, f);
       } else {
         double qn[2][4];
-        ld_nb4(a.qa, E[k].k2, E[k].e2, l, L, nt, qn[0]);
-        ld_nb4(a.qa + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
+        ld_nb4g(a.qa, E[k].k2, E[k].e2, l, L, nt, qn[0]);
+        ld_nb4g(a.qa + P6, E[k].k2, E[k].e2, l, L, nt, qn[1]);
         if (MODE == 2) {
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
@@ -1155,7 +1155,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double n4[4], ti[2][2], te[2][2], x[2][2];
-        ld_nb4(a.uc[cc], E[k].k2, E[k].e2, l, L, nt, n4);
+        ld_nb4g(a.uc[cc], E[k].k2, E[k].e2, l, L, nt, n4);
         tr_own(u[cc], k, ti);
         tr_nb(n4, te);
 #pragma unroll
@@ -1171,8 +1171,8 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
     if constexpr (NC >= 2) {
       if (MODE != 0 || a.mass_terms) {
         double rr[2][6];
-        ld6(a.r, l, c, L, nt, rr[0]);
-        ld6(a.r + P6, l, c, L, nt, rr[1]);
+        ld6g(a.r, l, c, L, nt, rr[0]);
+        ld6g(a.r + P6, l, c, L, nt, rr[1]);
         if (MODE == 0) {
           double M[6][6];
 #pragma unroll
@@ -1269,7 +1269,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double x0[6], m0x[6], o[6];
-        ld6(a.u0c[cc], l, c, L, nt, x0);
+        ld6g(a.u0c[cc], l, c, L, nt, x0);
         kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
