@@ -218,6 +218,14 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
                       double dt, const double* rhs, const double* xin, double* x, void* stream);
 
 /* explicit vertical stage of momentum (ncomp 2) and tracer in one pass */
+/* diagnostics_2d (external2d.py:366-380) and budget_3d (internal3d.py:942-951) of the resident state
+ * in one fused pass: S [3][3][nt] (eta, qx, qy), u [2][6][L][nt], T [6][L][nt]; out (device, 10
+ * doubles): 2D volume, 2D energy, eta min, eta max, 3D volume, momentum x, momentum y, tracer
+ * mass, T min, T max.  work: device scratch of pdg_diagnostics_work_doubles(ctx) doubles.
+ * Deterministic (fixed reduction order). */
+int pdg_step_diagnostics(pdg_ctx* ctx, const double* S, const double* u, const double* T, double g, double* work,
+                         double* out, void* stream);
+int pdg_diagnostics_work_doubles(pdg_ctx* ctx);
 int pdg_step_vertical_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, double dt_mesh,
                          const double* wt, double kh_u, double kv_u, double kh_T, double kv_T, double n0, int order,
                          double dt, const double* rhs_u, const double* xin_u, double* x_u, const double* rhs_T,

@@ -204,3 +204,13 @@ def diagnostics(st, mesh, p):
             "total_volume": float(mh_apply(st.eta - mesh.b, mesh.j2d).sum()),
             "total_energy": float((mesh.j2d[:, None] * dens * QW).sum()),
             "eta_min": float(st.eta.min()), "eta_max": float(st.eta.max())}
+
+
+def diagnostics_2d(eta, qx, qy, mesh, g):
+    """external2d.py:366-380: total volume (exact P1 integral of eta - b), quadrature energy, eta range."""
+    h_q = (eta - mesh.b) @ BARY.T
+    eta_q, qx_q, qy_q = eta @ BARY.T, qx @ BARY.T, qy @ BARY.T
+    dens = 0.5 * g * eta_q ** 2 + 0.5 * (qx_q ** 2 + qy_q ** 2) / h_q
+    return {"total_volume": float(mh_apply(eta - mesh.b, mesh.j2d).sum()),
+            "total_energy": float((mesh.j2d[:, None] * dens * QW[None, :]).sum()),
+            "eta_min": float(eta.min()), "eta_max": float(eta.max())}

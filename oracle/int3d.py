@@ -427,3 +427,10 @@ def scatter_columns(x, grid, els=None):
     out = np.zeros(shape)
     out.reshape((grid.mesh.nt, grid.n_layers) + shape[1:])[cols] = x
     return out
+
+
+def budget_3d(grid, mass, ux, uy, tr):
+    """internal3d.py:942-951: integrals of 1, u_x, u_y, T against the prism masses; T range."""
+    integ = lambda f: float(mass_apply(mass, f).sum())  # noqa: E731
+    return {"volume": integ(np.ones((mass.shape[0], 6))), "momentum_x": integ(ux), "momentum_y": integ(uy),
+            "tracer_mass": integ(tr), "tracer_min": float(np.min(tr)), "tracer_max": float(np.max(tr))}

@@ -259,6 +259,22 @@ class ImexStepper:
         self.graphs[self.cur] = g
         return g
 
+    def diagnostics(self) -> dict:
+        """diagnostics_2d (external2d.py:366-380) + budget_3d (internal3d.py:942-951) of the resident
+        state on the current grid, reduced on the device in one fused pass (one 80-byte read-back)."""
+        lb = _lib.lib()
+        with torch.cuda.device(self.dev):
+            if getattr(self, "_diag_work", None) is None:
+                self._diag_work = torch.empty(lb.pdg_diagnostics_work_doubles(self.dm.h), dtype=F64, device=self.dev)
+                self._diag_out = torch.empty(10, dtype=F64, device=self.dev)
+            self._c("diagnostics", lb.pdg_step_diagnostics(self.dm.h, ptr(self.S), ptr(self.U[self.cur]),
+                                                           ptr(self.T[self.cur]), self.p.g, ptr(self._diag_work),
+                                                           ptr(self._diag_out), stream_ptr()))
+            v = self._diag_out.cpu().tolist()
+        return {"t": self.t, "total_volume": v[0], "total_energy": v[1], "eta_min": v[2], "eta_max": v[3],
+                "volume": v[4], "momentum_x": v[5], "momentum_y": v[6], "tracer_mass": v[7], "tracer_min": v[8],
+                "tracer_max": v[9]}
+
     def check(self):
         """Synchronise and raise the first device-side error (DryColumn, ZeroPivot, CflViolation ...)."""
         self.dm.raise_errors("imex step")

@@ -108,3 +108,19 @@ def test_step(mesh, golden):
         s = stepper.imex_step(s, p, float(g["dt"]), int(g["m"]), float(g["kv"]), float(g["nu_v"]))
         for n, a in [("ux", s.ux), ("uy", s.uy), ("T", s.T), ("eta", s.s2d.eta), ("qx", s.s2d.qx), ("qy", s.s2d.qy)]:
             same(a, g[f"s{i}_{n}"])
+
+
+def test_diagnostics(golden):
+    """diagnostics_2d / budget_3d restatements vs the reference (scripts/make_golden_diag.py)."""
+    g = golden("diag")
+    lx, ly = float(g["lx"]), float(g["ly"])
+
+    def bed(x, y):
+        return -20.0 + 5.0 * np.sin(np.pi * x / lx) * np.cos(2.0 * np.pi * y / ly)
+    m = geom.hilbert_reorder(geom.basin_mesh(int(g["nx"]), int(g["ny"]), lx, ly, bed))
+    ref = dict(zip(g["keys"].tolist(), g["values"].tolist()))
+    d2 = ext2d.diagnostics_2d(g["eta"], g["qx"], g["qy"], m, float(g["g"]))
+    grid = geom.extrude(m, int(g["L"]), g["eta"])
+    b3 = int3d.budget_3d(grid, int3d.prism_mass(grid), g["ux"], g["uy"], g["T"])
+    for k, v in {**d2, **b3}.items():
+        assert abs(v - ref[k]) <= 1e-13 * max(abs(ref[k]), 1.0), (k, v, ref[k])

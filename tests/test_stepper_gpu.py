@@ -129,3 +129,22 @@ def test_100_steps_baroclinic_parity(pdg):
     o = _oracle_run(om, L, p, s0, 100, dt, msub, kv, nu_v)
     for k, ref in [("ux", o.ux), ("uy", o.uy), ("T", o.T), ("eta", o.s2d.eta), ("qx", o.s2d.qx), ("qy", o.s2d.qy)]:
         assert rel(g[k], ref) <= 1e-9, (k, rel(g[k], ref))
+
+
+def test_device_diagnostics_vs_reference(pdg, golden):
+    """ImexStepper.diagnostics(): diagnostics_2d + budget_3d of the resident state in one fused device
+    reduction, against the reference's values on the same state (tests/golden/diag.npz)."""
+    g = golden("diag")
+    lx, ly, L = float(g["lx"]), float(g["ly"]), int(g["L"])
+
+    def bed(x, y):
+        return -20.0 + 5.0 * np.sin(np.pi * x / lx) * np.cos(2.0 * np.pi * y / ly)
+    m = pdg.mesh.hilbert_reorder(pdg.mesh.generate_basin_mesh(int(g["nx"]), int(g["ny"]), lx, ly, bed))
+    st = pdg.stepper.ImexStepper(m, L, pdg.PhysParams(f=1e-4, alpha=0.2, t_ref=12.5), 40.0, 4, 1e-3, 1e-4)
+    st.set_state(g["eta"], g["qx"], g["qy"], g["ux"], g["uy"], g["T"])
+    d = st.diagnostics()
+    ref = dict(zip(g["keys"].tolist(), g["values"].tolist()))
+    for k, v in ref.items():
+        tol = 0.0 if k.endswith(("_min", "_max")) else 1e-12
+        assert abs(d[k] - v) <= tol * max(abs(v), 1.0), (k, d[k], v)
+    assert st.diagnostics() == d                      # deterministic reduction
