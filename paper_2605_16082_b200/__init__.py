@@ -12,6 +12,7 @@ from .params import BandedColumnMatrix, ExternalResult, LayerPolicy, PenaltyPara
 
 def __getattr__(name):
     import importlib
-    if name in ("mesh", "external2d", "internal3d", "columns", "stepper", "device", "scenarios", "partition"):
+    if name in ("mesh", "external2d", "internal3d", "columns", "stepper", "device", "scenarios", "partition",
+                "snapshot"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)
