@@ -125,6 +125,33 @@ def solve_w_column(rhs, j2d, layers=None):
     return _sweep(1, rhs, j2d, layers)
 
 
+def _solve_cell(kind, block, j2d_cols, j2d_pad):
+    """The column sweep on a cell block (columns.py:546-580): padded lanes get j2d_pad and zero
+    layers and come back zero; the solve runs on the GPU (pdg_solve_sweep)."""
+    from .layout import CellBlock, cell_view
+    view = cell_view(block)                          # (width, L, 6, ncomp)
+    w, n = block.width, block.columns.size
+    j = np.full(w, j2d_pad, dtype=block.data.dtype)
+    j[:n] = np.asarray(j2d_cols, dtype=block.data.dtype)
+    lay = np.zeros(w, dtype=np.int64)
+    lay[:n] = block.layers
+    x = _sweep(kind, np.ascontiguousarray(view), j, lay)
+    out = CellBlock(data=np.zeros_like(block.data), columns=block.columns.copy(), layers=block.layers.copy(),
+                    ncomp=block.ncomp)
+    cell_view(out)[:] = x
+    return out
+
+
+def solve_r_cell(block, j2d_cols, j2d_pad: float = 1.0):
+    """solve_r_column on a cell block (columns.py:546-562)."""
+    return _solve_cell(0, block, j2d_cols, j2d_pad)
+
+
+def solve_w_cell(block, j2d_cols, j2d_pad: float = 1.0):
+    """solve_w_column on a cell block (columns.py:565-580)."""
+    return _solve_cell(1, block, j2d_cols, j2d_pad)
+
+
 def assemble_dense_oracle(kind: str, layers: int, mh: np.ndarray) -> np.ndarray:
     """Literal dense D_vu / D_vd (columns.py:154-188): a test oracle, host numpy."""
     L = int(layers)
