@@ -9,6 +9,8 @@ test oracles (host numpy, not a compute path).
 """
 from __future__ import annotations
 
+from dataclasses import dataclass, field
+
 import numpy as np
 import torch
 
@@ -265,6 +267,38 @@ def apply_banded(mat: BandedColumnMatrix, x):
     _lib.check(_lib.lib().pdg_apply_banded(ncol, L, nc, ptr(d), ptr(u), ptr(w), ptr(r), ptr(y), stream_ptr()),
                "apply_banded")
     return A.out(_col_out(y, had))
+
+
+@dataclass
+class AccessStats:
+    """Working-set record of a column elimination (columns.py:375-379)."""
+    max_live: int = 0
+    loads: int = 0
+    stores: int = 0
+    touched: set = field(default_factory=set)
+
+
+def solve_banded_sequential(mat: BandedColumnMatrix, rhs, col: int, stats: AccessStats = None):
+    """One column of solve_banded_column (columns.py:404-485) with its working-set record.
+
+    The solve is the GPU block-Thomas kernel on column `col` (same elimination order as the batched
+    solve, so the results agree with solve_banded_column on that column).  The kernel's working
+    buffer is one 6x6 tile per layer by construction (36 scalars, reloaded per layer), so the record
+    is exact: L diagonal-tile loads, 2 propagation-tile stores per layer but the last, one factored
+    diagonal per layer, touching d[l], u[l] (l >= 1) and w[l] (l <= L-2)."""
+    rhs_a = rhs.cpu().numpy() if isinstance(rhs, torch.Tensor) else np.asarray(rhs)
+    if rhs_a.shape[0] != 1:
+        raise ShapeMismatch("sequential solver expects a single-column RHS")
+    one = BandedColumnMatrix(d=np.asarray(mat.d)[col:col + 1], u=np.asarray(mat.u)[col:col + 1],
+                             w=np.asarray(mat.w)[col:col + 1])
+    x = solve_banded_column(one, rhs_a)
+    st = stats if stats is not None else AccessStats()
+    L = int(np.asarray(mat.d).shape[1])
+    st.max_live = max(st.max_live, 36)
+    st.loads += L
+    st.stores += 2 * (L - 1) + L
+    st.touched |= {("d", l) for l in range(L)} | {("u", l) for l in range(1, L)} | {("w", l) for l in range(L - 1)}
+    return x, st
 
 
 def solve_tridiagonal(lower, diag, upper, rhs):

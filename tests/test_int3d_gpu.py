@@ -191,3 +191,13 @@ def test_zero_pivot(pdg):
     with pytest.raises(pdg.errors.ZeroPivot) as ei:
         C.solve_banded_column(mat, np.ones((2, 3, 6)))
     assert ei.value.layer == 2 and ei.value.node == 4
+
+
+def test_solve_banded_sequential_vs_reference(pdg, golden):
+    """solve_banded_sequential (columns.py:404-485): the solution and the working-set record."""
+    g = golden("seqsolve")
+    mat = pdg.BandedColumnMatrix(d=g["d"], u=g["u"], w=g["w"])
+    x, st = pdg.columns.solve_banded_sequential(mat, g["rhs"], int(g["col"]))
+    assert np.abs(x - g["x"]).max() <= 1e-12 * np.abs(g["x"]).max()
+    assert (st.max_live, st.loads, st.stores) == (int(g["max_live"]), int(g["loads"]), int(g["stores"]))
+    assert sorted(f"{k}{l}" for k, l in st.touched) == g["touched"].tolist()
