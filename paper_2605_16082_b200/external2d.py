@@ -19,8 +19,60 @@ from . import _lib
 from .device import Arr, c3_in, c3_out, device_mesh, els_dev, ptr, require_cuda, stream_ptr
 from .params import ExternalResult, PhysParams, State2D
 
-__all__ = ["PhysParams", "State2D", "ExternalResult", "eos_density", "rhs_free_surface", "rhs_depth_momentum",
-           "external_tendencies", "check_cfl", "subcycle_external", "integrate_nodal", "diagnostics_2d"]
+__all__ = ["PhysParams", "State2D", "ExternalResult", "eos_density", "trace_int", "trace_ext", "edge_celerity",
+           "rhs_free_surface", "rhs_depth_momentum", "external_tendencies", "check_cfl", "subcycle_external",
+           "integrate_nodal", "diagnostics_2d"]
+
+# edge-point shapes in the edge's own traversal order (dg.py:76-81): ES[h][s]
+_GZ = 1.0 / math.sqrt(3.0)
+_ES = ((0.5 * (1.0 + _GZ), 0.5 * (1.0 - _GZ)), (0.5 * (1.0 - _GZ), 0.5 * (1.0 + _GZ)))
+_EV0, _EV1 = (0, 1, 2), (1, 2, 0)
+
+
+def _cuda():
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _idx(a, device):
+    return torch.as_tensor(np.asarray(a.cpu() if isinstance(a, torch.Tensor) else a, dtype=np.int64), device=device)
+
+
+def trace_int(field2d, els, k):
+    """Interior trace of a (nt, 3) nodal field on local edge k at the 2 Gauss points: (nel, 2)
+    (external2d.py:95-99)."""
+    A = Arr()
+    f = A.dev(field2d, _cuda())
+    r = _idx(els, f.device)
+    n0, n1 = f[r, _EV0[k]], f[r, _EV1[k]]
+    return A.out(torch.stack([n0 * _ES[q][0] + n1 * _ES[q][1] for q in range(2)], dim=-1))
+
+
+def trace_ext(field2d, nbr_e, nbr_k):
+    """Exterior trace at the same physical points, mirrored point order (external2d.py:102-107)."""
+    A = Arr()
+    f = A.dev(field2d, _cuda())
+    e = _idx(nbr_e, f.device).clamp_min(0)
+    kk = _idx(nbr_k, f.device)
+    ev0 = torch.as_tensor(_EV0, device=f.device)[kk]
+    ev1 = torch.as_tensor(_EV1, device=f.device)[kk]
+    m0, m1 = f[e, ev0], f[e, ev1]
+    t = torch.stack([m0 * _ES[q][1] + m1 * _ES[q][0] for q in range(2)], dim=-1)
+    return A.out(t)
+
+
+def edge_celerity(eta_i, eta_e, b_i, b_e, g):
+    """max over both sides of sqrt(g H) per point; DryColumn(-1, min H) if either side is dry
+    (external2d.py:110-116)."""
+    A = Arr()
+    dev = _cuda()
+    hi = A.dev(eta_i, dev) - A.dev(b_i, dev)
+    he = A.dev(eta_e, dev) - A.dev(b_e, dev)
+    lo = float(torch.minimum(hi.min(), he.min()).item()) if hi.numel() else 1.0
+    if lo <= 0.0:
+        from .errors import DryColumn
+        raise DryColumn(-1, lo)
+    return A.out(torch.maximum(torch.sqrt(g * hi), torch.sqrt(g * he)))
 
 
 def eos_density(T, params: PhysParams, S=None):

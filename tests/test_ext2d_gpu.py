@@ -135,3 +135,19 @@ def test_torch_inputs_zero_copy(pdg):
     assert isinstance(d[0], torch.Tensor) and d[0].is_cuda
     o = O.tendencies(st, m, p)
     assert rel(d[0].cpu().numpy(), o[0]) <= TOL_RHS
+
+
+def test_trace_helpers_vs_reference(pdg, golden):
+    """trace_int / trace_ext / edge_celerity (external2d.py:95-116) against the reference."""
+    g = golden("traces")
+    eta, b = g["eta"], g["b"]
+    els = np.arange(eta.shape[0])
+    for k in range(3):
+        ti = pdg.external2d.trace_int(eta, els, k)
+        te = pdg.external2d.trace_ext(eta, g[f"nbr{k}"], g[f"nbrk{k}"])
+        assert np.array_equal(ti, g[f"ti{k}"]) and np.array_equal(te, g[f"te{k}"])
+        bi = pdg.external2d.trace_int(b, els, k)
+        be = pdg.external2d.trace_ext(b, g[f"nbr{k}"], g[f"nbrk{k}"])
+        assert np.array_equal(pdg.external2d.edge_celerity(ti, te, bi, be, 9.81), g[f"cel{k}"])
+    with pytest.raises(pdg.errors.DryColumn):
+        pdg.external2d.edge_celerity(np.array([-30.0]), np.array([0.0]), np.array([-20.0]), np.array([-20.0]), 9.81)
