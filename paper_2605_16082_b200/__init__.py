@@ -13,6 +13,6 @@ from .params import BandedColumnMatrix, ExternalResult, LayerPolicy, PenaltyPara
 def __getattr__(name):
     import importlib
     if name in ("mesh", "external2d", "internal3d", "columns", "stepper", "device", "scenarios", "partition",
-                "snapshot", "layout"):
+                "snapshot", "layout", "dg"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)
