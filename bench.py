@@ -321,13 +321,10 @@ def main():
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(ke):
-            dv = {k: (v.to("cuda", non_blocking=True) if isinstance(v, torch.Tensor) else v) for k, v in pin.items()}
-            st.set_state(dv["eta"], dv["qx"], dv["qy"], dv["ux"], dv["uy"], dv["T"], dv["t"])
+            # public API with host (pinned) buffers: upload, step, download into the same buffers
+            st.set_state(pin["eta"], pin["qx"], pin["qy"], pin["ux"], pin["uy"], pin["T"], pin["t"])
             stepper.step(1)
-            out = st.get_state(numpy=False)
-            for k, v in out.items():
-                if isinstance(v, torch.Tensor):
-                    pin[k].copy_(v, non_blocking=True)
+            st.get_state(numpy=False, out=pin)
         f1.record()
         torch.cuda.synchronize()
         te = f0.elapsed_time(f1) / ke

@@ -106,27 +106,67 @@ class ImexStepper:
         self.prof.setdefault(name, []).append((e0, e1))
 
     # ------------------------------------------------------------------ state I/O (reference layouts)
-    def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
-        nt, L, dev = self.nt, self.L, self.dev
-
-        def d(a):
-            return (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
-        self.S[0].copy_(c3_in(d(eta), dev))
-        self.S[1].copy_(c3_in(d(qx), dev))
-        self.S[2].copy_(c3_in(d(qy), dev))
-        self.U[self.cur][0].copy_(p6_in(d(ux), nt, L))
-        self.U[self.cur][1].copy_(p6_in(d(uy), nt, L))
-        self.T[self.cur].copy_(p6_in(d(T), nt, L))
-        self.t = float(t)
-
-    def get_state(self, numpy=True):
+    def _dests(self):
         nt, L = self.nt, self.L
         u = self.U[self.cur]
-        out = dict(eta=c3_out(self.S[0]), qx=c3_out(self.S[1]), qy=c3_out(self.S[2]), ux=p6_out(u[0], nt, L),
+        # destination planes and the (reference layout) -> device layout view of a source
+        return [("eta", self.S[0], lambda a: a.t()), ("qx", self.S[1], lambda a: a.t()),
+                ("qy", self.S[2], lambda a: a.t()),
+                ("ux", u[0], lambda a: a.reshape(nt, L, 6).permute(2, 1, 0)),
+                ("uy", u[1], lambda a: a.reshape(nt, L, 6).permute(2, 1, 0)),
+                ("T", self.T[self.cur], lambda a: a.reshape(nt, L, 6).permute(2, 1, 0))]
+
+    def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
+        """Load a state in the reference layouts ((nt, 3) 2D fields, (P, 6) prism fields).
+
+        Host torch tensors (ideally pinned) are uploaded on a copy stream, field by field, while
+        the compute stream rearranges the previous field into the device layout."""
+        dev = self.dev
+        src = dict(eta=eta, qx=qx, qy=qy, ux=ux, uy=uy, T=T)
+        host = all(isinstance(a, torch.Tensor) and not a.is_cuda for a in src.values())
+        main = torch.cuda.current_stream(dev)
+        cs = self._copy_stream() if host else None
+        for name, dest, view in self._dests():
+            a = src[name]
+            if host:
+                cs.wait_stream(main)
+                with torch.cuda.stream(cs):
+                    buf = a.to(dev, F64, non_blocking=True)
+                main.wait_stream(cs)
+                buf.record_stream(main)
+            else:
+                buf = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
+            dest.copy_(view(buf))
+        self.t = float(t)
+
+    def get_state(self, numpy=True, out=None):
+        """The state in the reference layouts.  out: dict of host tensors (pinned) to fill -- the
+        device-to-host copies then run on a copy stream, overlapped with the next field's
+        rearrangement (asynchronous: synchronise before reading them)."""
+        nt, L = self.nt, self.L
+        u = self.U[self.cur]
+        if out is not None:
+            main = torch.cuda.current_stream(self.dev)
+            cs = self._copy_stream()
+            for name, dest, _ in self._dests():
+                tmp = c3_out(dest) if name in ("eta", "qx", "qy") else p6_out(dest, nt, L)
+                cs.wait_stream(main)
+                with torch.cuda.stream(cs):
+                    out[name].copy_(tmp, non_blocking=True)
+                tmp.record_stream(cs)
+            main.wait_stream(cs)
+            out["t"] = self.t
+            return out
+        res = dict(eta=c3_out(self.S[0]), qx=c3_out(self.S[1]), qy=c3_out(self.S[2]), ux=p6_out(u[0], nt, L),
                    uy=p6_out(u[1], nt, L), T=p6_out(self.T[self.cur], nt, L), t=self.t)
         if numpy:
-            out = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in out.items()}
-        return out
+            res = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
+        return res
+
+    def _copy_stream(self):
+        if getattr(self, "_cstream", None) is None:
+            self._cstream = torch.cuda.Stream(device=self.dev)
+        return self._cstream
 
     # ------------------------------------------------------------------ one stage
     def _stage(self, s, eta_u, u, T, u0, T0, Sw, out_u, out_T, dt_s, m_s, implicit, t_wind):

@@ -148,3 +148,24 @@ def test_device_diagnostics_vs_reference(pdg, golden):
         tol = 0.0 if k.endswith(("_min", "_max")) else 1e-12
         assert abs(d[k] - v) <= tol * max(abs(v), 1.0), (k, d[k], v)
     assert st.diagnostics() == d                      # deterministic reduction
+
+
+def test_host_pinned_state_io(pdg):
+    """set_state from pinned host tensors and get_state(out=pinned buffers) (the e2e path) agree
+    bitwise with the numpy path."""
+    import torch
+    L = 4
+    m, om, p, s0 = _setup(pdg, L=L)
+    st = pdg.stepper.ImexStepper(m, L, p, 40.0, 4, 1e-3, 1e-4)
+    st.set_state(**s0)
+    st.step(1)
+    ref = st.get_state()
+    pin = {k: torch.as_tensor(v).pin_memory() for k, v in s0.items()}
+    st2 = pdg.stepper.ImexStepper(m, L, p, 40.0, 4, 1e-3, 1e-4)
+    st2.set_state(pin["eta"], pin["qx"], pin["qy"], pin["ux"], pin["uy"], pin["T"])
+    st2.step(1)
+    out = {k: torch.empty_like(v).pin_memory() for k, v in pin.items()}
+    st2.get_state(numpy=False, out=out)
+    torch.cuda.synchronize()
+    for k in ("eta", "qx", "qy", "ux", "uy", "T"):
+        assert np.array_equal(out[k].numpy(), ref[k]), k
