@@ -325,6 +325,7 @@ def main():
             st.set_state(pin["eta"], pin["qx"], pin["qy"], pin["ux"], pin["uy"], pin["T"], pin["t"])
             stepper.step(1)
             st.get_state(numpy=False, out=pin)
+        st.wait_io()                      # the last step's download is inside the timed region
         f1.record()
         torch.cuda.synchronize()
         te = f0.elapsed_time(f1) / ke

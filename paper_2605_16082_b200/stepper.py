@@ -90,6 +90,7 @@ class ImexStepper:
         self.prof = None       # {name: [(start_event, end_event), ...]} when profiling
         self.fuse_rhs = True   # momentum + tracer stage right-hand sides in one kernel
         self.fuse_vexpl = False  # momentum + tracer explicit vertical in one kernel (slower: register spills)
+        self._pending_d2h = {}   # host buffer address -> event of the download filling it
 
     def _c(self, name, rc):
         _lib.check(rc, name)
@@ -119,20 +120,26 @@ class ImexStepper:
     def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
         """Load a state in the reference layouts ((nt, 3) 2D fields, (P, 6) prism fields).
 
-        Host torch tensors (ideally pinned) are uploaded on a copy stream, field by field, while
-        the compute stream rearranges the previous field into the device layout."""
+        Host torch tensors (ideally pinned) are uploaded field by field on an upload stream while
+        the compute stream rearranges the previous field into the device layout.  A host buffer
+        that a previous get_state(out=...) is still filling is uploaded as soon as THAT field has
+        arrived (per-buffer events), so downloads and uploads of different fields overlap on the
+        two PCIe directions."""
         dev = self.dev
         src = dict(eta=eta, qx=qx, qy=qy, ux=ux, uy=uy, T=T)
         host = all(isinstance(a, torch.Tensor) and not a.is_cuda for a in src.values())
         main = torch.cuda.current_stream(dev)
-        cs = self._copy_stream() if host else None
+        up = self._io_streams()[0] if host else None
         for name, dest, view in self._dests():
             a = src[name]
             if host:
-                cs.wait_stream(main)
-                with torch.cuda.stream(cs):
+                up.wait_stream(main)
+                ev = self._pending_d2h.pop(a.data_ptr(), None)
+                if ev is not None:
+                    up.wait_event(ev)
+                with torch.cuda.stream(up):
                     buf = a.to(dev, F64, non_blocking=True)
-                main.wait_stream(cs)
+                main.wait_stream(up)
                 buf.record_stream(main)
             else:
                 buf = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
@@ -140,21 +147,24 @@ class ImexStepper:
         self.t = float(t)
 
     def get_state(self, numpy=True, out=None):
-        """The state in the reference layouts.  out: dict of host tensors (pinned) to fill -- the
-        device-to-host copies then run on a copy stream, overlapped with the next field's
-        rearrangement (asynchronous: synchronise before reading them)."""
+        """The state in the reference layouts.  out: dict of host tensors (pinned) to fill: the
+        device-to-host copies run on a download stream, field by field, overlapped with the next
+        field's rearrangement (asynchronous: synchronise before reading them on the host; a later
+        set_state from the same buffers orders itself after each field's copy)."""
         nt, L = self.nt, self.L
         u = self.U[self.cur]
         if out is not None:
             main = torch.cuda.current_stream(self.dev)
-            cs = self._copy_stream()
+            down = self._io_streams()[1]
             for name, dest, _ in self._dests():
                 tmp = c3_out(dest) if name in ("eta", "qx", "qy") else p6_out(dest, nt, L)
-                cs.wait_stream(main)
-                with torch.cuda.stream(cs):
+                down.wait_stream(main)
+                with torch.cuda.stream(down):
                     out[name].copy_(tmp, non_blocking=True)
-                tmp.record_stream(cs)
-            main.wait_stream(cs)
+                    ev = torch.cuda.Event()
+                    ev.record(down)
+                tmp.record_stream(down)
+                self._pending_d2h[out[name].data_ptr()] = ev
             out["t"] = self.t
             return out
         res = dict(eta=c3_out(self.S[0]), qx=c3_out(self.S[1]), qy=c3_out(self.S[2]), ux=p6_out(u[0], nt, L),
@@ -163,10 +173,17 @@ class ImexStepper:
             res = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
         return res
 
-    def _copy_stream(self):
-        if getattr(self, "_cstream", None) is None:
-            self._cstream = torch.cuda.Stream(device=self.dev)
-        return self._cstream
+    def wait_io(self):
+        """Order the current stream after every pending get_state(out=...) download."""
+        if getattr(self, "_io", None) is not None:
+            torch.cuda.current_stream(self.dev).wait_stream(self._io[1])
+        self._pending_d2h.clear()
+
+    def _io_streams(self):
+        """(upload, download) streams: the two PCIe directions run concurrently."""
+        if getattr(self, "_io", None) is None:
+            self._io = (torch.cuda.Stream(device=self.dev), torch.cuda.Stream(device=self.dev))
+        return self._io
 
     # ------------------------------------------------------------------ one stage
     def _stage(self, s, eta_u, u, T, u0, T0, Sw, out_u, out_T, dt_s, m_s, implicit, t_wind):
