@@ -107,64 +107,86 @@ class ImexStepper:
         self.prof.setdefault(name, []).append((e0, e1))
 
     # ------------------------------------------------------------------ state I/O (reference layouts)
+    IO_CHUNKS = 8   # column chunks per prism field in the pipelined host I/O
+
     def _dests(self):
-        nt, L = self.nt, self.L
+        """(name, device planes, chunked?) of the prognostic state."""
         u = self.U[self.cur]
-        # destination planes and the (reference layout) -> device layout view of a source
-        return [("eta", self.S[0], lambda a: a.t()), ("qx", self.S[1], lambda a: a.t()),
-                ("qy", self.S[2], lambda a: a.t()),
-                ("ux", u[0], lambda a: a.reshape(nt, L, 6).permute(2, 1, 0)),
-                ("uy", u[1], lambda a: a.reshape(nt, L, 6).permute(2, 1, 0)),
-                ("T", self.T[self.cur], lambda a: a.reshape(nt, L, 6).permute(2, 1, 0))]
+        return [("eta", self.S[0], False), ("qx", self.S[1], False), ("qy", self.S[2], False),
+                ("ux", u[0], True), ("uy", u[1], True), ("T", self.T[self.cur], True)]
+
+    def _chunks(self, chunked):
+        nt = self.nt
+        n = self.IO_CHUNKS if chunked else 1
+        b = [nt * i // n for i in range(n + 1)]
+        return [(b[i], b[i + 1]) for i in range(n) if b[i + 1] > b[i]]
+
+    def _to_dev_view(self, dest, chunked, c0, c1):
+        """device planes of columns [c0, c1) and the reference-layout -> device view of a host chunk."""
+        L = self.L
+        if not chunked:
+            return dest[:, c0:c1], (lambda a: a.t())
+        return dest[:, :, c0:c1], (lambda a: a.reshape(c1 - c0, L, 6).permute(2, 1, 0))
 
     def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
         """Load a state in the reference layouts ((nt, 3) 2D fields, (P, 6) prism fields).
 
-        Host torch tensors (ideally pinned) are uploaded field by field on an upload stream while
-        the compute stream rearranges the previous field into the device layout.  A host buffer
-        that a previous get_state(out=...) is still filling is uploaded as soon as THAT field has
-        arrived (per-buffer events), so downloads and uploads of different fields overlap on the
-        two PCIe directions."""
-        dev = self.dev
+        Host torch tensors (ideally pinned) are uploaded in column chunks on an upload stream while
+        the compute stream rearranges the previous chunk into the device layout.  A host chunk that
+        a previous get_state(out=...) is still filling is uploaded as soon as THAT chunk has arrived
+        (per-chunk events), so downloads and uploads overlap on the two PCIe directions."""
+        dev, L = self.dev, self.L
         src = dict(eta=eta, qx=qx, qy=qy, ux=ux, uy=uy, T=T)
         host = all(isinstance(a, torch.Tensor) and not a.is_cuda for a in src.values())
         main = torch.cuda.current_stream(dev)
         up = self._io_streams()[0] if host else None
-        for name, dest, view in self._dests():
+        for name, dest, chunked in self._dests():
             a = src[name]
-            if host:
-                up.wait_stream(main)
-                ev = self._pending_d2h.pop(a.data_ptr(), None)
-                if ev is not None:
-                    up.wait_event(ev)
-                with torch.cuda.stream(up):
-                    buf = a.to(dev, F64, non_blocking=True)
-                main.wait_stream(up)
-                buf.record_stream(main)
-            else:
-                buf = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
-            dest.copy_(view(buf))
+            if not host:
+                a = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
+            for c0, c1 in self._chunks(chunked and host):
+                part = a[c0 * L:c1 * L] if chunked else a[c0:c1]
+                dpart, view = self._to_dev_view(dest, chunked, c0, c1)
+                if host:
+                    up.wait_stream(main)
+                    ev = self._pending_d2h.pop(part.data_ptr(), None)
+                    if ev is not None:
+                        up.wait_event(ev)
+                    with torch.cuda.stream(up):
+                        buf = part.to(dev, F64, non_blocking=True)
+                    main.wait_stream(up)
+                    buf.record_stream(main)
+                else:
+                    buf = part
+                dpart.copy_(view(buf))
         self.t = float(t)
 
     def get_state(self, numpy=True, out=None):
         """The state in the reference layouts.  out: dict of host tensors (pinned) to fill: the
-        device-to-host copies run on a download stream, field by field, overlapped with the next
-        field's rearrangement (asynchronous: synchronise before reading them on the host; a later
-        set_state from the same buffers orders itself after each field's copy)."""
+        device-to-host copies run on a download stream in column chunks, overlapped with the next
+        chunk's rearrangement (asynchronous: wait_io() / synchronise before reading them on the
+        host; a later set_state from the same buffers orders itself after each chunk's copy)."""
         nt, L = self.nt, self.L
         u = self.U[self.cur]
         if out is not None:
             main = torch.cuda.current_stream(self.dev)
             down = self._io_streams()[1]
-            for name, dest, _ in self._dests():
-                tmp = c3_out(dest) if name in ("eta", "qx", "qy") else p6_out(dest, nt, L)
-                down.wait_stream(main)
-                with torch.cuda.stream(down):
-                    out[name].copy_(tmp, non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(down)
-                tmp.record_stream(down)
-                self._pending_d2h[out[name].data_ptr()] = ev
+            for name, dest, chunked in self._dests():
+                for c0, c1 in self._chunks(chunked):
+                    dpart, _ = self._to_dev_view(dest, chunked, c0, c1)
+                    if chunked:
+                        tmp = dpart.permute(2, 1, 0).reshape((c1 - c0) * L, 6)
+                        hpart = out[name][c0 * L:c1 * L]
+                    else:
+                        tmp = dpart.t().contiguous()
+                        hpart = out[name][c0:c1]
+                    down.wait_stream(main)
+                    with torch.cuda.stream(down):
+                        hpart.copy_(tmp, non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(down)
+                    tmp.record_stream(down)
+                    self._pending_d2h[hpart.data_ptr()] = ev
             out["t"] = self.t
             return out
         res = dict(eta=c3_out(self.S[0]), qx=c3_out(self.S[1]), qy=c3_out(self.S[2]), ux=p6_out(u[0], nt, L),
