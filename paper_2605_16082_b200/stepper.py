@@ -338,21 +338,50 @@ class ImexStepper:
         self.graphs[self.cur] = g
         return g
 
-    def diagnostics(self) -> dict:
+    def diagnostics(self, stage: int = 2) -> dict:
         """diagnostics_2d (external2d.py:366-380) + budget_3d (internal3d.py:942-951) of the resident
-        state on the current grid, reduced on the device in one fused pass (one 80-byte read-back)."""
+        state on its grid, reduced on the device in one fused pass (one 80-byte read-back).
+
+        stage 2 (default): the current state; stage 1: the last step's stage-1 result (midpoint
+        fields on the stage-1 free surface), kept in the rotating buffers until the next step."""
         lb = _lib.lib()
+        if stage == 1:
+            S, u, T, t = self.Sw[0], self.U[(self.cur + 2) % 3], self.T[(self.cur + 2) % 3], self.t - 0.5 * self.dt
+        else:
+            S, u, T, t = self.S, self.U[self.cur], self.T[self.cur], self.t
         with torch.cuda.device(self.dev):
             if getattr(self, "_diag_work", None) is None:
                 self._diag_work = torch.empty(lb.pdg_diagnostics_work_doubles(self.dm.h), dtype=F64, device=self.dev)
                 self._diag_out = torch.empty(10, dtype=F64, device=self.dev)
-            self._c("diagnostics", lb.pdg_step_diagnostics(self.dm.h, ptr(self.S), ptr(self.U[self.cur]),
-                                                           ptr(self.T[self.cur]), self.p.g, ptr(self._diag_work),
-                                                           ptr(self._diag_out), stream_ptr()))
+            self._c("diagnostics", lb.pdg_step_diagnostics(self.dm.h, ptr(S), ptr(u), ptr(T), self.p.g,
+                                                           ptr(self._diag_work), ptr(self._diag_out), stream_ptr()))
             v = self._diag_out.cpu().tolist()
-        return {"t": self.t, "total_volume": v[0], "total_energy": v[1], "eta_min": v[2], "eta_max": v[3],
+        return {"t": t, "total_volume": v[0], "total_energy": v[1], "eta_min": v[2], "eta_max": v[3],
                 "volume": v[4], "momentum_x": v[5], "momentum_y": v[6], "tracer_mass": v[7], "tracer_min": v[8],
                 "tracer_max": v[9]}
+
+    DIAG_CSV = ("t", "total_volume", "total_energy", "eta_min", "eta_max")                   # SPEC.md:325
+    BUDGET_CSV = ("t", "stage", "volume", "momentum_x", "momentum_y", "tracer_mass", "tracer_min",
+                  "tracer_max")                                                            # SPEC.md:540
+
+    def log_csv(self, diag_path=None, budget_path=None):
+        """Append this step's rows to the diagnostics CSV (t,total_volume,total_energy,eta_min,eta_max)
+        and the per-step budget CSV (one row per IMEX stage); headers are written on creation."""
+        import os
+        rows = []
+        if diag_path is not None:
+            d = self.diagnostics()
+            rows.append((diag_path, self.DIAG_CSV, [d[k] for k in self.DIAG_CSV]))
+        if budget_path is not None:
+            for stage in (1, 2):
+                d = self.diagnostics(stage)
+                rows.append((budget_path, self.BUDGET_CSV, [d["t"], stage] + [d[k] for k in self.BUDGET_CSV[2:]]))
+        for path, header, vals in rows:
+            new = not os.path.exists(path)
+            with open(path, "a") as f:
+                if new:
+                    f.write(",".join(header) + "\n")
+                f.write(",".join(repr(float(v)) if isinstance(v, float) else str(v) for v in vals) + "\n")
 
     def check(self):
         """Synchronise and raise the first device-side error (DryColumn, ZeroPivot, CflViolation ...)."""

@@ -184,3 +184,23 @@ def test_host_pinned_state_io(pdg):
     g2 = ref2.get_state()
     for k in ("eta", "ux", "T"):
         assert np.array_equal(pin[k].numpy(), g2[k]), k
+
+
+def test_diagnostics_csv(pdg, tmp_path):
+    """SPEC.md:325 diagnostics CSV and SPEC.md:540 per-step budget CSV (one row per IMEX stage)."""
+    L = 4
+    m, om, p, s0 = _setup(pdg, L=L)
+    st = pdg.stepper.ImexStepper(m, L, p, 40.0, 4, 1e-3, 1e-4)
+    st.set_state(**s0)
+    for _ in range(3):
+        st.step(1)
+        st.log_csv(tmp_path / "diag.csv", tmp_path / "budget.csv")
+    d = (tmp_path / "diag.csv").read_text().splitlines()
+    b = (tmp_path / "budget.csv").read_text().splitlines()
+    assert d[0] == "t,total_volume,total_energy,eta_min,eta_max" and len(d) == 4
+    assert b[0] == "t,stage,volume,momentum_x,momentum_y,tracer_mass,tracer_min,tracer_max" and len(b) == 7
+    rows = [list(map(float, r.split(","))) for r in b[1:]]
+    assert [r[1] for r in rows] == [1, 2, 1, 2, 1, 2]
+    assert rows[0][0] == 20.0 and rows[1][0] == 40.0            # stage 1 at the midpoint, stage 2 at t
+    vols = [float(r.split(",")[1]) for r in d[1:]]
+    assert max(vols) - min(vols) <= 1e-12 * abs(vols[0])         # closed basin: volume conserved
