@@ -9,6 +9,11 @@
 
 namespace pdg {
 
+// 32-bit plane index (k * L + l) * nt + c: one field array never exceeds 2^32 words (checked at
+// pdg_ctx_set_layers), and unsigned arithmetic keeps the address math in single IMADs
+__device__ __forceinline__ unsigned pix(int k, int l, int c, int L, int nt) {
+  return ((unsigned)k * (unsigned)L + (unsigned)l) * (unsigned)nt + (unsigned)c;
+}
 // per-thread asynchronous global -> shared copies (LDGSTS): the staged kernels issue the next
 // layer's words one or two layers ahead and wait for them only when the layer is consumed
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
@@ -26,24 +31,24 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) 
 
 __device__ __forceinline__ void ld6(const double* __restrict__ f, int l, int c, int L, int nt, double v[6]) {
 #pragma unroll
-  for (int k = 0; k < 6; ++k) v[k] = f[((size_t)k * L + l) * nt + c];
+  for (int k = 0; k < 6; ++k) v[k] = f[pix(k, l, c, L, nt)];
 }
 __device__ __forceinline__ void st6(double* __restrict__ f, int l, int c, int L, int nt, const double v[6]) {
 #pragma unroll
-  for (int k = 0; k < 6; ++k) f[((size_t)k * L + l) * nt + c] = v[k];
+  for (int k = 0; k < 6; ++k) f[pix(k, l, c, L, nt)] = v[k];
 }
 
 // read-only-path (ld.global.nc) variants for kernels whose inputs never alias their outputs
 __device__ __forceinline__ void ld6g(const double* f, int l, int c, int L, int nt, double v[6]) {
 #pragma unroll
-  for (int k = 0; k < 6; ++k) v[k] = __ldg(f + ((size_t)k * L + l) * nt + c);
+  for (int k = 0; k < 6; ++k) v[k] = __ldg(f + pix(k, l, c, L, nt));
 }
 __device__ __forceinline__ void ld_nb4g(const double* f, int k2, int e2, int l, int L, int nt, double n4[4]) {
   const int a = EV0(k2), b = EV1(k2);
-  n4[0] = __ldg(f + ((size_t)a * L + l) * nt + e2);
-  n4[1] = __ldg(f + ((size_t)b * L + l) * nt + e2);
-  n4[2] = __ldg(f + ((size_t)(3 + a) * L + l) * nt + e2);
-  n4[3] = __ldg(f + ((size_t)(3 + b) * L + l) * nt + e2);
+  n4[0] = __ldg(f + pix(a, l, e2, L, nt));
+  n4[1] = __ldg(f + pix(b, l, e2, L, nt));
+  n4[2] = __ldg(f + pix((3 + a), l, e2, L, nt));
+  n4[3] = __ldg(f + pix((3 + b), l, e2, L, nt));
 }
 
 // L1 prefetch of the 6 node planes of layer l (issued one layer ahead: the thread-per-column
@@ -51,24 +56,24 @@ __device__ __forceinline__ void ld_nb4g(const double* f, int k2, int e2, int l, 
 // software pipelining -- a prefetch costs no register)
 __device__ __forceinline__ void pf6(const double* f, int l, int c, int L, int nt) {
 #pragma unroll
-  for (int k = 0; k < 6; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)k * L + l) * nt + c));
+  for (int k = 0; k < 6; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + pix(k, l, c, L, nt)));
 }
 __device__ __forceinline__ void pf_nb4(const double* f, int k2, int e2, int l, int L, int nt) {
   const int a = EV0(k2), b = EV1(k2);
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)a * L + l) * nt + e2));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)b * L + l) * nt + e2));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)(3 + a) * L + l) * nt + e2));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + ((size_t)(3 + b) * L + l) * nt + e2));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + pix(a, l, e2, L, nt)));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + pix(b, l, e2, L, nt)));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + pix((3 + a), l, e2, L, nt)));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(f + pix((3 + b), l, e2, L, nt)));
 }
 
 // the 4 lateral nodes (t0, t1, b0, b1) of the neighbour prism across local edge k2 of column e2
 __device__ __forceinline__ void ld_nb4(const double* __restrict__ f, int k2, int e2, int l, int L, int nt,
                                        double n4[4]) {
   const int a = EV0(k2), b = EV1(k2);
-  n4[0] = f[((size_t)a * L + l) * nt + e2];
-  n4[1] = f[((size_t)b * L + l) * nt + e2];
-  n4[2] = f[((size_t)(3 + a) * L + l) * nt + e2];
-  n4[3] = f[((size_t)(3 + b) * L + l) * nt + e2];
+  n4[0] = f[pix(a, l, e2, L, nt)];
+  n4[1] = f[pix(b, l, e2, L, nt)];
+  n4[2] = f[pix((3 + a), l, e2, L, nt)];
+  n4[3] = f[pix((3 + b), l, e2, L, nt)];
 }
 
 // own lateral trace on edge k at the 2v x 2h face points (internal3d.py:229-258, mirror=False)

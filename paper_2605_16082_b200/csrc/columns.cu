@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __re
     wm_layer(a, C.b, nullptr, nullptr, 0, 0, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
     }
     VPieces P;
     vop_pieces(C.j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
     }
     VPieces P;
     vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) g[i][cc] = rhs[cc * P6 + ((size_t)i * L + l) * nt + c];
+      for (int cc = 0; cc < NC; ++cc) g[i][cc] = rhs[cc * P6 + pix(i, l, c, L, nt)];
     if (l > 0) {
       // previous layer's tile, stored contiguously per prism ([l][c][36], row-major 6x6)
       const double2* gq = reinterpret_cast<const double2*>(Gs + ((size_t)(l - 1) * nt + c) * 36);
@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
-        x[cc * P6 + ((size_t)i * L + l) * nt + c] = g[i][cc];
+        x[cc * P6 + pix(i, l, c, L, nt)] = g[i][cc];
         gp[i][cc] = g[i][cc];
       }
     Vp = V;
@@ -890,14 +890,14 @@ __global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, dou
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < 6; ++k) acc = acc + G[k] * xn[k][cc];
-        xl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c] - acc;
+        xl[i][cc] = x[cc * P6 + pix(i, l, c, L, nt)] - acc;
       }
     }
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
-        x[cc * P6 + ((size_t)i * L + l) * nt + c] = xl[i][cc];
+        x[cc * P6 + pix(i, l, c, L, nt)] = xl[i][cc];
         xn[i][cc] = xl[i][cc];
       }
   }
@@ -981,9 +981,9 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-        for (int i = 0; i < 6; ++i) cp_async8(s + (cc * 6 + i) * VBLK, rhs + cc * P6 + ((size_t)i * L + l) * nt + c);
+        for (int i = 0; i < 6; ++i) cp_async8(s + (cc * 6 + i) * VBLK, rhs + cc * P6 + pix(i, l, c, L, nt));
 #pragma unroll
-      for (int i = 0; i < 6; ++i) cp_async8(s + (6 * NC + i) * VBLK, a.wt + ((size_t)i * L + l) * nt + c);
+      for (int i = 0; i < 6; ++i) cp_async8(s + (6 * NC + i) * VBLK, a.wt + pix(i, l, c, L, nt));
     }
     cp_async_commit();
   };
@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
-        x[cc * P6 + ((size_t)i * L + l) * nt + c] = g[i][cc];
+        x[cc * P6 + pix(i, l, c, L, nt)] = g[i][cc];
         gp[i][cc] = g[i][cc];
       }
     if (l < L - 1) {
@@ -1157,7 +1157,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, con
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = x[cc * P6 + ((size_t)i * L + L - 1) * nt + c];
+    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = x[cc * P6 + pix(i, L - 1, c, L, nt)];
   for (int l = L - 2; l >= 0; --l) {
     const double* gt = Gs + (size_t)l * VT * nt + c;
     double tv[VT];
@@ -1167,7 +1167,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, con
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c];
+      for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + pix(i, l, c, L, nt)];
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
       double dz[3], y[3];
@@ -1183,7 +1183,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, con
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const double v = gl[i][cc] - (tv[i * 3] * y[0] + tv[i * 3 + 1] * y[1] + tv[i * 3 + 2] * y[2]);
-        x[cc * P6 + ((size_t)i * L + l) * nt + c] = v;
+        x[cc * P6 + pix(i, l, c, L, nt)] = v;
         xn[i][cc] = v;
       }
     }
@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = x[cc * P6 + ((size_t)i * L + L - 1) * nt + c];
+    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = x[cc * P6 + pix(i, L - 1, c, L, nt)];
   for (int l = L - 2; l >= 0; --l) {
     const double* gt = Gs + (size_t)l * 18 * nt + c;
     double E[18];
@@ -1227,10 +1227,10 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + ((size_t)i * L + l) * nt + c];
+      for (int cc = 0; cc < NC; ++cc) gl[i][cc] = x[cc * P6 + pix(i, l, c, L, nt)];
     double wtn[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) wtn[k] = __ldg(a.wt + ((size_t)k * L + l + 1) * nt + c);
+    for (int k = 0; k < 3; ++k) wtn[k] = __ldg(a.wt + pix(k, l + 1, c, L, nt));
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     VG Vl;
     vgeo<true>(C, eta, ft, fb, Vl);
@@ -1275,7 +1275,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const double v = gl[i][cc] - (E[i * 3] * y[0] + E[i * 3 + 1] * y[1] + E[i * 3 + 2] * y[2]);
-        x[cc * P6 + ((size_t)i * L + l) * nt + c] = v;
+        x[cc * P6 + pix(i, l, c, L, nt)] = v;
         xn[i][cc] = v;
       }
     }
@@ -1340,7 +1340,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, dou
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
     }
     VPieces P;
     vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
@@ -1422,12 +1422,12 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
       for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
-          const size_t o = cc * P6 + ((size_t)i * L + l) * nt + c;
+          const size_t o = cc * P6 + pix(i, l, c, L, nt);
           cp_async8(s + (cc * 6 + i) * VBLK, rhs + o);
           cp_async8(s + (6 * NC + cc * 6 + i) * VBLK, xin + o);
         }
 #pragma unroll
-      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + ((size_t)i * L + l) * nt + c);
+      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + pix(i, l, c, L, nt));
     }
     cp_async_commit();
   };
@@ -1608,7 +1608,7 @@ __global__ void __launch_bounds__(128, MINB) k_vexplicit_ut(DMesh m, VopArgs a, 
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[((size_t)k * L + l + 1) * nt + c];
+      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
     }
     VAdv A;
     VDif Du, Dt;

@@ -117,6 +117,7 @@ int pdg_ctx_destroy(pdg_ctx* c) {
 
 int pdg_ctx_set_layers(pdg_ctx* c, int L, const double* fracs) {
   if (L < 1) return PDG_ERR_SHAPE;
+  if ((long long)6 * L * c->nt >= (1LL << 32)) return PDG_ERR_SHAPE;  // 32-bit plane indices (col3d.cuh pix)
   if (c->fracs) cudaFree(c->fracs);
   c->fracs = nullptr;
   if (cudaMalloc(&c->fracs, (L + 1) * sizeof(double)) != cudaSuccess) return PDG_ERR_CUDA;

@@ -41,7 +41,7 @@ __global__ void k_prism_mass(DMesh m, const double* __restrict__ eta_g, Cols cs,
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
-      for (int s = 0; s < 6; ++s) out[((size_t)(r * 6 + s) * L + l) * nt + c] = K[r / 3][s / 3] * (j2d * Mh[r % 3][s % 3]);
+      for (int s = 0; s < 6; ++s) out[pix((r * 6 + s), l, c, L, nt)] = K[r / 3][s / 3] * (j2d * Mh[r % 3][s % 3]);
   }
 }
 
@@ -80,7 +80,7 @@ __global__ void k_project(DMesh m, const double* __restrict__ eta_g, const doubl
 #pragma unroll
       for (int r = 0; r < 6; ++r)
 #pragma unroll
-        for (int s = 0; s < 6; ++s) a[r][s] = mass[((size_t)(r * 6 + s) * L + l) * nt + c];
+        for (int s = 0; s < 6; ++s) a[r][s] = mass[pix((r * 6 + s), l, c, L, nt)];
       double up[2][2][6];
       at_pts(u[0], up[0]);
       at_pts(u[1], up[1]);
@@ -171,8 +171,8 @@ __global__ void k_colsum(int nt, int L, int ncomp, const double* __restrict__ f,
     for (int a = 0; a < 3; ++a) {
       double st = 0.0, sb = 0.0;
       for (int l = 0; l < L; ++l) {
-        st += fc[((size_t)a * L + l) * nt + c];
-        sb += fc[((size_t)(3 + a) * L + l) * nt + c];
+        st += fc[pix(a, l, c, L, nt)];
+        sb += fc[pix((3 + a), l, c, L, nt)];
       }
       out[(cc * 3 + a) * nt + c] = st + sb;
     }
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(128) k_compute_w(DMesh m, const double* __rest
       double wb[3], mw[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        wb[a] = ux[((size_t)(3 + a) * L + l) * nt + c] * bx + uy[((size_t)(3 + a) * L + l) * nt + c] * by;
+        wb[a] = ux[pix((3 + a), l, c, L, nt)] * bx + uy[pix((3 + a), l, c, L, nt)] * by;
       mh_apply3(wb, j2d, mw);
 #pragma unroll
       for (int a = 0; a < 3; ++a) acc[3 + a] += mw[a];
@@ -1178,7 +1178,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
           for (int p = 0; p < 6; ++p)
 #pragma unroll
-            for (int q = 0; q < 6; ++q) M[p][q] = a.mass[((size_t)(p * 6 + q) * L + l) * nt + c];
+            for (int q = 0; q < 6; ++q) M[p][q] = a.mass[pix((p * 6 + q), l, c, L, nt)];
 #pragma unroll
           for (int p = 0; p < 6; ++p) {
             double mu0 = 0, mu1 = 0, mr0 = 0, mr1 = 0;
@@ -1922,7 +1922,7 @@ __global__ void k_stress(DMesh m, const double* __restrict__ ux, const double* _
     double dx3[3], dy3[3], mx[3], my[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const double bx = ux[((size_t)(3 + k) * L + L - 1) * nt + c], by = uy[((size_t)(3 + k) * L + L - 1) * nt + c];
+      const double bx = ux[pix((3 + k), L - 1, c, L, nt)], by = uy[pix((3 + k), L - 1, c, L, nt)];
       const double sp = sqrt(bx * bx + by * by);
       dx3[k] = -cd * sp * bx;
       dy3[k] = -cd * sp * by;
@@ -1931,8 +1931,8 @@ __global__ void k_stress(DMesh m, const double* __restrict__ ux, const double* _
     mh_apply3(dy3, j2d, my);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      out[((size_t)(3 + k) * L + L - 1) * nt + c] += mx[k];
-      out[P6 + ((size_t)(3 + k) * L + L - 1) * nt + c] += my[k];
+      out[pix((3 + k), L - 1, c, L, nt)] += mx[k];
+      out[P6 + pix((3 + k), L - 1, c, L, nt)] += my[k];
     }
   }
 }
