@@ -707,16 +707,20 @@ struct TileStage {
     hw1 = min(NW, hw0 + wpp);
     hcol = part < nparts ? halo[h0 + hj] : 0;
   }
-  __device__ __forceinline__ void issue(double* s, int tj, const StagePlanes& sp, size_t lo,
+  // lo = l * nt: plane offsets stay below 2^32 words (col3d.cuh pix), so one 32-bit offset per
+  // column is added to each plane pointer
+  __device__ __forceinline__ void issue(double* s, int tj, const StagePlanes& sp, unsigned lo,
                                         const int* __restrict__ halo) const {
     if (act) {
+      const unsigned oc = lo + (unsigned)c;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + t, sp.p[w] + lo + c);
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + t, sp.p[w] + oc);
     }
-    for (int w = hw0; w < hw1; ++w) cp_async8(s + w * tj + TW + hj, sp.p[w] + lo + hcol);
+    const unsigned oh = lo + (unsigned)hcol;
+    for (int w = hw0; w < hw1; ++w) cp_async8(s + w * tj + TW + hj, sp.p[w] + oh);
     for (int j = TW + t; j < nh; j += TW) {
-      const int col = halo[h0 + j];
-      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + TW + j, sp.p[w] + lo + col);
+      const unsigned oj = lo + (unsigned)halo[h0 + j];
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + TW + j, sp.p[w] + oj);
     }
     cp_async_commit();
   }
@@ -768,7 +772,7 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
   cp_async_wait0();
   __syncthreads();
   for (int l = 0; l < L; ++l) {
-    if (l + 1 < L) ts.issue(sbuf + (size_t)((l + 1) & 1) * 6 * tj, tj, sp, (size_t)(l + 1) * nt, halo);
+    if (l + 1 < L) ts.issue(sbuf + (size_t)((l + 1) & 1) * 6 * tj, tj, sp, (unsigned)(l + 1) * (unsigned)nt, halo);
     const double* S = sbuf + (size_t)(l & 1) * 6 * tj;
     const double ft = frs[l], fb = frs[l + 1];
     if (ts.act) {
@@ -889,7 +893,7 @@ __global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* 
   const int c = ts.c, nt = m.nt, L = m.L, t = ts.t;
   double* frs = sbuf + (size_t)2 * 12 * tj;
   for (int i2 = t; i2 <= L; i2 += TW) frs[i2] = m.fracs[i2];
-  ts.issue(sbuf + (size_t)((L - 1) & 1) * 12 * tj, tj, sp, (size_t)(L - 1) * nt, halo);
+  ts.issue(sbuf + (size_t)((L - 1) & 1) * 12 * tj, tj, sp, (unsigned)(L - 1) * (unsigned)nt, halo);
   Col C;
   double eta[3];
   EdgeNb E[3];
@@ -920,7 +924,7 @@ __global__ void __launch_bounds__(TW) k_compute_wtilde_t(DMesh m, const double* 
   cp_async_wait0();
   __syncthreads();
   for (int l = L - 1; l >= 0; --l) {
-    if (l > 0) ts.issue(sbuf + (size_t)((l - 1) & 1) * 12 * tj, tj, sp, (size_t)(l - 1) * nt, halo);
+    if (l > 0) ts.issue(sbuf + (size_t)((l - 1) & 1) * 12 * tj, tj, sp, (unsigned)(l - 1) * (unsigned)nt, halo);
     const double* S = sbuf + (size_t)(l & 1) * 12 * tj;
     if (ts.act) {
       const double jm = 0.5 * (frs[l + 1] - frs[l]);
@@ -1611,15 +1615,17 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
   // halo columns beyond TW threads (nh > TW) are covered by a strided fallback
   auto stage = [&](int l) {
     double* s = sbuf + (size_t)(l & 1) * NW * tj;
-    const size_t lo = (size_t)l * nt;
+    const unsigned lo = (unsigned)l * (unsigned)nt;
     if (act) {
+      const unsigned oc = lo + (unsigned)c;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + t, sp.p[w] + lo + c);
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + t, sp.p[w] + oc);
     }
-    for (int w = hw0; w < hw1; ++w) cp_async8(s + w * tj + TW + hj, sp.p[w] + lo + hcol);
+    const unsigned oh = lo + (unsigned)hcol;
+    for (int w = hw0; w < hw1; ++w) cp_async8(s + w * tj + TW + hj, sp.p[w] + oh);
     for (int j = TW + t; j < nh; j += TW) {
-      const int col = halo[h0 + j];
-      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + TW + j, sp.p[w] + lo + col);
+      const unsigned oj = lo + (unsigned)halo[h0 + j];
+      for (int w = 0; w < NW; ++w) cp_async8(s + w * tj + TW + j, sp.p[w] + oj);
     }
     cp_async_commit();
   };
@@ -1678,7 +1684,7 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
       if (NC >= 2 && a.bulkpf && t < 12) {   // r is read per layer from global: warm it in L2
         const int c0 = b * TW;
         const unsigned segb = (unsigned)(min(TW, m.nown - c0) * 8 + 15) & ~15u;
-        bulk_prefetch_l2(a.r + (size_t)(t / 6) * P6 + ((size_t)(t % 6) * L + l + 1) * nt + c0, segb);
+        bulk_prefetch_l2(a.r + (size_t)(t / 6) * P6 + pix(t % 6, l + 1, c0, L, nt), segb);
       }
     }
     const double* S = sbuf + (size_t)(l & 1) * NW * tj;
