@@ -114,6 +114,11 @@ def exported_symbols():
 
 
 def check(rc, what=""):
+    """Return status of a C entry: argument errors (PDG_ERR_SHAPE, ...) raise their errors.py
+    class eagerly, PDG_ERR_CUDA raises RuntimeError with the CUDA error string."""
     if rc != 0:
+        from . import errors
+        if rc != errors.ERR_CUDA:
+            errors.raise_for_code(rc, what=what)
         msg = lib().pdg_cuda_error_string().decode(errors="replace")
         raise RuntimeError(f"{what}: CUDA error ({rc}) {msg}")

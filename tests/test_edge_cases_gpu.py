@@ -102,3 +102,15 @@ def test_full_size_c4_properties(c4):
     assert float((T - 12.5).abs().max().item()) <= 1e-10 * 12.5
     for f in (st.U[st.cur], st.S):
         assert bool(torch.isfinite(f).all().item())
+
+
+def test_layer_count_beyond_32bit_planes_rejected(pdg):
+    """Per-layer addresses are 32-bit plane indices (csrc/col3d.cuh pix): a layer count that would
+    make one field array reach 2^32 words is refused with ShapeMismatch, before any allocation."""
+    m = pdg.mesh.hilbert_reorder(pdg.mesh.generate_basin_mesh(8, 8, 1e4, 1e4, lambda x, y: -20.0 + 0.0 * x))
+    dm = pdg.device.DeviceMesh(m)
+    L = (1 << 32) // (6 * m.nt) + 1
+    with pytest.raises(pdg.errors.ShapeMismatch):
+        dm.set_layers(L)
+    dm.set_layers(50)          # the context stays usable
+    assert dm.L == 50
