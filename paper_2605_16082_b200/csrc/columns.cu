@@ -369,6 +369,79 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
   V.nz = KH0 ? drsqrt(1.0 + tt) : rsqrt(1.0 + tt);
 }
 
+// sigma layers: z = eta - f (eta - b), so Jz = (f_b - f_t) H / 2 at every point and the layer's
+// diffusion mass is R_l = 2 / (f_b - f_t) Rc with the per-column Rc = sum_q QW BARY BARY / H(q),
+// and the mean height 2 mean(Jz) = (f_b - f_t) sum(H) / 3.  k_vcol forms Rc (packed symmetric),
+// sum(H) and 1 / sum(H) once per column and stage; the kh == 0 kernels then build a layer's
+// geometry from them with 6 multiplications and one reciprocal instead of 6 reciprocals and the
+// 6-point contractions (the values agree with vgeo to rounding).
+constexpr int NVC = 8;
+__global__ void k_vcol(DMesh m, const double* __restrict__ eta_u, double* __restrict__ vc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = m.nt;
+  if (c >= m.nown) return;
+  double H[3], hqv[6], ih[6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) H[k] = __dsub_rn(__ldg(eta_u + k * nt + c), __ldg(m.b + k * nt + c));
+  hq(H, hqv);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) ih[q] = QW[q] * drcp(hqv[q]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) acc += ih[q] * (BARY[q][a] * BARY[q][b]);
+      vc[(a == b ? a : 2 + a + b) * nt + c] = acc;   // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
+    }
+  const double sh = (H[0] + H[1]) + H[2];
+  vc[6 * nt + c] = sh;
+  vc[7 * nt + c] = drcp(sh);
+}
+// the column constants are re-read every layer: keep their lines resident in L1
+__device__ __forceinline__ double ldg_keep(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void vgeo_sigma(const Col& C, const double eta[3], double ft, double fb,
+                                           const double* __restrict__ vc, int c, int nt, VG& V) {
+  const double df = __dsub_rn(fb, ft);
+  const double rdf = drcp(df);
+  const double s2 = 2.0 * rdf;
+  const double r00 = ldg_keep(vc + c), r11 = ldg_keep(vc + nt + c), r22 = ldg_keep(vc + 2 * nt + c);
+  const double r01 = ldg_keep(vc + 3 * nt + c), r02 = ldg_keep(vc + 4 * nt + c), r12 = ldg_keep(vc + 5 * nt + c);
+  V.R[0][0] = s2 * r00;
+  V.R[1][1] = s2 * r11;
+  V.R[2][2] = s2 * r22;
+  V.R[0][1] = V.R[1][0] = s2 * r01;
+  V.R[0][2] = V.R[2][0] = s2 * r02;
+  V.R[1][2] = V.R[2][1] = s2 * r12;
+  V.m2a = V.m2b = V.bb = 0.0;
+  double zt[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) zt[i] = __dsub_rn(eta[i], __dmul_rn(ft, __dsub_rn(eta[i], C.b[i])));
+  const double gx = dot3_rn(zt, C.dx), gy = dot3_rn(zt, C.dy);
+  const double tt = gx * gx + gy * gy;
+  V.tt = tt;
+  V.hgt = df * ldg_keep(vc + 6 * nt + c) * (1.0 / 3.0);
+  V.rhgt = 3.0 * rdf * ldg_keep(vc + 7 * nt + c);
+  V.nz = drsqrt(1.0 + tt);
+}
+// the kh == 0 split kernels of the tracer (NC = 1) take the sigma form (their dispatcher always
+// provides the constants); the momentum kernels are at the register limit, where the extra live
+// values cost more than the saved FP64 work (measured), and keep vgeo.  The forward elimination and
+// the back substitution of one solve use the same form (the rebuilt coupling blocks match bitwise).
+template <bool KH0, bool SIG>
+__device__ __forceinline__ void vgeo_x(const Col& C, const double eta[3], double ft, double fb, const double* vc,
+                                       int c, int nt, VG& V) {
+  if constexpr (KH0 && SIG)
+    vgeo_sigma(C, eta, ft, fb, vc, c, nt, V);
+  else
+    vgeo<KH0>(C, eta, ft, fb, V);
+}
+
 // interior penalty sigma (dg.py:161-173) with L = min(L_a, L_b): n0 (p+1)(p+3) / (2 3 L)
 __device__ __forceinline__ double pen_sigma(const VG& A, const VG& B, double n0, int order, pdg_err* err) {
   const double lmin = fmin(A.hgt, B.hgt);
@@ -609,6 +682,7 @@ struct VopArgs {
   double dtm, rdtm;     // mesh-velocity step and its reciprocal
   double kh, kv, n0;
   int order;
+  const double* vc = nullptr;  // kh == 0 kernels: per-column sigma constants [8][nt] (k_vcol)
 };
 
 // node values of w_m at layer l
@@ -1000,7 +1074,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   }
   cs_put(cst, t, C, eta, e0, e1);
   VG Vp, V, Vn;
-  vgeo<KH0>(C, eta, fr[0], fr[1], V);
+  vgeo_x<KH0, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
   Vp = V;
   Vn = V;
   double gp[6][NC];
@@ -1012,7 +1086,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     const double* cur = ring + (l % 3) * NE * VBLK + t;
     const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
     const double ft = fr[l], fb = fr[l + 1];
-    if (l < L - 1) vgeo<KH0>(C, eta, fb, fr[l + 2], Vn);
+    if (l < L - 1) vgeo_x<KH0, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(6 * NC + i) * VBLK];
@@ -1212,7 +1286,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
   }
   const double j2d = C.j2d;
   VG Vu;  // geometry of layer l + 1
-  vgeo<true>(C, eta, m.fracs[L - 1], m.fracs[L], Vu);
+  vgeo_x<true, NC == 1>(C, eta, m.fracs[L - 1], m.fracs[L], a.vc, c, nt, Vu);
   double xn[6][NC];
 #pragma unroll
   for (int i = 0; i < 6; ++i)
@@ -1233,7 +1307,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
     for (int k = 0; k < 3; ++k) wtn[k] = __ldg(a.wt + pix(k, l + 1, c, L, nt));
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     VG Vl;
-    vgeo<true>(C, eta, ft, fb, Vl);
+    vgeo_x<true, NC == 1>(C, eta, ft, fb, a.vc, c, nt, Vl);
     double wm[6];
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     // Fo (vop_adv, bottom face of layer l) and the diffusion pieces cn, pb (vop_dif)
@@ -1446,7 +1520,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
   constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
   VG Vp, V, Vn;
-  vgeo<KH0>(C, eta, fr[0], fr[1], V);
+  vgeo_x<KH0, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
   Vp = V;
   Vn = V;
   // xin of layers l-1 (registers: its ring slot is refilled at the top of iteration l), l and
@@ -1486,7 +1560,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
 #pragma unroll
         for (int k = 0; k < 6; ++k) xbr[cc][k] = l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0;
     }
-    if (l < L - 1) vgeo<KH0>(C, eta, fb, fr[l + 2], Vn);
+    if (l < L - 1) vgeo_x<KH0, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
@@ -1750,6 +1824,13 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
+  if (kh == 0.0 && (implicit ? tune_get(TUNE_VSPLIT) >= 2 : tune_get(TUNE_VSPLIT) >= 3)) {
+    double* vc = ctx->vcol();
+    if (!vc) return PDG_ERR_CUDA;
+    k_vcol<<<nblocks(ctx->nown, 256), 256, 0, strm>>>(m, eta_u, vc);
+    if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+    a.vc = vc;
+  }
   if (implicit && tune_get(TUNE_VSPLIT) == 4 && kh == 0.0) {
     double* Gs = ctx->ws3((size_t)18 * ctx->L * nt);
     if (!Gs) return PDG_ERR_CUDA;

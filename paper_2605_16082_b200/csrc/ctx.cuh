@@ -49,6 +49,12 @@ struct pdg_ctx {
     m.err = err;
     return m;
   }
+  // per-column sigma-layer constants of the kh == 0 vertical kernels ([8][nt], columns.cu k_vcol)
+  double* vc = nullptr;
+  double* vcol() {
+    if (!vc && cudaMalloc(&vc, (size_t)8 * nt * sizeof(double)) != cudaSuccess) vc = nullptr;
+    return vc;
+  }
   // grows the 3D workspace (never on the hot path once sized)
   double* ws3(size_t n) {
     if (n > ws3d_doubles) {
