@@ -285,6 +285,38 @@ __device__ __forceinline__ void ld_fac(const double* __restrict__ fac, int k, in
 }
 
 // ============================================================================ baroclinic head r
+// sigma-layer geometry of the baroclinic head from per-column constants: z = eta - f H gives
+// grad z_top = grad eta - f_t grad H, grad z_mid = grad eta - f_mid grad H, grad Jz = jm grad H and
+// MHQ Jz = jm MHQ H with jm = (f_b - f_t)/2 -- a handful of FMAs per layer instead of layer_geo's
+// node-wise z evaluation and eight rounded dot products (values agree to rounding).
+struct RSig {
+  double ex, ey, hx, hy, mh[3];
+};
+__device__ __forceinline__ void rsig_init(const Col& C, const double eta[3], RSig& R) {
+  double H[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) H[i] = eta[i] - C.b[i];
+  R.ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
+  R.ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
+  R.hx = (H[0] * C.dx[0] + H[1] * C.dx[1]) + H[2] * C.dx[2];
+  R.hy = (H[0] * C.dy[0] + H[1] * C.dy[1]) + H[2] * C.dy[2];
+  mhq_vec(H, R.mh);
+}
+struct RLay {
+  double A[3], dzmid[2], djz[2], dztop[2];
+};
+__device__ __forceinline__ void rsig_layer(const RSig& R, double ft, double fb, RLay& G) {
+  const double jm = 0.5 * (fb - ft), fm = 0.5 * (ft + fb);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) G.A[a] = jm * R.mh[a];
+  G.dzmid[0] = R.ex - fm * R.hx;
+  G.dzmid[1] = R.ey - fm * R.hy;
+  G.djz[0] = jm * R.hx;
+  G.djz[1] = jm * R.hy;
+  G.dztop[0] = R.ex - ft * R.hx;
+  G.dztop[1] = R.ey - ft * R.hy;
+}
+
 // internal3d.py:327-405 + columns.py:95-122.  FROM_T: rho' = -alpha (T - t_ref) inline.
 // Volume term in closed form: -g J2D sum_v VS[v][lev] (grad_iso(v) (MHQ Jz)_a - mid2(v) (MHQ drho/dzeta)_a)
 // (meas * m_h = -J2D mid2 cancels the 1/Jz of the metric); lateral {Jz} = (f_b - f_t)/2 {H}.
@@ -303,8 +335,9 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
   EdgeNb E[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) edge_setup(m, C, eta, eta_g, k, g, E[k]);
-  const double ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
-  const double ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
+  RSig R;
+  rsig_init(C, eta, R);
+  const double ex = R.ex, ey = R.ey;
   const double j2d = C.j2d;
   const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
@@ -313,8 +346,8 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     const double jm = 0.5 * (fb - ft);
     if (l + 1 < L) pf6(rhoT, l + 1, c, L, nt);
-    LGeo G;
-    layer_geo(C, eta, ft, fb, G);
+    RLay G;
+    rsig_layer(R, ft, fb, G);
     double rho[6];
     ld6(rhoT, l, c, L, nt, rho);
     if (FROM_T) {
@@ -331,7 +364,8 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
       }
 #pragma unroll
       for (int a = 0; a < 3; ++a) dzn[a] = 0.5 * (rho[a] - rho[3 + a]);
-      mhq_vec(G.jz, A);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) A[a] = G.A[a];
       mhq_vec(dzn, B);
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
@@ -753,6 +787,7 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
   Col C;
   double eta[3], ex = 0.0, ey = 0.0;
   EdgeNb E[3];
+  RSig R{};
   if (ts.act) {
     load_col(m, c, C);
     load_eta(eta_g, c, nt, eta);
@@ -762,8 +797,9 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
       nsl[k * TW + t] = tslot[k * nt + c];
       nsl[(3 + k) * TW + t] = E[k].k2;
     }
-    ex = (eta[0] * C.dx[0] + eta[1] * C.dx[1]) + eta[2] * C.dx[2];
-    ey = (eta[0] * C.dy[0] + eta[1] * C.dy[1]) + eta[2] * C.dy[2];
+    rsig_init(C, eta, R);
+    ex = R.ex;
+    ey = R.ey;
   }
   const double j2d = ts.act ? C.j2d : 0.0;
   const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
@@ -777,8 +813,8 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
     const double ft = frs[l], fb = frs[l + 1];
     if (ts.act) {
       const double jm = 0.5 * (fb - ft);
-      LGeo G;
-      layer_geo(C, eta, ft, fb, G);
+      RLay G;
+      rsig_layer(R, ft, fb, G);
       double rho[6];
 #pragma unroll
       for (int n = 0; n < 6; ++n) rho[n] = S[n * tj + t];
@@ -796,7 +832,8 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a) dzn[a] = 0.5 * (rho[a] - rho[3 + a]);
-        mhq_vec(G.jz, A);
+  #pragma unroll
+      for (int a = 0; a < 3; ++a) A[a] = G.A[a];
         mhq_vec(dzn, B);
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
