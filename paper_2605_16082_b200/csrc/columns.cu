@@ -1049,15 +1049,19 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   __syncthreads();
   if (c >= m.nown) return;
   const size_t P6 = (size_t)6 * L * nt;
+  // plane stride hidden from the optimiser (see k_vexpl2)
   auto stage = [&](int l) {
     if (l < L) {
+      unsigned ln = (unsigned)L * (unsigned)nt;
+      asm volatile("" : "+r"(ln));
+      const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
       double* s = ring + (l % 3) * NE * VBLK + t;
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-        for (int i = 0; i < 6; ++i) cp_async8(s + (cc * 6 + i) * VBLK, rhs + cc * P6 + pix(i, l, c, L, nt));
+        for (int i = 0; i < 6; ++i) cp_async8(s + (cc * 6 + i) * VBLK, rhs + cc * P6 + (i * ln + lo));
 #pragma unroll
-      for (int i = 0; i < 6; ++i) cp_async8(s + (6 * NC + i) * VBLK, a.wt + pix(i, l, c, L, nt));
+      for (int i = 0; i < 6; ++i) cp_async8(s + (6 * NC + i) * VBLK, a.wt + (i * ln + lo));
     }
     cp_async_commit();
   };
@@ -1169,13 +1173,18 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
       return;
     }
     lu6r_solve<NC>(d, rp, g);
+    {
+      unsigned ln = (unsigned)L * (unsigned)nt;
+      asm volatile("" : "+r"(ln));
+      const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
 #pragma unroll
-    for (int i = 0; i < 6; ++i)
+      for (int i = 0; i < 6; ++i)
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        x[cc * P6 + pix(i, l, c, L, nt)] = g[i][cc];
-        gp[i][cc] = g[i][cc];
-      }
+        for (int cc = 0; cc < NC; ++cc) {
+          x[cc * P6 + (i * ln + lo)] = g[i][cc];
+          gp[i][cc] = g[i][cc];
+        }
+    }
     if (l < L - 1) {
       // E = Dt^-1 [0; I3]: forward substitution starts at row 3
       constexpr int GT = CT ? 18 : VT;   // global tile words (CT: S0, S1 rebuilt by k_vimpl_bwd_r)
@@ -1489,19 +1498,24 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   __syncthreads();
   if (c >= m.nown) return;
   const size_t P6 = (size_t)6 * L * nt;
+  // plane stride L * nt hidden from the optimiser: otherwise it keeps the five k * L * nt plane
+  // offsets live across the layer loop, which spills this 255-register kernel
   auto stage = [&](int l) {
     if (l < L) {
+      unsigned ln = (unsigned)L * (unsigned)nt;
+      asm volatile("" : "+r"(ln));
+      const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
       double* s = ring + (l % 3) * NE * VBLK + t;
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
-          const size_t o = cc * P6 + pix(i, l, c, L, nt);
+          const size_t o = cc * P6 + (i * ln + lo);
           cp_async8(s + (cc * 6 + i) * VBLK, rhs + o);
           cp_async8(s + (6 * NC + cc * 6 + i) * VBLK, xin + o);
         }
 #pragma unroll
-      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + pix(i, l, c, L, nt));
+      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + (i * ln + lo));
     }
     cp_async_commit();
   };
@@ -1613,7 +1627,13 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
 #pragma unroll
         for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
       }
-      st6(x + cc * P6, l, c, L, nt, o);
+      {
+        unsigned ln = (unsigned)L * (unsigned)nt;
+        asm volatile("" : "+r"(ln));
+        const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
+#pragma unroll
+        for (int n = 0; n < 6; ++n) x[cc * P6 + (n * ln + lo)] = o[n];
+      }
     }
     if (!XR) {
 #pragma unroll
