@@ -51,6 +51,20 @@ __device__ __forceinline__ void ld_nb4g(const double* f, int k2, int e2, int l, 
   n4[3] = __ldg(f + pix((3 + b), l, e2, L, nt));
 }
 
+// the same loads with the plane stride ln = L * nt passed in (the caller hides it from the
+// optimiser so the per-node plane offsets are re-formed instead of held live across the layer loop)
+__device__ __forceinline__ void ld6g_o(const double* f, unsigned lo, unsigned ln, double v[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = __ldg(f + (k * ln + lo));
+}
+__device__ __forceinline__ void ld_nb4g_o(const double* f, int k2, unsigned le2, unsigned ln, double n4[4]) {
+  const unsigned a = EV0(k2), b = EV1(k2);
+  n4[0] = __ldg(f + (a * ln + le2));
+  n4[1] = __ldg(f + (b * ln + le2));
+  n4[2] = __ldg(f + ((3 + a) * ln + le2));
+  n4[3] = __ldg(f + ((3 + b) * ln + le2));
+}
+
 // L1 prefetch of the 6 node planes of layer l (issued one layer ahead: the thread-per-column
 // kernels run at ~8 warps/SM, too few to hide HBM latency, and have no registers to spare for
 // software pipelining -- a prefetch costs no register)

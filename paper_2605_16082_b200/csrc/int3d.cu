@@ -1434,11 +1434,14 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
     fcur = fnext;
     fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
     const double jm = 0.5 * (fb - ft);
+    unsigned ln = (unsigned)L * (unsigned)nt;   // plane stride, hidden from the optimiser (see k_vexpl2)
+    asm volatile("" : "+r"(ln));
+    const unsigned lnt = (unsigned)l * (unsigned)nt, lo = lnt + (unsigned)c;
     double u[NC][6], qv[2][6];
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) ld6g(a.uc[cc], l, c, L, nt, u[cc]);
-    ld6g(a.qa, l, c, L, nt, qv[0]);
-    ld6g(a.qa + P6, l, c, L, nt, qv[1]);
+    for (int cc = 0; cc < NC; ++cc) ld6g_o(a.uc[cc], lo, ln, u[cc]);
+    ld6g_o(a.qa, lo, ln, qv[0]);
+    ld6g_o(a.qa + P6, lo, ln, qv[1]);
     if (MODE == 2) {
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
@@ -1483,8 +1486,8 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
       double f[2][2];
       {
         double qn[2][4];
-        ld_nb4g(a.qa, k2, e2, l, L, nt, qn[0]);
-        ld_nb4g(a.qa + P6, k2, e2, l, L, nt, qn[1]);
+        ld_nb4g_o(a.qa, k2, lnt + (unsigned)e2, ln, qn[0]);
+        ld_nb4g_o(a.qa + P6, k2, lnt + (unsigned)e2, ln, qn[1]);
         if (MODE == 2) {
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
@@ -1502,7 +1505,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double n4[4], ti[2][2], te[2][2], x[2][2];
-        ld_nb4g(a.uc[cc], k2, e2, l, L, nt, n4);
+        ld_nb4g_o(a.uc[cc], k2, lnt + (unsigned)e2, ln, n4);
         tr_own(u[cc], k, ti);
         tr_nb(n4, te);
 #pragma unroll
@@ -1520,8 +1523,8 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
     }
     if constexpr (NC >= 2) {
       double rr[2][6];
-      ld6g(a.r, l, c, L, nt, rr[0]);
-      ld6g(a.r + P6, l, c, L, nt, rr[1]);
+      ld6g_o(a.r, lo, ln, rr[0]);
+      ld6g_o(a.r + P6, lo, ln, rr[1]);
       double jz[3], Mu[3][3];
       layer_jz(bb, eta, ft, fb, jz);
       mjz(jz, Mu);
@@ -1599,7 +1602,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
           for (int n = 0; n < 6; ++n) x0[n] = u[cc][n];
         } else {
-          ld6g(a.u0c[cc], l, c, L, nt, x0);
+          ld6g_o(a.u0c[cc], lo, ln, x0);
         }
         kron_apply(M0, j2d, x0, m0x);
 #pragma unroll
