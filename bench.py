@@ -313,21 +313,24 @@ def main():
     # ---- e2e: public API, host pinned buffers, full state round trip every step
     e2e = None
     if not args.no_e2e:
-        host = st.get_state(numpy=False)
-        pin = {k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in host.items()}
-        h2d = sum(v.numel() * 8 for v in pin.values() if isinstance(v, torch.Tensor))
-        ke = max(1, min(args.steps, 5))
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record()
-        for _ in range(ke):
-            # public API with host (pinned) buffers: upload, step, download into the same buffers
-            st.set_state(pin["eta"], pin["qx"], pin["qy"], pin["ux"], pin["uy"], pin["T"], pin["t"])
-            stepper.step(1)
-            st.get_state(numpy=False, out=pin)
-        st.wait_io()                      # the last step's download is inside the timed region
-        f1.record()
-        torch.cuda.synchronize()
+        from paper_2605_16082_b200.hostmem import near_gpu
+        with near_gpu() as local_cpus:    # pinned buffers on the GPU's NUMA node (hostmem.py)
+            host = st.get_state(numpy=False)
+            pin = {k: (torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v) if isinstance(v, torch.Tensor)
+                       else v) for k, v in host.items()}
+            h2d = sum(v.numel() * 8 for v in pin.values() if isinstance(v, torch.Tensor))
+            ke = max(1, min(args.steps, 5))
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            for _ in range(ke):
+                # public API with host (pinned) buffers: upload, step, download into the same buffers
+                st.set_state(pin["eta"], pin["qx"], pin["qy"], pin["ux"], pin["uy"], pin["T"], pin["t"])
+                stepper.step(1)
+                st.get_state(numpy=False, out=pin)
+            st.wait_io()                      # the last step's download is inside the timed region
+            f1.record()
+            torch.cuda.synchronize()
         te = f0.elapsed_time(f1) / ke
         if world > 1:
             tt = torch.tensor([te], device="cuda", dtype=torch.float64)
@@ -335,7 +338,9 @@ def main():
             te = float(tt.item())
         e2e = {"value": dof_per_step / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": h2d * world, "ms_per_step": te, "steps": ke,
-               "path": "ImexStepper.set_state/step/get_state with pinned host buffers (full state round trip)"}
+               "path": "ImexStepper.set_state/step/get_state with pinned host buffers (full state round trip)",
+               "host_cpus": (f"{len(local_cpus)} GPU-local cpus ({local_cpus[0]}-{local_cpus[-1]})" if local_cpus
+                             else "unbound")}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
