@@ -1,0 +1,8 @@
+"""Host placement helper of the pinned state buffers (paper_2605_16082_b200/hostmem.py)."""
+from paper_2605_16082_b200.hostmem import _parse_cpulist
+
+
+def test_parse_cpulist():
+    assert _parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert _parse_cpulist("5") == [5]
+    assert _parse_cpulist("") == []
