@@ -14,6 +14,10 @@ namespace pdg {
 __device__ __forceinline__ unsigned pix(int k, int l, int c, int L, int nt) {
   return ((unsigned)k * (unsigned)L + (unsigned)l) * (unsigned)nt + (unsigned)c;
 }
+// the 36-plane prism-mass arrays (API only) reach 36 * L * nt words: 64-bit offsets
+__device__ __forceinline__ size_t pix36(int rs, int l, int c, int L, int nt) {
+  return ((size_t)rs * (size_t)L + (size_t)l) * (size_t)nt + (size_t)c;
+}
 // per-thread asynchronous global -> shared copies (LDGSTS): the staged kernels issue the next
 // layer's words one or two layers ahead and wait for them only when the layer is consumed
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {

@@ -1855,13 +1855,13 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     double* Gs = ctx->ws3((size_t)18 * ctx->L * nt);
     if (!Gs) return PDG_ERR_CUDA;
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
       cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)vimpl_fwd_smem(2, 4096));
       cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)vimpl_fwd_smem(1, 4096));
-      attr = true;
+      
     }
     if (ncomp == 2) {
       k_vimpl_fwd<2, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
@@ -1878,13 +1878,13 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
 #define LAUNCH_FWD(NCV, MB)                                                                       \
   {                                                                                               \
-    static bool attr = false;                                                                     \
-    if (!attr) {                                                                                  \
+    static unsigned long long attr = 0;                                                                     \
+    if (first_on_device(attr)) {                                                                                  \
       cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)vimpl_fwd_smem(NCV, 4096));                                       \
       cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)vimpl_fwd_smem(NCV, 4096));                                       \
-      attr = true;                                                                                \
+                                                                                      \
     }                                                                                             \
     if (a.kh == 0.0)                                                                              \
       k_vimpl_fwd<NCV, MB, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                  \
@@ -1916,11 +1916,11 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     const size_t sm = vexpl2_smem(ncomp, ctx->L);
 #define LAUNCH_EX(NCV, MB)                                                                                           \
   {                                                                                                                \
-    static bool attr = false;                                                                                      \
-    if (!attr) {                                                                                                   \
+    static unsigned long long attr = 0;                                                                                      \
+    if (first_on_device(attr)) {                                                                                                   \
       cudaFuncSetAttribute(k_vexpl2<NCV, MB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
       cudaFuncSetAttribute(k_vexpl2<NCV, MB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
-      attr = true;                                                                                                 \
+                                                                                                       \
     }                                                                                                              \
     if (a.kh == 0.0)                                                                                               \
       k_vexpl2<NCV, MB, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                      \

@@ -340,6 +340,16 @@ __host__ __device__ inline size_t pidx(int k, int l, int c, int L, int nt) {
 }
 
 inline int nblocks(long long n, int bs) { return (int)((n + bs - 1) / bs); }
+// kernel attributes (dynamic shared-memory limits) are per device: true the first time this
+// call site runs on the current device
+inline bool first_on_device(unsigned long long& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (seen & bit) return false;
+  seen |= bit;
+  return true;
+}
 
 // occupancy variants of the heavy thread-per-column kernels: __launch_bounds__(128, MINB)
 // (MINB 1 -> up to 255 regs / 8 warps per SM, 3 -> 168 regs, 4 -> 128 regs); chosen per

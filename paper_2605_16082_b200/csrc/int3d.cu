@@ -41,7 +41,7 @@ __global__ void k_prism_mass(DMesh m, const double* __restrict__ eta_g, Cols cs,
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
-      for (int s = 0; s < 6; ++s) out[pix((r * 6 + s), l, c, L, nt)] = K[r / 3][s / 3] * (j2d * Mh[r % 3][s % 3]);
+      for (int s = 0; s < 6; ++s) out[pix36(r * 6 + s, l, c, L, nt)] = K[r / 3][s / 3] * (j2d * Mh[r % 3][s % 3]);
   }
 }
 
@@ -80,7 +80,7 @@ __global__ void k_project(DMesh m, const double* __restrict__ eta_g, const doubl
 #pragma unroll
       for (int r = 0; r < 6; ++r)
 #pragma unroll
-        for (int s = 0; s < 6; ++s) a[r][s] = mass[pix((r * 6 + s), l, c, L, nt)];
+        for (int s = 0; s < 6; ++s) a[r][s] = mass[pix36(r * 6 + s, l, c, L, nt)];
       double up[2][2][6];
       at_pts(u[0], up[0]);
       at_pts(u[1], up[1]);
@@ -1219,7 +1219,7 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 #pragma unroll
           for (int p = 0; p < 6; ++p)
 #pragma unroll
-            for (int q = 0; q < 6; ++q) M[p][q] = a.mass[pix((p * 6 + q), l, c, L, nt)];
+            for (int q = 0; q < 6; ++q) M[p][q] = a.mass[pix36(p * 6 + q, l, c, L, nt)];
 #pragma unroll
           for (int p = 0; p < 6; ++p) {
             double mu0 = 0, mu1 = 0, mr0 = 0, mr1 = 0;
@@ -1998,17 +1998,23 @@ using namespace pdg;
 #define COLS(els, n) Cols{els, (els) ? (n) : ctx->nown}
 #define GRID1(nn) nblocks((nn), 128), 128, 0, (cudaStream_t)stream
 
+template <typename K>
+static void set_smem(K kernel, size_t sm, size_t (&attr)[64]) {   // per device (the attribute is)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (sm > attr[dev & 63]) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr[dev & 63] = sm;
+  }
+}
 template <int NC, int MODE, int TW>
 static int launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t s) {
   const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
   const size_t sm = (size_t)2 * (6 * NC + 12) * tj * sizeof(double);
-  static size_t attr = 0;
-  if (sm > attr) {
-    cudaFuncSetAttribute(k_hrhs_t<NC, MODE, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
-  }
+  static size_t attr[64] = {};
+  set_smem(k_hrhs_t<NC, MODE, TW>, sm, attr);
   StagePlanes sp{};
   const size_t P6 = (size_t)6 * ctx->L * ctx->nt, LN = (size_t)ctx->L * ctx->nt;
   for (int w = 0; w < 6 * NC + 12; ++w)
@@ -2025,13 +2031,6 @@ static StagePlanes planes_of(const double* base, int nc, const pdg_ctx* ctx) {
   for (int w = 0; w < 6 * nc; ++w) sp.p[w] = base + (size_t)(w / 6) * P6 + (size_t)(w % 6) * LN;
   return sp;
 }
-template <typename K>
-static void set_smem(K kernel, size_t sm, size_t& attr) {
-  if (sm > attr) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = sm;
-  }
-}
 template <bool FROM_T, int TW>
 static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, double alpha, double tref, double g,
                          double* r, cudaStream_t s) {
@@ -2039,7 +2038,7 @@ static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, d
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
   const size_t sm = ((size_t)2 * 6 * tj + ctx->L + 1) * sizeof(double) + (size_t)6 * TW * sizeof(int);
-  static size_t attr = 0;
+  static size_t attr[64] = {};
   set_smem(k_compute_r_t<FROM_T, TW>, sm, attr);
   k_compute_r_t<FROM_T, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, alpha, tref, g,
                                                                  planes_of(rho, 1, ctx), tm->tslot, tm->halo,
@@ -2053,7 +2052,7 @@ static int launch_wt_tile(pdg_ctx* ctx, const double* eta_g, const double* qb, c
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
   const size_t sm = ((size_t)2 * 12 * tj + ctx->L + 1) * sizeof(double);
-  static size_t attr = 0;
+  static size_t attr[64] = {};
   set_smem(k_compute_wtilde_t<TW>, sm, attr);
   k_compute_wtilde_t<TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, mis, g, planes_of(qb, 2, ctx),
                                                               tm->tslot, tm->halo, tm->hoff, tj, w);

@@ -54,16 +54,21 @@ class DeviceMesh:
             _lib.check(L.pdg_ctx_create(ctypes.byref(desc), self.device.index, ctypes.byref(h)), "pdg_ctx_create")
         self.h = h
         self.L = 0
+        self._fracs = None
         self.fingerprint = mesh_fingerprint(mesh)
         # device copies used by host-side glue (Python never reads them per step)
         self.j2d = torch.as_tensor(arrs["j2d"], device=self.device)
         self.b3 = torch.as_tensor(arrs["b"].T.copy(), device=self.device)
 
-    def set_layers(self, L: int):
-        if L != self.L:
-            fr = np.linspace(0.0, 1.0, L + 1)
+    def set_layers(self, L: int, fracs=None):
+        """Layer count and sigma fractions (default: uniform, as extrude builds them, mesh.py:389)."""
+        fr = np.linspace(0.0, 1.0, L + 1) if fracs is None else np.ascontiguousarray(fracs, dtype=np.float64)
+        if fr.shape != (L + 1,):
+            from .errors import ShapeMismatch
+            raise ShapeMismatch(f"fracs has shape {fr.shape}, expected ({L + 1},)")
+        if L != self.L or not np.array_equal(fr, self._fracs):
             _lib.check(_lib.lib().pdg_ctx_set_layers(self.h, int(L), fr.ctypes.data), "pdg_ctx_set_layers")
-            self.L = L
+            self.L, self._fracs = L, fr.copy()
         return self
 
     def raise_errors(self, what=""):
@@ -110,8 +115,9 @@ def mesh_fingerprint(mesh) -> bytes:
     return hsh.digest()
 
 
-def device_mesh(mesh, L: int | None = None) -> DeviceMesh:
-    """Cached DeviceMesh of a Mesh2D (rebuilt if the mesh arrays were edited in place)."""
+def device_mesh(mesh, L: int | None = None, fracs=None) -> DeviceMesh:
+    """Cached DeviceMesh of a Mesh2D for the per-function API (rebuilt if the mesh arrays were
+    edited in place).  Steppers never share it: each owns a DeviceMesh of its own."""
     dm = getattr(mesh, "_pdg_dev", None)
     if dm is None or dm.fingerprint != mesh_fingerprint(mesh):
         dm = DeviceMesh(mesh)
@@ -120,7 +126,7 @@ def device_mesh(mesh, L: int | None = None) -> DeviceMesh:
         except Exception:
             pass
     if L is not None:
-        dm.set_layers(L)
+        dm.set_layers(L, fracs)
     return dm
 
 

@@ -29,7 +29,14 @@ def _parse_cpulist(text: str):
 
 def gpu_local_cpus(device=None):
     """CPUs on the GPU's NUMA node (sysfs local_cpulist), or None when unknown."""
-    d = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    if device is None:
+        d = torch.cuda.current_device()
+    elif isinstance(device, int):
+        d = device
+    else:
+        d = torch.device(device).index
+        if d is None:                      # "cuda" without an index: the current device
+            d = torch.cuda.current_device()
     p = torch.cuda.get_device_properties(d)
     path = f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0/local_cpulist"
     try:

@@ -24,7 +24,7 @@ F64 = torch.float64
 
 
 def _dm(grid):
-    return device_mesh(grid.mesh, grid.n_layers)
+    return device_mesh(grid.mesh, grid.n_layers, getattr(grid, "fracs", None))
 
 
 def _eta(grid, A, dev):

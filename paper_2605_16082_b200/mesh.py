@@ -164,15 +164,19 @@ class Mesh2D:
 
 
 def _gpu() -> bool:
+    """Mesh setup runs on the GPU (csrc/mesh.cu).  The host restatement is used only when it is
+    asked for explicitly (PDG_MESH_HOST=1: CPU-only processes such as the oracle baseline workers
+    and the CPU test suite); without it a missing GPU or a broken library raises."""
     import os
-    if os.environ.get("PDG_MESH_HOST"):        # CPU-only processes (the oracle baseline workers)
+    if os.environ.get("PDG_MESH_HOST"):
         return False
-    try:
-        import torch
-        from . import _lib
-        return torch.cuda.is_available() and _lib.lib() is not None
-    except Exception:
-        return False
+    import torch
+    from . import _lib
+    if not torch.cuda.is_available():
+        raise RuntimeError("Mesh2D setup needs a CUDA device (csrc/mesh.cu); set PDG_MESH_HOST=1 to build "
+                           "the connectivity on the host instead")
+    _lib.lib()                                 # raises if the sm_100a library is missing
+    return True
 
 
 def make_mesh(vx, vy, vb, tri) -> Mesh2D:
@@ -307,15 +311,35 @@ class ColumnGrid:
     attributes below are computed lazily on the host only for API users.
     """
 
-    def __init__(self, mesh: Mesh2D, L: int, eta: np.ndarray, eta_prev=None, dt_prev=None):
+    def __init__(self, mesh: Mesh2D, layers=None, offsets=None, fracs=None, eta=None, z=None, jz=None, w_m=None,
+                 dzmid=None, djz=None, dztop=None, dzbot=None, *, L: int | None = None, eta_prev=None,
+                 dt_prev=None):
+        """The reference dataclass's field order (mesh.py:308-325): (mesh, layers, offsets, fracs,
+        eta, z, jz, w_m, dzmid, djz, dztop, dzbot).  Array fields left out are derived from
+        (eta, fracs) on first access; ones passed in are kept as given (the device kernels always
+        rebuild the geometry from eta, b and fracs).  Keyword-only extras: L (uniform layer count
+        instead of `layers`) and eta_prev / dt_prev (the previous free surface and step, from which
+        w_m is derived, mesh.py:418)."""
+        if layers is None:
+            if L is None:
+                raise TypeError("ColumnGrid needs `layers` (per-column counts) or L=")
+            layers = np.full(mesh.nt, int(L), dtype=np.int64)
+        elif np.ndim(layers) == 0:          # a bare layer count
+            layers = np.full(mesh.nt, int(layers), dtype=np.int64)
         self.mesh = mesh
-        self.layers = np.full(mesh.nt, L, dtype=np.int64)
-        self.offsets = np.arange(mesh.nt + 1, dtype=np.int64) * L
-        self.fracs = np.linspace(0.0, 1.0, L + 1)
-        self.eta = eta
+        self.layers = np.asarray(layers, dtype=np.int64)
+        if self.layers.size and self.layers.min() != self.layers.max():
+            raise NonConforming("the device path needs one layer count for every column")
+        Lc = self.n_layers
+        self.offsets = np.arange(mesh.nt + 1, dtype=np.int64) * Lc if offsets is None else np.asarray(offsets)
+        self.fracs = np.linspace(0.0, 1.0, Lc + 1) if fracs is None else np.asarray(fracs, dtype=float)
+        self.eta = np.zeros((mesh.nt, 3)) if eta is None else eta
         self._eta_prev = eta_prev
         self._dt_prev = dt_prev
         self._geo = None
+        given = dict(z=z, jz=jz, dzmid=dzmid, djz=djz, dztop=dztop, dzbot=dzbot)
+        self._given = {k: v for k, v in given.items() if v is not None}
+        self._w_m = w_m
 
     @property
     def n_layers(self) -> int:
@@ -352,16 +376,22 @@ class ColumnGrid:
                              dztop=grad(zt), dzbot=grad(zb))
         return self._geo
 
-    z = property(lambda self: self._geometry()["z"])
-    jz = property(lambda self: self._geometry()["jz"])
-    dzmid = property(lambda self: self._geometry()["dzmid"])
-    djz = property(lambda self: self._geometry()["djz"])
-    dztop = property(lambda self: self._geometry()["dztop"])
-    dzbot = property(lambda self: self._geometry()["dzbot"])
+    def _field(self, k):
+        v = self._given.get(k)
+        return v if v is not None else self._geometry()[k]
+
+    z = property(lambda self: self._field("z"))
+    jz = property(lambda self: self._field("jz"))
+    dzmid = property(lambda self: self._field("dzmid"))
+    djz = property(lambda self: self._field("djz"))
+    dztop = property(lambda self: self._field("dztop"))
+    dzbot = property(lambda self: self._field("dzbot"))
 
     @property
     def w_m(self) -> np.ndarray:
         """Nodal mesh velocity (z - z_prev)/dt (mesh.py:418); zero for a fresh extrusion."""
+        if self._w_m is not None:
+            return self._w_m
         if self._eta_prev is None:
             return np.zeros((self.n_prisms, 6))
         zt, zb = self._z(self._eta_prev)
@@ -389,7 +419,7 @@ def extrude(mesh: Mesh2D, policy: LayerPolicy, eta=None) -> ColumnGrid:
         c = int(np.argmin(H.min(axis=1)))
         raise DryColumn(c, float(H[c].min()))
     L = int(counts[0])
-    g = ColumnGrid(mesh, L, eta.copy())
+    g = ColumnGrid(mesh, L=L, eta=eta.copy())
     if L > 1 and np.any(np.diff(g.fracs) <= 0.0):
         raise DegenerateLayer("non-positive layer thickness after extrusion")
     return g

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import c3_in, c3_out, device_mesh, p6_in, p6_out, ptr, stream_ptr
+from .device import DeviceMesh, c3_out, p6_out, ptr, stream_ptr
 from .params import PenaltyParams, PhysParams
 
 F64 = torch.float64
@@ -48,11 +48,10 @@ class ImexStepper:
         self.mesh, self.L, self.p = mesh, L, params
         self.dt, self.m, self.kv, self.nu_v, self.pen = float(dt), int(m), float(kv), float(nu_v), pen
         self.part = part          # partition.Part when this stepper owns only part of the columns
-        if part is None:
-            self.dm = device_mesh(mesh, L)
-        else:
-            from .device import DeviceMesh
-            self.dm = DeviceMesh(mesh, device).set_layers(L)
+        # a context of its own: the captured graphs hold its layer count, sigma fractions and
+        # block-Thomas workspace, which a shared (per-mesh) context could resize under them
+        self.dm = DeviceMesh(mesh, device).set_layers(L)
+        if part is not None:
             _lib.check(_lib.lib().pdg_ctx_set_owned(self.dm.h, part.n_own), "set_owned")
         self.halo = None          # DistHalo for multi-process runs (VirtualGroup drives several steppers)
         self.dev = self.dm.device

@@ -8,6 +8,13 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+try:   # no GPU here: the CPU suite builds meshes with the host restatement, explicitly
+    import torch
+    if not torch.cuda.is_available():
+        os.environ.setdefault("PDG_MESH_HOST", "1")
+except ImportError:
+    os.environ.setdefault("PDG_MESH_HOST", "1")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built extension")

@@ -19,3 +19,15 @@ def test_near_gpu_restores_affinity():
         if cpus:
             assert os.sched_getaffinity(0) == set(cpus)
     assert os.sched_getaffinity(0) == before
+
+
+@pytest.mark.gpu
+def test_device_argument_forms_agree():
+    """'cuda' (no index), an int and torch.device all name the current device."""
+    import torch
+    from paper_2605_16082_b200.hostmem import gpu_local_cpus
+    cur = torch.cuda.current_device()
+    ref = gpu_local_cpus(None)
+    assert gpu_local_cpus("cuda") == ref
+    assert gpu_local_cpus(cur) == ref
+    assert gpu_local_cpus(torch.device("cuda", cur)) == ref
