@@ -32,7 +32,9 @@ sys.path.insert(0, ROOT)
 METRIC = "prism-DOF updates/s (FP64 RK step)"
 UNIT = "prism-DOF/s"
 
-# compulsory (algorithmic) HBM bytes per prism for each stepper launch
+# compulsory (algorithmic) HBM bytes per prism for each stepper launch: the
+# prism fields each launch must read and write once; per-column 2D data, neighbour traces and
+# geometry (recomputed from eta, b and the sigma fractions) are not counted
 KERNEL_BYTES = {
     "r": 48 + 96,                       # read T, write r (2 comps)
     "project": 96 + 96,                 # read u, write q
@@ -40,15 +42,19 @@ KERNEL_BYTES = {
     "wtilde": 96 + 48,                  # read q, write w~
     "rhs_u": 96 * 4 + 96,               # read u, u0, q, r; write rhs
     "rhs_T": 48 + 48 + 96 + 48,         # read T, T0, q; write rhs
-    "rhs_uT": 96 * 4 + 96 + 48 * 2 + 48,  # read u, u0, q, r, T, T0; write rhs_u, rhs_T
+    "rhs_uT_s1": 96 * 3 + 48 + 96 + 48,   # stage 1 (u0 = u, T0 = T): read u, q, r, T; write rhs_u, rhs_T = 480
+    "rhs_uT_s2": 96 * 4 + 48 * 2 + 96 + 48,   # stage 2: + u0, T0 = 624
     "vertical_u_impl": 96 + 48 + 96,    # read rhs, w~; write u1
     "vertical_T_impl": 48 + 48 + 48,
     "vertical_u_expl": 96 + 48 + 96 + 96,   # + u for A u
     "vertical_T_expl": 48 + 48 + 48 + 48,
     "vertical_uT_expl": 96 + 48 + 96 + 96 + 48 * 3,
 }
-# 2D RK stage per triangle: X 72 + S0 72 + geometry 188 + F3D->2D 48 + write 72 (+ Qbar 48 on stage 3)
-RK_STAGE_BYTES_PER_TRI = 72 + 72 + 188 + 48 + 72 + 16
+# 2D sub-cycle, SURVEY.md section 8d model M2: per triangle and SSP-RK3 substep 3 evaluations x
+# (state 72 + geometry incl. b 194) + 2 x 72 substep-start reads + 3 x 72 writes + 96 Qbar = 1254 B.
+# (Part of the 1 M-triangle 2D working set stays in the 126 MB L2 between RK stages, so the
+# measured DRAM traffic per substep is below this count: profiles/<round>_traffic.json.)
+RK_SUBSTEP_BYTES_PER_TRI = 3 * (72 + 194) + 2 * 72 + 3 * 72 + 96
 M2_BYTES_PER_PRISM = lambda L, m: 2736 + 1881.0 * m / L  # noqa: E731  (SURVEY.md section 8d model M2)
 
 
@@ -121,30 +127,66 @@ class Clocks:
 # ----------------------------------------------------------------------------------------- CPU (oracle)
 
 def _oracle_worker(args):
-    """One bounded oracle run: `steps` full IMEX steps on a patch of the workload (own process)."""
-    name, scale, L, steps, seed = args
+    """One bounded CPU run: `steps` full IMEX steps on a patch of the workload (own process).
+    kind "reference": the reference's own functions (baseline/_ref, oracle/refops.py) composed by
+    the shared orchestrator; "port": the numpy restatement (oracle/)."""
+    name, scale, L, steps, seed, kind = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from types import SimpleNamespace
 
-    from oracle import ext2d as OE
-    from oracle import geom as OG
     from oracle import stepper as OS
     from paper_2605_16082_b200.scenarios import make_case
     c = make_case(name, scale=scale, L=L)
-    om = OG.make_mesh(c.mesh.vx, c.mesh.vy, c.mesh.vb, c.mesh.tri)
     s0 = c.state
-    s = SimpleNamespace(grid=OG.extrude(om, c.L, s0["eta"]), ux=s0["ux"], uy=s0["uy"], T=s0["T"],
-                        s2d=OE.S2(s0["eta"].copy(), s0["qx"], s0["qy"], 0.0))
+    if kind == "reference":
+        from oracle import refops
+        ref = refops.load()
+        s, p = refops.initial(ref, (c.mesh.vx, c.mesh.vy, c.mesh.vb, c.mesh.tri), c.L, s0, c.params)
+        step = lambda s_: OS.imex_step_ops(ref.ops, s_, p, c.dt, c.m, c.kv, c.nu_v)  # noqa: E731
+    else:
+        from oracle import ext2d as OE
+        from oracle import geom as OG
+        om = OG.make_mesh(c.mesh.vx, c.mesh.vy, c.mesh.vb, c.mesh.tri)
+        s = SimpleNamespace(grid=OG.extrude(om, c.L, s0["eta"]), ux=s0["ux"], uy=s0["uy"], T=s0["T"],
+                            s2d=OE.S2(s0["eta"].copy(), s0["qx"], s0["qy"], 0.0))
+        step = lambda s_: OS.imex_step(s_, c.params, c.dt, c.m, c.kv, c.nu_v)  # noqa: E731
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        s = OS.imex_step(s, c.params, c.dt, c.m, c.kv, c.nu_v)
+        s = step(s)
         times.append(time.perf_counter() - t0)
     return times, c.prisms
 
 
-def cpu_oracle_throughput(name, steps, procs, scale, skip=0):
-    """prism-DOF/s of the oracle: `procs` independent patches in parallel processes (all host cores).
+def cpu_kind():
+    """"reference" when the unmodified reference is installed (baseline/_ref), else the "port"."""
+    from oracle import refops
+    return "reference" if refops.find() else "port"
+
+
+def host_info():
+    """CPU model, core count and numpy build of the host the CPU legs ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name')} {b.get('version')}".strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__, "numpy_blas": blas}
+
+
+def cpu_oracle_throughput(name, steps, procs, scale, skip=0, kind="port"):
+    """prism-DOF/s of the CPU path: `procs` independent patches in parallel processes (all host cores).
 
     Returns (value, seconds per step (max over processes, mean over the timed steps), prisms per process).
     """
@@ -153,7 +195,7 @@ def cpu_oracle_throughput(name, steps, procs, scale, skip=0):
         os.environ[v] = "1"
     os.environ["PDG_MESH_HOST"] = "1"          # the CPU arm never touches the GPU
     L = 50 if name == "c4" else None
-    jobs = [(name, scale, L, steps, i) for i in range(procs)]
+    jobs = [(name, scale, L, steps, i, kind) for i in range(procs)]
     if procs == 1:
         res = [_oracle_worker(jobs[0])]
     else:
@@ -166,25 +208,61 @@ def cpu_oracle_throughput(name, steps, procs, scale, skip=0):
 
 
 def run_reference(args, rank, world):
-    """The reference arm: the CPU oracle (numpy restatement of the reference) on all host cores."""
+    """The reference arm: the reference's CPU implementation of the step on all host cores."""
     if rank != 0:
         return
     procs = max(1, min(os.cpu_count() or 1, 64))
     scale = 0.02 if args.config == "c4" else 0.2   # c4 patch: 20 x 10 squares = 400 tri x 50 layers
+    kind = cpu_kind()
     value, tstep, prisms = cpu_oracle_throughput(args.config, args.warmup + args.steps, procs, scale,
-                                                 skip=args.warmup)
+                                                 skip=args.warmup, kind=kind)
+    what = ("the reference's own functions (baseline/_ref prismdg, unmodified) composed by the shared "
+            "orchestrator oracle/stepper.py" if kind == "reference" else "numpy restatement oracle/")
     sample = (f"{procs} independent processes, each one full IMEX step (L=50, m=20) of a {prisms}-prism patch of the "
-              f"{args.config} workload per bench step (numpy oracle, oracle/stepper.py)")
+              f"{args.config} workload per bench step ({what}); the full C4 step (50 M prisms) does not fit a "
+              f"single CPU process (SURVEY.md section 0.5), so the value is per-prism throughput on patches")
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": tstep * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": f"{args.config} (bounded CPU sample: {prisms} prisms per process)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": kind, "sample": sample,
+                            "host": host_info()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
 # ----------------------------------------------------------------------------------------- GPU
+
+def pcie_bandwidth(torch, nbytes=1 << 30, reps=3):
+    """Measured pinned-host <-> device copy bandwidth (GB/s): H2D alone, D2H alone, both at once."""
+    h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
+    h2 = torch.empty_like(h, pin_memory=True)
+    d = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    d2 = torch.empty_like(d)
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return best
+    t_up = timed(lambda: d.copy_(h, non_blocking=True))
+    t_dn = timed(lambda: h2.copy_(d2, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(up):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(down):
+            h2.copy_(d2, non_blocking=True)
+    t_bi = timed(both)
+    return {"h2d_GBps": nbytes / t_up / 1e9, "d2h_GBps": nbytes / t_dn / 1e9, "bidir_GBps": 2 * nbytes / t_bi / 1e9,
+            "probe_bytes": nbytes}
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -287,26 +365,32 @@ def main():
             b = KERNEL_BYTES[k] * P_local
         elif k.startswith("subcycle"):
             msub = int(k[len("subcycle"):])
-            b = RK_STAGE_BYTES_PER_TRI * (P_local // case.L) * 3 * msub
+            b = RK_SUBSTEP_BYTES_PER_TRI * (P_local // case.L) * msub
         elif k.startswith("rk"):
-            b = RK_STAGE_BYTES_PER_TRI * (P_local // case.L)
+            b = RK_SUBSTEP_BYTES_PER_TRI * (P_local // case.L) / 3.0
         else:
             b = 0
         per[k] = {"ms": ms, "share": ms * counts[k] / step_sum, "GBps": (b / (ms * 1e-3) / 1e9) if b else None,
                   "bytes": b}
     dom = max((k for k in per if per[k]["bytes"]), key=lambda k: per[k]["ms"] * counts[k])
     ach = per[dom]["GBps"]
-    traffic, traffic_src = None, None
-    try:   # DRAM read+write bytes of one launch from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            tr = json.load(f).get(dom)
-        if tr and args.config == "c4" and world == 1:
-            traffic, traffic_src = tr["dram_bytes"], tr["source"]
+    traffic, traffic_src, tr_all = None, None, {}
+    try:   # DRAM read+write bytes per launch from the newest committed ncu --set full capture
+        import glob
+        tj = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))[-1]
+        with open(tj) as f:
+            tr_all = json.load(f) if args.config == "c4" and world == 1 else {}
+        if dom in tr_all:
+            traffic, traffic_src = tr_all[dom]["dram_bytes"], tr_all[dom]["source"]
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
                 "bytes_per_launch": per[dom]["bytes"], "launch_ms": per[dom]["ms"],
+                "per_kernel": {k: {"alg_bytes": v["bytes"], "ms": round(v["ms"], 4),
+                                   "frac": (round(v["GBps"] / hbm, 4) if v["GBps"] else None),
+                                   "dram_bytes": (tr_all[k]["dram_bytes"] if k in tr_all else None)}
+                               for k, v in per.items() if v["bytes"]},
                 "step_model_M2": {"bytes_per_prism": M2_BYTES_PER_PRISM(case.L, case.m),
                                   "frac": M2_BYTES_PER_PRISM(case.L, case.m) * P / world / (t_ms * 1e-3) / 1e9 / hbm}}
 
@@ -336,20 +420,31 @@ def main():
             tt = torch.tensor([te], device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
+        pcie = pcie_bandwidth(torch)
+        # floor of the host round trip: a step needs its whole state uploaded before it starts and the
+        # previous state's download overlaps the next upload on the other PCIe direction
+        floor_ms = max(h2d / pcie["h2d_GBps"], h2d / pcie["d2h_GBps"]) / 1e6 + t_ms
+        pcie.update(floor_ms=floor_ms, frac_of_floor=floor_ms / te,
+                    achieved_io_GBps=h2d / max(te - t_ms, 1e-9) / 1e6)
         e2e = {"value": dof_per_step / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": h2d * world, "ms_per_step": te, "steps": ke,
                "path": "ImexStepper.set_state/step/get_state with pinned host buffers (full state round trip)",
                "host_cpus": (f"{len(local_cpus)} GPU-local cpus ({local_cpus[0]}-{local_cpus[-1]})" if local_cpus
-                             else "unbound")}
+                             else "unbound"), "pcie": pcie}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         procs = 1
-        v, tstep, prisms = cpu_oracle_throughput(args.config, 2, procs, 0.02 if args.config == "c4" else 0.2)
-        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+        kind = cpu_kind()
+        v, tstep, prisms = cpu_oracle_throughput(args.config, 2, procs, 0.02 if args.config == "c4" else 0.2,
+                                                 kind=kind)
+        what = "reference functions (baseline/_ref) + oracle/stepper.py" if kind == "reference" else \
+            "numpy oracle (oracle/stepper.py)"
+        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": kind, "host": host_info(),
                "sample": f"2 full IMEX steps (L={case.L}, m={case.m}) of a {prisms}-prism patch of {args.config}, "
-                         f"numpy oracle (oracle/stepper.py), single process; {tstep:.2f} s/step"}
+                         f"{what}, single process; {tstep:.2f} s/step. C4 at full size extrapolated per prism: "
+                         f"{tstep * case.prisms / prisms / 3600:.1f} h/step (not run: ~280 GB)"}
 
     if args.dump:
         s_ = st.get_state()

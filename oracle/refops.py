@@ -1,0 +1,55 @@
+"""The REAL reference's functions as the operator set of the shared orchestrator.
+
+Test / measurement infrastructure only (bench.py --impl reference and its cpu_baseline leg,
+scripts/make_golden*.py).  The reference ships no stepper, so a reference
+"step" is oracle/stepper.imex_step_ops driven by these operators: every arithmetic operation is the
+reference's own (/root/reference/pkg/src/prismdg, installed unmodified into baseline/_ref).
+"""
+import os
+import sys
+from types import SimpleNamespace
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CANDIDATES = (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
+
+
+def find():
+    """Directory holding the reference package `prismdg`, or None."""
+    for p in CANDIDATES:
+        if os.path.isfile(os.path.join(p, "prismdg", "internal3d.py")):
+            return p
+    return None
+
+
+def load(path=None):
+    path = path or find()
+    if path is None:
+        raise ImportError("reference package prismdg not found (baseline/_ref or /root/reference)")
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    from prismdg import columns as RC
+    from prismdg import external2d as RE
+    from prismdg import internal3d as RI
+    from prismdg import mesh as RM
+    ops = SimpleNamespace(
+        eos=RE.eos_density, compute_r=RI.compute_r, prism_mass=RI.prism_mass,
+        project_transport=RI.project_transport, lateral_flux_factor=RI.lateral_flux_factor,
+        horizontal_rhs=RI.horizontal_rhs, stress_rhs=RI.stress_rhs, column_sum=RI.column_sum,
+        consistent_transport=RI.consistent_transport, compute_wtilde=RI.compute_wtilde,
+        tracer_horizontal_rhs=RI.tracer_horizontal_rhs, assemble_vertical_operator=RI.assemble_vertical_operator,
+        build_implicit=RI.build_implicit, mass_apply=RI.mass_apply, mass_solve=RI.mass_solve,
+        solve_banded_column=RC.solve_banded_column, apply_banded=RC.apply_banded,
+        update_moving_mesh=RM.update_moving_mesh,
+        subcycle=lambda s, m_, pp, ms_, dt_, f3d2d: RE.subcycle_external(s, m_, pp, ms_, dt_, f3d2d=f3d2d))
+    return SimpleNamespace(ops=ops, RC=RC, RE=RE, RI=RI, RM=RM, path=path)
+
+
+def initial(ref, mesh_arrays, L, state, params):
+    """Reference mesh / grid / State2D / PhysParams for a product-built case (same arrays)."""
+    import dataclasses
+    vx, vy, vb, tri = mesh_arrays
+    m = ref.RM.make_mesh(vx, vy, vb, tri)
+    grid = ref.RM.extrude(m, ref.RM.LayerPolicy(count=L), state["eta"])
+    s = SimpleNamespace(grid=grid, ux=state["ux"], uy=state["uy"], T=state["T"],
+                        s2d=ref.RE.State2D(state["eta"].copy(), state["qx"], state["qy"], 0.0))
+    return s, ref.RE.PhysParams(**dataclasses.asdict(params))

@@ -253,7 +253,7 @@ class ImexStepper:
         tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
            ptr(self.wt), s)
         if self.fuse_rhs:
-            tm("rhs_uT", lb.pdg_step_rhs_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(T), ptr(u0), ptr(T0),
+            tm("rhs_uT_s1" if u is u0 else "rhs_uT_s2", lb.pdg_step_rhs_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(T), ptr(u0), ptr(T0),
                ptr(self.q), ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s,
                ptr(out_u), ptr(out_T), s)
         else:

@@ -13,12 +13,15 @@ KEYS = {
     "project": ["k_project<0"],
     "f3d2d": ["k_hrhs_t<2, 1"],
     "wtilde": ["k_compute_wtilde_t"],
-    "rhs_uT": ["k_hrhs_s<3, 2"],
+    "rhs_uT_s1": ["k_hrhs_s<3, 2, 1, 1"],     # stage 1 (u = u0, T = T0)
+    "rhs_uT_s2": ["k_hrhs_s<3, 2, 1, 0"],
     "vertical_u_impl": ["k_vimpl_fwd<2", "k_vimpl_bwd_r<2"],
     "vertical_T_impl": ["k_vimpl_fwd<1", "k_vimpl_bwd_r<1"],
     "vertical_u_expl": ["k_vexpl2<2"],
     "vertical_T_expl": ["k_vexpl2<1"],
-    "rk_stage": ["k_rk_stage<1"],
+    "rk_stage0": ["k_rk_stage<0"],
+    "rk_stage1": ["k_rk_stage<1"],
+    "rk_stage2": ["k_rk_stage<2"],
 }
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 

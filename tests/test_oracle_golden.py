@@ -124,3 +124,29 @@ def test_diagnostics(golden):
     b3 = int3d.budget_3d(grid, int3d.prism_mass(grid), g["ux"], g["uy"], g["T"])
     for k, v in {**d2, **b3}.items():
         assert abs(v - ref[k]) <= 1e-13 * max(abs(ref[k]), 1.0), (k, v, ref[k])
+
+
+@pytest.mark.parametrize("name", ["c2", "c3w"])
+def test_oracle_first_step_of_config_fixtures(golden, name):
+    """The oracle orchestrator + oracle functions reproduce the reference's first step of the
+    stated-size config fixtures (tests/golden/cfg_*.npz)."""
+    import os
+    import sys
+    from types import SimpleNamespace
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import config_states as CS
+    from oracle import ext2d as OE
+    from oracle import geom as OG
+    from oracle import stepper as OS
+    from paper_2605_16082_b200.params import PhysParams
+    cfg = CS.C2 if name == "c2" else CS.C3W
+    g = golden(f"cfg_{name}")
+    om = OG.hilbert_reorder(OG.basin_mesh(cfg["nx"], cfg["ny"], cfg["lx"], cfg["ly"], CS.flat_bed))
+    L = cfg["L"]
+    s0 = CS.c2_state(om, L) if name == "c2" else CS.c3_state(om, L, cfg["lx"])
+    s = SimpleNamespace(grid=OG.extrude(om, L, s0["eta"]), ux=s0["ux"], uy=s0["uy"], T=s0["T"],
+                        s2d=OE.S2(s0["eta"].copy(), s0["qx"], s0["qy"], 0.0))
+    s = OS.imex_step(s, PhysParams(**cfg["params"]), cfg["dt"], cfg["m"], cfg["kv"], cfg["nu_v"])
+    for n, a in (("ux", s.ux), ("uy", s.uy), ("T", s.T), ("eta", s.s2d.eta), ("qx", s.s2d.qx), ("qy", s.s2d.qy)):
+        ref = g[f"s1_{n}"]
+        assert np.abs(a - ref).max() <= 1e-13 * max(np.abs(ref).max(), 1e-300), n
