@@ -16,6 +16,22 @@ except ImportError:
     os.environ.setdefault("PDG_MESH_HOST", "1")
 
 
+PARITY = {}   # test id -> worst normwise relative error it checked (PDG_PARITY_LOG=path writes them)
+
+
+def record(name, err):
+    PARITY[name] = max(PARITY.get(name, 0.0), float(err))
+    return err
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("PDG_PARITY_LOG")
+    if path and PARITY:
+        import json
+        with open(path, "w") as f:
+            json.dump(dict(sorted(PARITY.items())), f, indent=1)
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built extension")
     config.addinivalue_line("markers", "slow: long-running")
