@@ -196,6 +196,33 @@ int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, c
 int pdg_halo_pack(const double* field, long long nplanes, int nt, const int* idx, int n, double* buf, void* stream);
 int pdg_halo_unpack(const double* buf, long long nplanes, int nt, const int* idx, int n, double* field, void* stream);
 
+/* ---- NCCL halo exchange of a partitioned run (csrc/comm.cu).
+ * The library binds the process's NCCL at run time (pdg_comm_load(path of libnccl.so.2)); rank 0
+ * creates the 128-byte unique id, the caller broadcasts it (torch.distributed bootstrap).  A plan
+ * lists per peer the owned columns to send and the ghost slots to fill (host int32 lists, copied).
+ * start: pack + grouped ncclSend/ncclRecv on the plan's communication stream (after the pack);
+ * finish: `stream` waits for the transfers, then unpacks.  Work launched on `stream` between the
+ * two overlaps the exchange; every call is stream ordered and CUDA-graph capturable. */
+typedef struct pdg_comm pdg_comm;
+typedef struct pdg_halo_plan pdg_halo_plan;
+int pdg_comm_load(const char* libnccl_path);
+const char* pdg_comm_error_string(void);
+int pdg_comm_unique_id(void* id128);
+int pdg_comm_init(const void* id128, int rank, int nranks, int device, pdg_comm** out);
+int pdg_comm_destroy(pdg_comm* comm);
+int pdg_halo_plan_create(pdg_comm* comm, int nt, int npeers, const int* peers, const int* nsend,
+                         const int* const* send_idx, const int* nrecv, const int* const* recv_idx, int max_planes,
+                         pdg_halo_plan** out);
+int pdg_halo_plan_destroy(pdg_halo_plan* plan);
+int pdg_halo_start(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
+int pdg_halo_finish(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
+
+/* ---- host I/O layout conversion (set_state / get_state of the drop-in; csrc/hostio.cu):
+ * rows [ncols][L][nk] = columns [c0, c0 + ncols) of a reference-layout field ((P, nk) with
+ * p = c L + l, or (nt, nk) with L = 1) in a device staging buffer  <->  planes [nk][L][nt] */
+int pdg_rows_to_planes(const double* rows, int ncols, int L, int nk, double* planes, int nt, int c0, void* stream);
+int pdg_planes_to_rows(const double* planes, int nt, int c0, int ncols, int L, int nk, double* rows, void* stream);
+
 /* ---- fused IMEX stage entries (the stepper) ---------------- */
 /* F3D->2D = column sum of horizontal_rhs(u, q, fac(q)) + stress_rhs  -> [2][3][nt] */
 int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r, double g,

@@ -40,6 +40,17 @@ _SIGS = {
     "pdg_ext2d_rk_stage_cols": (I, [P, I, P, P, P, D, D, D, P, P, P, I, P]),
     "pdg_halo_pack": (I, [P, LL, I, P, I, P, P]),
     "pdg_halo_unpack": (I, [P, LL, I, P, I, P, P]),
+    "pdg_comm_load": (I, [ctypes.c_char_p]),
+    "pdg_comm_error_string": (ctypes.c_char_p, []),
+    "pdg_comm_unique_id": (I, [P]),
+    "pdg_comm_init": (I, [P, I, I, I, ctypes.POINTER(P)]),
+    "pdg_comm_destroy": (I, [P]),
+    "pdg_halo_plan_create": (I, [P, I, I, P, P, P, P, P, I, ctypes.POINTER(P)]),
+    "pdg_halo_plan_destroy": (I, [P]),
+    "pdg_halo_start": (I, [P, I, P, P, P]),
+    "pdg_halo_finish": (I, [P, I, P, P, P]),
+    "pdg_rows_to_planes": (I, [P, I, I, I, P, I, I, P]),
+    "pdg_planes_to_rows": (I, [P, I, I, I, I, I, P, P]),
     "pdg_ext2d_eval": (I, [P, P, P, P, P, P, P, I, D, D, D, P, I, I, P, P, P, P]),
     "pdg_ext2d_subcycle": (I, [P, P, I, D, D, D, P, P, P, P, P, P, I, P]),
     "pdg_ext2d_cfl": (I, [P, P, D, D, P, P]),

@@ -51,7 +51,7 @@ def build(verbose=False, force=False, extra=(), out=None):
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    cmd = ["nvcc", *ARCH, "-shared", "-o", out or LIB, *objs, "-lcudart"]
+    cmd = ["nvcc", *ARCH, "-shared", "-o", out or LIB, *objs, "-lcudart", "-ldl"]
     subprocess.check_call(cmd)
     return out or LIB
 

@@ -24,6 +24,8 @@ from __future__ import annotations
 
 from types import SimpleNamespace
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -106,88 +108,134 @@ class ImexStepper:
         self.prof.setdefault(name, []).append((e0, e1))
 
     # ------------------------------------------------------------------ state I/O (reference layouts)
-    IO_CHUNKS = 8   # column chunks per prism field in the pipelined host I/O
+    IO_CHUNK_BYTES = 128 << 20   # DMA granularity of the host I/O pipeline
+    IO_SLOTS = 4                 # device staging buffers per direction
 
-    def _dests(self):
-        """(name, device planes, chunked?) of the prognostic state."""
+    def _io_plan(self):
+        """(name, device planes, L_f, nk, [(c0, c1), ...]) of the prognostic state: the column chunks
+        of every field (the same plan for uploads and downloads, so chunk events pair up)."""
+        if getattr(self, "_plan", None) is None:
+            nt, L = self.nt, self.L
+            plan = []
+            for name, lf, nk in (("eta", 1, 3), ("qx", 1, 3), ("qy", 1, 3), ("ux", L, 6), ("uy", L, 6), ("T", L, 6)):
+                n = max(1, min(nt, self.IO_CHUNK_BYTES // (lf * nk * 8)))
+                plan.append((name, lf, nk, [(c, min(nt, c + n)) for c in range(0, nt, n)]))
+            self._plan = plan
+            self._read_ev = {}       # (field, chunk) -> event: the device planes of that chunk were read out
+        return self._plan
+
+    def _planes(self, name):
         u = self.U[self.cur]
-        return [("eta", self.S[0], False), ("qx", self.S[1], False), ("qy", self.S[2], False),
-                ("ux", u[0], True), ("uy", u[1], True), ("T", self.T[self.cur], True)]
+        return {"eta": self.S[0], "qx": self.S[1], "qy": self.S[2], "ux": u[0], "uy": u[1], "T": self.T[self.cur]}[name]
 
-    def _chunks(self, chunked):
-        nt = self.nt
-        n = self.IO_CHUNKS if chunked else 1
-        b = [nt * i // n for i in range(n + 1)]
-        return [(b[i], b[i + 1]) for i in range(n) if b[i + 1] > b[i]]
+    def _io(self):
+        """upload / download streams (the two PCIe directions), the two layout-conversion streams and
+        the device staging slots of each direction."""
+        if getattr(self, "_iost", None) is None:
+            S = lambda: torch.cuda.Stream(device=self.dev)  # noqa: E731
+            w = self.IO_CHUNK_BYTES // 8
+            self._iost = SimpleNamespace(
+                up=S(), down=S(), ut=S(), dt=S(),
+                ubuf=[torch.empty(w, dtype=F64, device=self.dev) for _ in range(self.IO_SLOTS)],
+                dbuf=[torch.empty(w, dtype=F64, device=self.dev) for _ in range(self.IO_SLOTS)],
+                ufree=[None] * self.IO_SLOTS, dfree=[None] * self.IO_SLOTS, ui=0, di=0)
+        return self._iost
 
-    def _to_dev_view(self, dest, chunked, c0, c1):
-        """device planes of columns [c0, c1) and the reference-layout -> device view of a host chunk."""
-        L = self.L
-        if not chunked:
-            return dest[:, c0:c1], (lambda a: a.t())
-        return dest[:, :, c0:c1], (lambda a: a.reshape(c1 - c0, L, 6).permute(2, 1, 0))
+    @staticmethod
+    def _event(stream):
+        e = torch.cuda.Event()
+        e.record(stream)
+        return e
 
     def set_state(self, eta, qx, qy, ux, uy, T, t: float = 0.0):
         """Load a state in the reference layouts ((nt, 3) 2D fields, (P, 6) prism fields).
 
-        Host torch tensors (ideally pinned) are uploaded in column chunks on an upload stream while
-        the compute stream rearranges the previous chunk into the device layout.  A host chunk that
-        a previous get_state(out=...) is still filling is uploaded as soon as THAT chunk has arrived
-        (per-chunk events), so downloads and uploads overlap on the two PCIe directions."""
-        dev, L = self.dev, self.L
+        Host tensors (ideally pinned) stream in column chunks: each chunk is copied by DMA into a
+        device staging slot on the upload stream and rearranged into the device planes by the
+        library kernel (pdg_rows_to_planes) on a conversion stream.  A chunk that a previous
+        get_state(out=...) is still downloading into the same host memory is uploaded as soon as
+        THAT chunk has arrived, so a download and the next upload overlap on the two PCIe
+        directions.  numpy / CUDA inputs are converted directly."""
+        lb = _lib.lib()
         src = dict(eta=eta, qx=qx, qy=qy, ux=ux, uy=uy, T=T)
+        main = torch.cuda.current_stream(self.dev)
         host = all(isinstance(a, torch.Tensor) and not a.is_cuda for a in src.values())
-        main = torch.cuda.current_stream(dev)
-        up = self._io_streams()[0] if host else None
-        for name, dest, chunked in self._dests():
+        io = self._io()
+        io.ut.wait_stream(main)                  # the planes may still be read by queued work
+        for name, lf, nk, chunks in self._io_plan():
             a = src[name]
             if not host:
-                a = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64))).to(dev, F64)
-            for c0, c1 in self._chunks(chunked and host):
-                part = a[c0 * L:c1 * L] if chunked else a[c0:c1]
-                dpart, view = self._to_dev_view(dest, chunked, c0, c1)
+                a = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a, np.float64)))
+                a = a.to(self.dev, F64).contiguous()
+            else:
+                a = a.to(F64).contiguous()
+            flat = a.reshape(-1)
+            dest = self._planes(name)
+            for ci, (c0, c1) in enumerate(chunks):
+                n = (c1 - c0) * lf * nk
+                part = flat[c0 * lf * nk:c0 * lf * nk + n]
+                rev = self._read_ev.pop((name, ci), None)
                 if host:
-                    up.wait_stream(main)
+                    k = io.ui
+                    io.ui = (io.ui + 1) % self.IO_SLOTS
+                    if io.ufree[k] is not None:
+                        io.up.wait_event(io.ufree[k])
                     ev = self._pending_d2h.pop(part.data_ptr(), None)
                     if ev is not None:
-                        up.wait_event(ev)
-                    with torch.cuda.stream(up):
-                        buf = part.to(dev, F64, non_blocking=True)
-                    main.wait_stream(up)
-                    buf.record_stream(main)
+                        io.up.wait_event(ev)
+                    buf = io.ubuf[k][:n]
+                    with torch.cuda.stream(io.up):
+                        buf.copy_(part, non_blocking=True)
+                    io.ut.wait_event(self._event(io.up))
                 else:
                     buf = part
-                dpart.copy_(view(buf))
+                    io.ut.wait_stream(main)
+                if rev is not None:
+                    io.ut.wait_event(rev)
+                _lib.check(lb.pdg_rows_to_planes(ptr(buf), c1 - c0, lf, nk, ptr(dest), self.nt, c0,
+                                                 ctypes.c_void_p(io.ut.cuda_stream)), "rows_to_planes")
+                if host:
+                    io.ufree[k] = self._event(io.ut)
+                else:
+                    buf.record_stream(io.ut)
+        main.wait_stream(io.ut)
         self.t = float(t)
 
     def get_state(self, numpy=True, out=None):
-        """The state in the reference layouts.  out: dict of host tensors (pinned) to fill: the
-        device-to-host copies run on a download stream in column chunks, overlapped with the next
-        chunk's rearrangement (asynchronous: wait_io() / synchronise before reading them on the
-        host; a later set_state from the same buffers orders itself after each chunk's copy)."""
+        """The state in the reference layouts.  out: dict of host tensors (pinned) to fill: each column
+        chunk is rearranged by the library kernel (pdg_planes_to_rows) into a device staging slot
+        and copied to the host on the download stream (asynchronous: wait_io() / synchronise before
+        reading the buffers; a later set_state from the same buffers orders itself after each
+        chunk's download)."""
         nt, L = self.nt, self.L
-        u = self.U[self.cur]
         if out is not None:
-            main = torch.cuda.current_stream(self.dev)
-            down = self._io_streams()[1]
-            for name, dest, chunked in self._dests():
-                for c0, c1 in self._chunks(chunked):
-                    dpart, _ = self._to_dev_view(dest, chunked, c0, c1)
-                    if chunked:
-                        tmp = dpart.permute(2, 1, 0).reshape((c1 - c0) * L, 6)
-                        hpart = out[name][c0 * L:c1 * L]
-                    else:
-                        tmp = dpart.t().contiguous()
-                        hpart = out[name][c0:c1]
-                    down.wait_stream(main)
-                    with torch.cuda.stream(down):
-                        hpart.copy_(tmp, non_blocking=True)
-                        ev = torch.cuda.Event()
-                        ev.record(down)
-                    tmp.record_stream(down)
+            lb = _lib.lib()
+            io = self._io()
+            io.dt.wait_stream(torch.cuda.current_stream(self.dev))
+            for name, lf, nk, chunks in self._io_plan():
+                src = self._planes(name)
+                flat = out[name].reshape(-1)
+                for ci, (c0, c1) in enumerate(chunks):
+                    n = (c1 - c0) * lf * nk
+                    k = io.di
+                    io.di = (io.di + 1) % self.IO_SLOTS
+                    if io.dfree[k] is not None:
+                        io.dt.wait_event(io.dfree[k])
+                    buf = io.dbuf[k][:n]
+                    _lib.check(lb.pdg_planes_to_rows(ptr(src), nt, c0, c1 - c0, lf, nk, ptr(buf),
+                                                     ctypes.c_void_p(io.dt.cuda_stream)), "planes_to_rows")
+                    rd = self._event(io.dt)
+                    self._read_ev[(name, ci)] = rd
+                    io.down.wait_event(rd)
+                    hpart = flat[c0 * lf * nk:c0 * lf * nk + n]
+                    with torch.cuda.stream(io.down):
+                        hpart.copy_(buf, non_blocking=True)
+                    ev = self._event(io.down)
+                    io.dfree[k] = ev
                     self._pending_d2h[hpart.data_ptr()] = ev
             out["t"] = self.t
             return out
+        u = self.U[self.cur]
         res = dict(eta=c3_out(self.S[0]), qx=c3_out(self.S[1]), qy=c3_out(self.S[2]), ux=p6_out(u[0], nt, L),
                    uy=p6_out(u[1], nt, L), T=p6_out(self.T[self.cur], nt, L), t=self.t)
         if numpy:
@@ -196,15 +244,9 @@ class ImexStepper:
 
     def wait_io(self):
         """Order the current stream after every pending get_state(out=...) download."""
-        if getattr(self, "_io", None) is not None:
-            torch.cuda.current_stream(self.dev).wait_stream(self._io[1])
+        if getattr(self, "_iost", None) is not None:
+            torch.cuda.current_stream(self.dev).wait_stream(self._iost.down)
         self._pending_d2h.clear()
-
-    def _io_streams(self):
-        """(upload, download) streams: the two PCIe directions run concurrently."""
-        if getattr(self, "_io", None) is None:
-            self._io = (torch.cuda.Stream(device=self.dev), torch.cuda.Stream(device=self.dev))
-        return self._io
 
     # ------------------------------------------------------------------ one stage
     def _stage(self, s, eta_u, u, T, u0, T0, Sw, out_u, out_T, dt_s, m_s, implicit, t_wind):
@@ -303,6 +345,8 @@ class ImexStepper:
     def step(self, n: int = 1):
         """Advance n internal steps (stream ordered, no host sync)."""
         with torch.cuda.device(self.dev):
+            if getattr(self, "_iost", None) is not None:   # a pending get_state(out=...) still reads S / U
+                torch.cuda.current_stream(self.dev).wait_stream(self._iost.dt)
             for _ in range(n):
                 wind_varies = self.p.tau_x1 is not None
                 if self.use_graph and not wind_varies and self.part is None:
