@@ -164,10 +164,19 @@ int pdg_compute_w(pdg_ctx* ctx, const double* eta_g, const double* q, const doub
 /* compute_wtilde (:505-541); mis != NULL -> qbar = qb + Jz mis and its factor on the fly */
 int pdg_compute_wtilde(pdg_ctx* ctx, const double* eta_g, const double* qb, const double* fac, const double* mis,
                        double g, const int* els, int n_els, double* w, void* stream);
-/* horizontal_rhs (ncomp 2, :695-751) / tracer_horizontal_rhs (ncomp 1, :754-792), kappa = 0 */
+/* horizontal_rhs (ncomp 2, :695-751) / tracer_horizontal_rhs (ncomp 1, :754-792) without the
+ * explicit diffusion term (pdg_horizontal_diffusion adds it) */
 int pdg_horizontal_rhs(pdg_ctx* ctx, const double* eta_g, const double* u, int ncomp, const double* q_adv,
                        const double* fac, const double* r, const double* mass, double f, double rho0, int mass_terms,
                        const int* els, int n_els, double* out, void* stream);
+/* _horizontal_diffusion (:549-692; the reference raises at :665/:676, so this is the patched
+ * oracle of tests/golden/hdiff.npz): out += scale * D(f).  ncomp 2 + wall_mirror 1: momentum
+ * (kappa_h, walls mirrored); ncomp 1 + wall_mirror 0: tracer (nu_h, walls insulated).
+ * mode 0: out is the prism residual [ncomp][6][L][nt] (rows of els, else the owned columns);
+ * mode 1: out is its column sum [ncomp][3][nt] (:184-187, the F3D->2D forcing).  kh == 0: no-op. */
+int pdg_horizontal_diffusion(pdg_ctx* ctx, const double* eta_g, const double* f, int ncomp, double kh,
+                             int wall_mirror, double scale, int mode, const int* els, int n_els, double* out,
+                             void* stream);
 int pdg_mass_terms(int L, int nt, const double* mass, const double* u, const double* r, double f, double rho0,
                    double* out, void* stream);                             /* :745-750 over all rows */
 int pdg_stress_rhs(pdg_ctx* ctx, const double* ux, const double* uy, double tsx, double tsy, double cd, const int* els,

@@ -288,10 +288,113 @@ def compute_wtilde(grid, qbar, factor, els=None):
 
 # ----------------------------------------------------------------------------- horizontal RHS
 
+W1 = QW @ BARY                                           # sum_q QW BARY_i (the P1 face moments)
+
+
+def horizontal_diffusion(grid, f, kh, kv, els=None, wall_mirror=True):
+    """internal3d.py:549-692 (_horizontal_diffusion), PATCHED ORACLE: the reference raises at
+    :665 and :676 (two (n,) per-edge arrays broadcast without their trailing axes; SURVEY.md
+    section 0.3); this is the function with those broadcasts as evidently intended
+    (oracle/refops.patch_horizontal_diffusion, pinned by tests/golden/hdiff.npz).
+
+    Restated in closed form.  With gv the iso-zeta gradient at the vertical points, mid2 = -m_h Jz
+    (internal3d.py:413-421) and dz = 0.5 (f_top - f_bot) per corner:
+      volume   sum_vq QW Jz gh = gv sum QW Jz - mid2 sum QW dz against grad_h phi; the m_h parts of
+               the phi_z test (:603-611) cancel to +kh J2D DV (sum_v gv . mid2) W1
+      top/bottom faces: the -kh |grad z_f|^2 dz/Jz remainder cancels the metric part of n.D.grad
+               (:624-636), leaving -kh J2D grad_iso . grad z_f, constant over the face
+      lateral  kh Jz n.gv - kh (n.mid2) dz per side, mean of both sides, plus the interior penalty
+               sigma kh {Jz} [[f]] (:644-678); walls: the penalty on the normal velocity only when
+               wall_mirror (:679-691).
+    f: (P, 6, nc) -> (nt, L, 6, nc) residual (rows outside els zero)."""
+    cols = _cols(grid, els)
+    mesh, L = grid.mesh, grid.n_layers
+    f = np.asarray(f, dtype=float)
+    nc = f.shape[-1]
+    acc = np.zeros((mesh.nt, L, 6, nc))
+    if kh == 0.0 and kv == 0.0:
+        return acc
+    fv = _cv(f, grid)                                                   # (nt, L, 6, c)
+    dxa, dya = mesh.dphx[:, None, :, None], mesh.dphy[:, None, :, None]
+    giso = np.stack([np.stack([(fv[:, :, 3 * lev:3 * lev + 3] * dxa).sum(2),
+                               (fv[:, :, 3 * lev:3 * lev + 3] * dya).sum(2)], 2) for lev in range(2)], 2)
+    gv_all = np.einsum("vm,nlmdc->nlvdc", VS, giso)                     # (nt, L, v, d, c)
+    allc = np.arange(mesh.nt)
+    jzq_all, mid2_all, _ = _metric(grid, allc)                           # mid2: (nt, L, v, d)
+    dz_all = 0.5 * (fv[:, :, 0:3] - fv[:, :, 3:6])                     # (nt, L, 3, c)
+    j2d = mesh.j2d[cols]
+    dx, dy = mesh.dphx[cols], mesh.dphy[cols]
+    gv, mid2, jzq, dz = gv_all[cols], mid2_all[cols], jzq_all[cols], dz_all[cols]
+
+    # volume
+    A = jzq @ QW                                                        # (n, L)
+    B = np.einsum("q,qj,nljc->nlc", QW, BARY, dz)                       # (n, L, c)
+    sv = np.einsum("vm,nlvdc->nlmdc", VS, gv * A[:, :, None, None, None]
+                   - mid2[..., None] * B[:, :, None, None, :])
+    for lev in range(2):
+        for i in range(3):
+            acc[cols, :, 3 * lev + i] -= kh * j2d[:, None, None] * (dx[:, None, i, None] * sv[:, :, lev, 0]
+                                                                    + dy[:, None, i, None] * sv[:, :, lev, 1])
+    gm = np.einsum("nlvdc,nlvd->nlc", gv, mid2)
+    for lev in range(2):
+        acc[cols, :, 3 * lev:3 * lev + 3] += (kh * DV[lev]) * j2d[:, None, None, None] * W1[None, None, :, None] \
+            * gm[:, :, None, :]
+
+    # interior top / bottom faces between layers l-1 and l
+    if L > 1:
+        dzt = _cv(grid.dztop, grid)[cols][:, 1:]                         # (n, L-1, d)
+        dzb = _cv(grid.dzbot, grid)[cols][:, :-1]
+        gsi = giso[cols]
+        f_lo = -kh * np.einsum("nldc,nld->nlc", gsi[:, 1:, 0], dzt)
+        f_hi = -kh * np.einsum("nldc,nld->nlc", gsi[:, :-1, 1], dzb)
+        face = (0.5 * j2d[:, None, None] * (f_lo + f_hi))[:, :, None, :] * W1[None, None, :, None]
+        acc[cols, 1:, 0:3] += face
+        acc[cols, :-1, 3:6] -= face
+
+    # lateral faces
+    jz6 = _dup(grid.jz)
+    dz6 = np.concatenate([dz_all, dz_all], axis=2).reshape(-1, 6, nc)
+    for k in range(3):
+        tag = mesh.btag[cols, k]
+        je_all = 0.5 * mesh.elen[cols, k]
+        rows = cols[tag == 0]
+        if rows.size:
+            e2 = mesh.nbr[rows, k]
+            nx, ny = mesh.enx[rows, k], mesh.eny[rows, k]
+            jzi, jze = lat_trace(jz6, grid, rows, k, False), lat_trace(jz6, grid, rows, k, True)   # (n, L, v, h)
+            dzi, dze = lat_trace(dz6, grid, rows, k, False), lat_trace(dz6, grid, rows, k, True)   # (n, L, v, h, c)
+
+            def side(src, jt, dt):
+                ng = nx[:, None, None, None] * gv_all[src][:, :, :, 0] + ny[:, None, None, None] * gv_all[src][:, :, :, 1]
+                nm = nx[:, None, None] * mid2_all[src][..., 0] + ny[:, None, None] * mid2_all[src][..., 1]
+                # (n, L, v, h, c): kh Jz (n.gv - (n.mid2) dz / Jz(v=0))
+                return kh * jt[..., None] * (ng[:, :, :, None, :] - nm[:, :, :, None, None] * dt
+                                             / jt[:, :, :1, :, None])
+
+            mean = 0.5 * (side(rows, jzi, dzi) + side(e2, jze, dze))
+            sig = penalty_sigma(0.5 * mesh.j2d[rows] / mesh.elen[rows, k], 0.5 * mesh.j2d[e2] / mesh.elen[rows, k], 3)
+            pen = sig[:, None, None, None] * kh * 0.5 * (jzi + jze) * 0.5
+            tri, tre = lat_trace(f, grid, rows, k, False), lat_trace(f, grid, rows, k, True)
+            je = 0.5 * mesh.elen[rows, k]
+            for c in range(nc):
+                lat_gather_add(acc[..., c], rows, k, mean[..., c], je, 1.0)
+                lat_gather_add(acc[..., c], rows, k, pen * (tri[..., c] - tre[..., c]), je, -1.0)
+        wr = cols[tag != 0]
+        if wall_mirror and wr.size:
+            nx, ny = mesh.enx[wr, k], mesh.eny[wr, k]
+            tri = lat_trace(f, grid, wr, k, False)
+            jzi = lat_trace(jz6, grid, wr, k, False)
+            ln = 0.5 * mesh.j2d[wr] / mesh.elen[wr, k]
+            pen = penalty_sigma(ln, ln, 3)[:, None, None, None] * kh * jzi
+            un = nx[:, None, None, None] * tri[..., 0] + ny[:, None, None, None] * tri[..., 1]
+            je = je_all[tag != 0]
+            lat_gather_add(acc[..., 0], wr, k, pen * un * nx[:, None, None, None], je, -1.0)
+            lat_gather_add(acc[..., 1], wr, k, pen * un * ny[:, None, None, None], je, -1.0)
+    return acc
+
+
 def horizontal_rhs(grid, ux, uy, q_adv, factor, r, mass, p, els=None):
-    """internal3d.py:695-751 with kappa_h = kappa_v = 0 (the only case the reference runs)."""
-    if p.kappa_h != 0.0 or p.kappa_v != 0.0:
-        raise NotImplementedError("explicit horizontal viscosity: reference crashes (internal3d.py:665); parity unpinned")
+    """internal3d.py:695-751 (explicit viscosity: the patched horizontal_diffusion above)."""
     cols = _cols(grid, els)
     mesh, L = grid.mesh, grid.n_layers
     j2d, dx, dy = mesh.j2d[cols], mesh.dphx[cols], mesh.dphy[cols]
@@ -312,6 +415,7 @@ def horizontal_rhs(grid, ux, uy, q_adv, factor, r, mass, p, els=None):
         up = np.where(fac[..., None] >= 0.0, lat_trace(U, grid, rows, k, False), lat_trace(U, grid, rows, k, True))
         for c in range(2):
             lat_gather_add(acc[..., c], rows, k, up[..., c] * fac, 0.5 * mesh.elen[rows, k], -1.0)
+    acc += horizontal_diffusion(grid, U, p.kappa_h, p.kappa_v, els, wall_mirror=True)
     out = acc.reshape(-1, 6, 2)
     if p.f != 0.0:
         mu = mass_apply(mass, U)
@@ -322,9 +426,7 @@ def horizontal_rhs(grid, ux, uy, q_adv, factor, r, mass, p, els=None):
 
 
 def tracer_horizontal_rhs(grid, tr, qbar, factor, p, els=None):
-    """internal3d.py:754-792 with nu_h = nu_v = 0."""
-    if p.nu_h != 0.0 or p.nu_v != 0.0:
-        raise NotImplementedError("explicit horizontal diffusion: reference crashes (internal3d.py:665); parity unpinned")
+    """internal3d.py:754-792 (explicit diffusion: the patched horizontal_diffusion above)."""
     cols = _cols(grid, els)
     mesh, L = grid.mesh, grid.n_layers
     j2d, dx, dy = mesh.j2d[cols], mesh.dphx[cols], mesh.dphy[cols]
@@ -339,6 +441,7 @@ def tracer_horizontal_rhs(grid, tr, qbar, factor, p, els=None):
         fac = factor[rows, :, k]
         up = np.where(fac >= 0.0, lat_trace(tr, grid, rows, k, False), lat_trace(tr, grid, rows, k, True))
         lat_gather_add(acc, rows, k, up * fac, 0.5 * mesh.elen[rows, k], -1.0)
+    acc += horizontal_diffusion(grid, np.asarray(tr)[..., None], p.nu_h, p.nu_v, els, wall_mirror=False)[..., 0]
     return acc.reshape(-1, 6)
 
 

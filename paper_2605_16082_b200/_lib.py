@@ -68,6 +68,7 @@ _SIGS = {
     "pdg_compute_w": (I, [P, P, P, P, P, P, P, I, P, P]),
     "pdg_compute_wtilde": (I, [P, P, P, P, P, D, P, I, P, P]),
     "pdg_horizontal_rhs": (I, [P, P, P, I, P, P, P, P, D, D, I, P, I, P, P]),
+    "pdg_horizontal_diffusion": (I, [P, P, P, I, D, I, D, I, P, I, P, P]),
     "pdg_mass_terms": (I, [I, I, P, P, P, D, D, P, P]),
     "pdg_stress_rhs": (I, [P, P, P, D, D, D, P, I, P, P]),
     "pdg_step_f3d2d": (I, [P, P, P, P, P, D, D, D, D, D, D, P, P]),

@@ -5,10 +5,12 @@ numpy out (parity path), torch CUDA in -> torch CUDA out.  Every assembly is
 one thread-per-column kernel in csrc/int3d.cu / csrc/columns.cu; the grid's
 prism geometry is rebuilt on device from (grid.eta, mesh.b, sigma fractions).
 
-Explicit horizontal viscosity / diffusivity (kappa_h, kappa_v, nu_h, nu_v != 0)
-raises NotImplementedError: the reference crashes in that branch
-(internal3d.py:665), so there is nothing to be parity
-with.  Vertical diffusion (assemble_vertical_operator's kh / kv) is complete.
+Explicit horizontal viscosity / diffusivity (kappa_h, nu_h != 0) is the
+"patched oracle" of _horizontal_diffusion (internal3d.py:549-692): the reference
+raises at internal3d.py:665 / :676 for every mesh (two per-edge broadcasts miss
+an axis); with those fixed (oracle/refops.py) its output
+is tests/golden/hdiff.npz, which csrc/hdiff.cu matches.  Vertical diffusion
+(assemble_vertical_operator's kh / kv) is the reference's own.
 """
 from __future__ import annotations
 
@@ -60,10 +62,13 @@ def _zeros(*shape, dev):
     return torch.zeros(shape, dtype=F64, device=dev)
 
 
-def _no_explicit_diffusion(kh, kv, what):
-    if kh != 0.0 or kv != 0.0:
-        raise NotImplementedError(f"{what}: explicit horizontal viscosity/diffusion is not parity-pinned "
-                                  "(the reference crashes at internal3d.py:665)")
+def _add_diffusion(dm, eta, f, nc, kh, el, out, scale=1.0, mode=0):
+    """out += scale * _horizontal_diffusion(f) (internal3d.py:549-692, patched; csrc/hdiff.cu).
+    Every term carries kh, so kh == 0 adds nothing (the reference returns zeros when kh == kv == 0)."""
+    if kh != 0.0:
+        _lib.check(_lib.lib().pdg_horizontal_diffusion(dm.h, ptr(eta), ptr(f), nc, float(kh), int(nc == 2),
+                                                       float(scale), mode, ptr(el), _nsel(dm, el), ptr(out),
+                                                       stream_ptr()), "horizontal_diffusion")
 
 
 # ----------------------------------------------------------------------------- mass
@@ -262,7 +267,6 @@ def compute_wtilde(grid, qbar, factor, els=None):
 
 def horizontal_rhs(grid, ux, uy, q_adv, factor, r, mass, params: PhysParams, els=None):
     """Explicit horizontal momentum forcing (P, 6, 2) (internal3d.py:695-751)."""
-    _no_explicit_diffusion(params.kappa_h, params.kappa_v, "horizontal_rhs")
     dm = _dm(grid)
     dev, nt, L = dm.device, dm.nt, dm.L
     A = Arr()
@@ -278,6 +282,7 @@ def horizontal_rhs(grid, ux, uy, q_adv, factor, r, mass, params: PhysParams, els
         _lib.check(lb.pdg_horizontal_rhs(dm.h, ptr(_eta(grid, A, dev)), ptr(u), 2, ptr(qd), ptr(fac), ptr(rd), ptr(md),
                                          params.f, params.rho0, int(el is None), ptr(el), _nsel(dm, el), ptr(out), s),
                    "horizontal_rhs")
+        _add_diffusion(dm, _eta(grid, A, dev), u, 2, params.kappa_h, el, out)
         if el is not None:   # the reference adds Coriolis and -M r / rho0 to ALL rows (internal3d.py:745-750)
             _lib.check(lb.pdg_mass_terms(L, nt, ptr(md), ptr(u), ptr(rd), params.f, params.rho0, ptr(out), s),
                        "mass_terms")
@@ -286,7 +291,6 @@ def horizontal_rhs(grid, ux, uy, q_adv, factor, r, mass, params: PhysParams, els
 
 def tracer_horizontal_rhs(grid, tr, qbar, factor, params: PhysParams, els=None):
     """Explicit horizontal tracer forcing (P, 6) (internal3d.py:754-792)."""
-    _no_explicit_diffusion(params.nu_h, params.nu_v, "tracer_horizontal_rhs")
     dm = _dm(grid)
     dev, nt, L = dm.device, dm.nt, dm.L
     A = Arr()
@@ -299,6 +303,8 @@ def tracer_horizontal_rhs(grid, tr, qbar, factor, params: PhysParams, els=None):
         _lib.check(_lib.lib().pdg_horizontal_rhs(dm.h, ptr(_eta(grid, A, dev)), ptr(t), 1, ptr(qd), ptr(fac), None,
                                                  None, 0.0, 1.0, 0, ptr(el), _nsel(dm, el), ptr(out), stream_ptr()),
                    "tracer_horizontal_rhs")
+        _add_diffusion(dm, _eta(grid, A, dev), t, 1, params.nu_h, el, out)
+        dm.raise_errors()
         return A.out(p6_out(out, nt, L))
 
 

@@ -43,10 +43,6 @@ class ImexStepper:
                  pen: PenaltyParams = PenaltyParams(), device=None, part=None):
         if m % 2:
             raise ValueError("m must be even (stage 1 uses m/2 substeps)")
-        if params.kappa_h or params.kappa_v or params.nu_h or params.nu_v:
-            raise NotImplementedError("explicit horizontal viscosity/diffusion (PhysParams kappa_*, nu_*) is not "
-                                      "parity-pinned: the reference crashes there (internal3d.py:665); vertical "
-                                      "diffusion is set by kv / nu_v")
         self.mesh, self.L, self.p = mesh, L, params
         self.dt, self.m, self.kv, self.nu_v, self.pen = float(dt), int(m), float(kv), float(nu_v), pen
         self.part = part          # partition.Part when this stepper owns only part of the columns
@@ -265,6 +261,9 @@ class ImexStepper:
             yield ("all", [self.q])
         tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
+        if p.kappa_h:   # explicit horizontal viscosity in horizontal_rhs: its column sum (csrc/hdiff.cu)
+            tm("hdiff_f3d2d", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(u), 2, p.kappa_h, 1, 1.0, 1, None, 0,
+               ptr(self.f3d2d), s)
         if part:
             yield ("deep", [self.f3d2d])   # the ring columns' RK stages need their forcing
         Sw.copy_(self.S)
@@ -303,6 +302,12 @@ class ImexStepper:
                ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s)
             tm("rhs_T", lb.pdg_step_rhs, h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q),
                ptr(self.mis), None, None, p.g, p.f, p.rho0, 0.0, 0.0, 0.0, dt_s, ptr(out_T), s)
+        if p.kappa_h:   # + dt D_u(u) (horizontal_rhs, internal3d.py:743) and + dt D_T(T) (:788)
+            tm("hdiff_u", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(u), 2, p.kappa_h, 1, dt_s, 0, None, 0,
+               ptr(out_u), s)
+        if p.nu_h:
+            tm("hdiff_T", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(T), 1, p.nu_h, 0, dt_s, 0, None, 0,
+               ptr(out_T), s)
         pe = self.pen
         if not implicit and self.fuse_vexpl:
             tm("vertical_uT_expl", lb.pdg_step_vertical_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt),
