@@ -274,6 +274,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--backend", default="nccl", help="process group for N>1 (gloo: host-staged halos, testing)")
+    ap.add_argument("--halo", default="capi", choices=["capi", "torch"],
+                    help="N>1 halo transport: the library's NCCL plans (graph-captured step) or torch.distributed")
+    ap.add_argument("--phase-csv", default=None, help="append step,rank,phase,micros rows of one eager step")
     ap.add_argument("--dump", default=None, help="write the final local state to this .npz (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -297,7 +300,7 @@ def main():
             dist.init_process_group("gloo")
 
     from paper_2605_16082_b200 import stepper as S
-    from paper_2605_16082_b200.partition import PartitionedRun
+    from paper_2605_16082_b200.partition import PAPER_EXCHANGES_PER_STEP, PartitionedRun, exchanges_per_step
     from paper_2605_16082_b200.scenarios import device_state_c4, make_case
 
     t_setup = time.perf_counter()
@@ -308,7 +311,8 @@ def main():
     else:
         # strong scaling: the one C4 mesh split into `world` Hilbert ranges, halos over NCCL
         run = PartitionedRun(case.mesh, case.L, case.params, case.dt, case.m, case.kv, case.nu_v, world,
-                             transport="dist", rank=rank, device=local)
+                             transport=("nccl" if args.backend == "nccl" and args.halo == "capi" else "dist"),
+                             rank=rank, device=local)
         st = run.st[rank]
         stepper = run
     if args.config == "c4":
@@ -355,6 +359,11 @@ def main():
     prof = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in st.prof.items()}
     counts = {k: len(v) / args.steps for k, v in st.prof.items()}
     st.prof = None
+    if args.phase_csv:   # SPEC.md:616 phase timings (step,rank,phase,micros) of one eager step per rank
+        st.phase_trace = []
+        stepper.step(1)
+        st.phase_csv(args.phase_csv + (f".{rank}" if world > 1 else ""), step=0)
+        st.phase_trace = None
     st.use_graph = True
     step_sum = sum(prof[k] * counts[k] for k in prof)
     hbm, peak_kind = peaks()
@@ -460,11 +469,16 @@ def main():
                "config": {"workload": f"{args.config}: {case.mesh.nt} tri x {case.L} layers = {P} prisms, "
                                       f"m={case.m}, dt2d={case.dt2d} s, momentum+tracer, FP64",
                           "nt": case.mesh.nt, "L": case.L, "m": case.m, "prism_dof_per_step": dof_per_step,
-                          "parallelism": (f"column partition x{world} (Hilbert ranges, one-ring ghosts, "
-                                          f"{'NCCL' if args.backend == 'nccl' else 'gloo host-staged'} halo "
-                                          "send/recv, 2D halos overlapped with interior columns)")
+                          "parallelism": (f"column partition x{world} (Hilbert ranges, 3 ghost rings, "
+                                          + ("library NCCL halo plans, one CUDA graph per rank and step"
+                                             if args.backend == "nccl" and args.halo == "capi" else
+                                             f"{'NCCL' if args.backend == 'nccl' else 'gloo host-staged'} "
+                                             "torch.distributed send/recv, eager")
+                                          + ", 2D halos overlapped with interior columns)")
                           if world > 1 else "single GPU",
-                          "l2": "inputs larger than L2 (~48 GB resident fields)"},
+                          "l2": "inputs larger than L2 (~48 GB resident fields)",
+                          "halo_exchanges_per_step": (exchanges_per_step(case.m) if world > 1 else 0),
+                          "paper_exchanges_per_step": PAPER_EXCHANGES_PER_STEP},
                "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
                "kernels": {k: {"ms": round(v["ms"], 4), "share": round(v["share"], 4),

@@ -253,27 +253,161 @@ class DistHalo:
 
 
 class VirtualGroup:
-    """P ranks in one process on one device: halo messages are device-to-device copies."""
+    """P ranks in one process on one device: halo messages are device-to-device copies (pack into a
+    message buffer, unpack on the receiving rank).  Buffers are allocated once per message shape,
+    so an exchange is allocation-free and stream ordered: a whole P-rank step can be one graph."""
+
+    capturable = True
 
     def __init__(self, parts, nts, device):
         self.maps = {d: [_Maps(p, device, d) for p in parts] for d in (True, False)}
         self.nts = nts
         self.device = device
         self.exchanges = 0
+        self._bufs = {}
+
+    def _buffers(self, deep, tots):
+        import torch
+        key = (deep, tuple(tots))
+        bufs = self._bufs.get(key)
+        if bufs is None:
+            bufs = {(r, peer): torch.empty(tots[r] * idx.numel(), dtype=torch.float64, device=self.device)
+                    for r, mp in enumerate(self.maps[deep]) for peer, idx in mp.send.items()}
+            self._bufs[key] = bufs
+        return bufs
 
     def exchange_all(self, fields_per_rank, deep=False):
-        import torch
-        msgs = {}
         maps = self.maps[deep]
+        tots = [sum(f.numel() // self.nts[r] for f in fields) for r, fields in enumerate(fields_per_rank)]
+        msgs = self._buffers(deep, tots)
         for r, (mp, fields) in enumerate(zip(maps, fields_per_rank)):
-            tot = sum(f.numel() // self.nts[r] for f in fields)
             for peer, idx in mp.send.items():
-                buf = torch.empty(tot * idx.numel(), dtype=torch.float64, device=self.device)
-                _pack(fields, self.nts[r], idx, buf)
-                msgs[(r, peer)] = buf
+                _pack(fields, self.nts[r], idx, msgs[(r, peer)])
         for r, (mp, fields) in enumerate(zip(maps, fields_per_rank)):
             for peer, idx in mp.recv.items():
                 _unpack(fields, self.nts[r], idx, msgs[(peer, r)])
+        self.exchanges += 1
+
+
+# ----------------------------------------------------------------------------- NCCL through the C ABI
+
+_NCCL = {}
+
+
+def nccl_library_path():
+    """The libnccl the process already uses (torch's), so one process never holds two NCCLs."""
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                if "libnccl.so" in line:
+                    return line.split()[-1]
+    except OSError:
+        pass
+    import os
+    try:
+        import nvidia.nccl
+        base = os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            return cand
+    except ImportError:
+        pass
+    return "libnccl.so.2"
+
+
+def nccl_comm(rank: int, nranks: int, device: int):
+    """This process's pdg_comm (csrc/comm.cu), created once: rank 0 draws the NCCL unique id and
+    torch.distributed broadcasts it (nranks == 1 needs no process group)."""
+    import ctypes
+    from . import _lib
+    key = (rank, nranks, device)
+    if key in _NCCL:
+        return _NCCL[key]
+    lb = _lib.lib()
+    if lb.pdg_comm_load(nccl_library_path().encode()) != 0:
+        raise RuntimeError("pdg_comm_load: " + lb.pdg_comm_error_string().decode())
+    uid = (ctypes.c_char * 128)()
+    if rank == 0 and lb.pdg_comm_unique_id(uid) != 0:
+        raise RuntimeError("pdg_comm_unique_id: " + lb.pdg_comm_error_string().decode())
+    if nranks > 1:
+        import torch.distributed as dist
+        obj = [bytes(uid) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctypes.memmove(uid, obj[0], 128)
+    h = ctypes.c_void_p()
+    if lb.pdg_comm_init(uid, rank, nranks, device, ctypes.byref(h)) != 0:
+        raise RuntimeError("pdg_comm_init: " + lb.pdg_comm_error_string().decode())
+    _NCCL[key] = h
+    return h
+
+
+class NcclHalo:
+    """One rank's halo exchange through the library (csrc/comm.cu):
+    start = pack kernels + grouped ncclSend / ncclRecv on a communication stream, finish = stream
+    wait + unpack.  No host synchronisation and no allocation after the plans are built, so the
+    partitioned step (2D exchanges once per substep, boundary-first) is captured in one CUDA graph
+    per rank like the single-GPU step."""
+
+    capturable = True
+
+    def __init__(self, part: Part, nt_local: int, device, L: int, comm=None, peers_of=None):
+        import ctypes
+        from . import _lib
+        self.part, self.nt, self.device = part, nt_local, device
+        self.exchanges = 0
+        self.comm = comm if comm is not None else nccl_comm(part.rank, part.nparts, device.index or 0)
+        lb = _lib.lib()
+        self._keep = []
+        self.plans = {}
+        # ring-1 messages carry at most u and T (18 L planes per column); deep ones the 2D state (9)
+        for deep, maxp in ((True, 9), (False, 18 * L)):
+            snd, rcv = (part.send, part.recv) if deep else (part.send1, part.recv1)
+            peers = sorted(set(snd) | set(rcv))
+            arrs = []
+            for d in (snd, rcv):
+                lists = [np.ascontiguousarray(d.get(q, np.zeros(0, np.int32)), dtype=np.int32) for q in peers]
+                arrs.append(lists)
+            self._keep.append(arrs)
+            n = len(peers)
+            IntArr = ctypes.c_int * max(n, 1)
+            PtrArr = ctypes.POINTER(ctypes.c_int) * max(n, 1)
+            sp = PtrArr(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_int)) for a in arrs[0]])
+            rp = PtrArr(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_int)) for a in arrs[1]])
+            h = ctypes.c_void_p()
+            _lib.check(lb.pdg_halo_plan_create(self.comm, nt_local, n, IntArr(*peers),
+                                               IntArr(*[a.size for a in arrs[0]]), sp,
+                                               IntArr(*[a.size for a in arrs[1]]), rp, maxp, ctypes.byref(h)),
+                       "pdg_halo_plan_create")
+            self.plans[deep] = h
+        self._args = {}
+
+    def _fields(self, fields):
+        import ctypes
+        key = tuple((f.data_ptr(), f.numel()) for f in fields)
+        a = self._args.get(key)
+        if a is None:
+            a = ((ctypes.c_void_p * len(fields))(*[f.data_ptr() for f in fields]),
+                 (ctypes.c_longlong * len(fields))(*[f.numel() // self.nt for f in fields]))
+            self._args[key] = a
+        return a
+
+    def exchange(self, fields, deep=False):
+        self.start(fields, deep)
+        self.finish(fields, deep)
+
+    def start(self, fields, deep=True):
+        from . import _lib
+        from .device import stream_ptr
+        fp, npl = self._fields(fields)
+        rc = _lib.lib().pdg_halo_start(self.plans[deep], len(fields), fp, npl, stream_ptr())
+        if rc != 0:
+            raise RuntimeError("pdg_halo_start: " + _lib.lib().pdg_comm_error_string().decode())
+
+    def finish(self, fields, deep=True):
+        from . import _lib
+        from .device import stream_ptr
+        fp, npl = self._fields(fields)
+        _lib.check(_lib.lib().pdg_halo_finish(self.plans[deep], len(fields), fp, npl, stream_ptr()), "halo_finish")
         self.exchanges += 1
 
 
@@ -297,9 +431,27 @@ class PartitionedRun:
                    for r in ranks}
         if transport == "virtual":
             self.group = VirtualGroup(self.parts, [lm.nt for lm in self.local], dev)
-        else:
+        elif transport == "nccl":    # the library's NCCL halo plans (csrc/comm.cu): graph-captured steps
+            self.group = None
+            self.st[rank].halo = NcclHalo(self.parts[rank], self.local[rank].nt, dev, L)
+        else:                        # torch.distributed send / recv (gloo tests, un-graphed)
             self.group = None
             self.st[rank].halo = DistHalo(self.parts[rank], self.local[rank].nt, dev)
+        self.use_graph = True
+        self.graphs = {}
+        self.dev = dev
+        self._skip_exchanges = set()   # tests only: exchange names to leave out (a broken schedule)
+
+    @property
+    def schedule_check(self) -> bool:
+        """Debug mode: ghost slots are poisoned (NaN) while their exchange is pending
+        and every eager step ends with ScheduleViolation if a poisoned value reached an owned one."""
+        return any(st.schedule_check for st in self.st.values())
+
+    @schedule_check.setter
+    def schedule_check(self, on: bool):
+        for st in self.st.values():
+            st.schedule_check = bool(on)
 
     def set_state(self, eta, qx, qy, ux, uy, T, t=0.0):
         L = self.L
@@ -325,35 +477,120 @@ class PartitionedRun:
             out["t"] = s["t"]
         return out
 
-    def step(self, n=1):
+    def _lockstep(self):
+        """One step of every virtual rank: the ranks' step generators advance together and every
+        exchange point is one VirtualGroup exchange (the 'start' of a boundary-first exchange is
+        a no-op on one device: the copies happen at its 'finish', after the interior work)."""
+        gens = {r: st._step_gen(st.t) for r, st in self.st.items()}
+        while True:
+            fields, phases, done = [], set(), 0
+            for r in self.ranks:          # every rank runs the same phase, then one exchange
+                try:
+                    ph, f, name = next(gens[r])
+                    phases.add((ph, name))
+                    fields.append(f)
+                except StopIteration:
+                    done += 1
+            if done:
+                if done != len(self.ranks):
+                    raise MapMismatch("ranks reached different exchange points")
+                break
+            if len(phases) != 1:
+                raise MapMismatch(f"ranks at different exchange phases {phases}")
+            ph, name = phases.pop()
+            if name in self._skip_exchanges:      # tests: a deliberately broken schedule
+                continue
+            if ph != "start":
+                self.group.exchange_all(fields, deep=ph in ("finish", "deep"))
+
+    def _capture(self, key):
+        """One CUDA graph of the whole P-rank lockstep step (the stepper's capture recipe)."""
+        import gc
+
         import torch
+        side = torch.cuda.Stream(device=self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        saved = {r: st.S.clone() for r, st in self.st.items()}
+        n_before = self.group.exchanges
+        with torch.cuda.stream(side):
+            self._lockstep()                       # sizes workspaces and message buffers
+            for r, st in self.st.items():
+                st.S.copy_(saved[r])
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        gc.collect()
+        gcflag = gc.isenabled()
+        gc.disable()
+        try:
+            n0 = self.group.exchanges
+            with torch.cuda.graph(g):
+                self._lockstep()
+            self._graph_exchanges = self.group.exchanges - n0
+            self.group.exchanges = n_before      # warm-up and recording moved nothing: replays count
+        finally:
+            if gcflag:
+                gc.enable()
+        self.graphs[key] = g
+        return g
+
+    def step(self, n=1):
+        if self.group is None:            # one rank of a multi-process job: its stepper drives the halo
+            for st in self.st.values():
+                st.step(n)
+            return
         for _ in range(n):
-            if self.group is not None:
-                gens = {r: st._step_gen(st.t) for r, st in self.st.items()}
-                while True:
-                    fields, phases, done = [], set(), 0
-                    for r in self.ranks:          # every rank runs the same phase, then one exchange
-                        try:
-                            ph, f = next(gens[r])
-                            phases.add(ph)
-                            fields.append(f)
-                        except StopIteration:
-                            done += 1
-                    if done:
-                        if done != len(self.ranks):
-                            raise MapMismatch("ranks reached different exchange points")
-                        break
-                    if len(phases) != 1:
-                        raise MapMismatch(f"ranks at different exchange phases {phases}")
-                    ph = phases.pop()
-                    if ph != "start":             # one device: the copies happen at "finish"
-                        self.group.exchange_all(fields, deep=ph in ("finish", "deep"))
+            varies = any(st.p.tau_x1 is not None for st in self.st.values())
+            if self.use_graph and not varies and not self.schedule_check:
+                key = next(iter(self.st.values())).cur
+                g = self.graphs.get(key)
+                if g is None:
+                    g = self._capture(key)
+                g.replay()
+                self.group.exchanges += self._graph_exchanges
             else:
-                for st in self.st.values():
-                    st._launch_step(st.t)
+                self._lockstep()
             for st in self.st.values():
                 st._advance()
+            if self.schedule_check:
+                for st in self.st.values():
+                    st.check_schedule()
 
     def check(self):
         for st in self.st.values():
             st.check()
+
+
+# ----------------------------------------------------------------------------- scaling plumbing
+
+PAPER_EXCHANGES_PER_STEP = 100    # PAPER.md section 4.2: "approximately 100 halo exchanges" at m = 20
+
+
+def exchanges_per_step(m: int) -> int:
+    """Halo exchanges of one partitioned internal step, derived from the step plan (stepper._stage):
+    per stage q, F3D->2D (all rings), mis and (u, T); per external substep one exchange of the 2D
+    state over all ghost rings (three rings: the RK stages run on owned + rings 1-2 / 1 / 0).
+    m = 20 -> 2 x 4 + 10 + 20 = 38 (the paper's one-ring scheme: ~100)."""
+    return 2 * 4 + m // 2 + m
+
+
+def amdahl_report(times: dict, path: str | None = None) -> dict:
+    """Least-squares fit T(P) = a + b / P over a rank-count sweep: a is the serial /
+    latency share, b the parallel work.  times: {P: seconds per step} (>= 2 rank counts).  Writes
+    P,T,T_fit,a,b,r2 rows to `path` when given; returns {"a", "b", "r2", "rows"}."""
+    P = np.asarray(sorted(times), dtype=float)
+    if P.size < 2:
+        raise ValueError("amdahl_report needs >= 2 rank counts")
+    T = np.asarray([times[int(p)] if int(p) in times else times[p] for p in sorted(times)], dtype=float)
+    X = np.stack([np.ones_like(P), 1.0 / P], axis=1)
+    (a, b), *_ = np.linalg.lstsq(X, T, rcond=None)
+    fit = a + b / P
+    ss_res = float(((T - fit) ** 2).sum())
+    ss_tot = float(((T - T.mean()) ** 2).sum())
+    r2 = 1.0 - ss_res / ss_tot if ss_tot > 0 else (1.0 if ss_res <= 1e-30 else 0.0)
+    rows = [(int(p), float(t), float(f)) for p, t, f in zip(P, T, fit)]
+    if path is not None:
+        with open(path, "w") as fh:
+            fh.write("P,T,T_fit,a,b,r2\n")
+            for p, t, f in rows:
+                fh.write(f"{p},{t!r},{f!r},{float(a)!r},{float(b)!r},{r2!r}\n")
+    return {"a": float(a), "b": float(b), "r2": r2, "rows": rows}

@@ -88,6 +88,9 @@ class ImexStepper:
         self.fuse_rhs = True   # momentum + tracer stage right-hand sides in one kernel
         self.fuse_vexpl = False  # momentum + tracer explicit vertical in one kernel (slower: register spills)
         self._pending_d2h = {}   # host buffer address -> event of the download filling it
+        self.schedule_check = False  # debug: poison in-flight ghost slots (partitioned runs)
+        self._skip_exchanges = set()  # tests only: exchange names to leave out (a broken schedule)
+        self.phase_trace = None      # list -> per-phase CUDA events of eager steps (phase_csv)
 
     def _c(self, name, rc):
         _lib.check(rc, name)
@@ -254,18 +257,21 @@ class ImexStepper:
         eta0 = self.S[0]
         tsx, tsy = p.wind(t_wind)
         tag = "impl" if implicit else "expl"
+        if part:   # debug: ghosts of the fields this stage produces stay NaN until their exchange lands
+            self._poison([self.q, self.mis, out_u, out_T], False)
+            self._poison([self.f3d2d], True)
         tm("r", lb.pdg_compute_r, h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s)
         tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
            ptr(self.qsum), ptr(self.htot), s)
         if part:
-            yield ("all", [self.q])
+            yield ("all", [self.q], "q")
         tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
         if p.kappa_h:   # explicit horizontal viscosity in horizontal_rhs: its column sum (csrc/hdiff.cu)
             tm("hdiff_f3d2d", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(u), 2, p.kappa_h, 1, 1.0, 1, None, 0,
                ptr(self.f3d2d), s)
         if part:
-            yield ("deep", [self.f3d2d])   # the ring columns' RK stages need their forcing
+            yield ("deep", [self.f3d2d], "f3d2d")   # the ring columns' RK stages need their forcing
         Sw.copy_(self.S)
         dt2 = dt_s / m_s
         if not part:
@@ -281,16 +287,17 @@ class ImexStepper:
                        ptr(self.f3d2d), ptr(self.qbar), ptr(cols), cols.numel(), s)
                 tm("rk2", lb.pdg_ext2d_rk_stage_cols, h, 2, ptr(W2), ptr(Sw), ptr(Sw), dt2, p.g, p.rho0,
                    ptr(self.f3d2d), ptr(self.qbar), ptr(bnd), bnd.numel(), s)
-                yield ("start", [Sw])
+                self._poison([Sw], True)      # in flight: the interior stage must not read ghosts
+                yield ("start", [Sw], "state2d")
                 tm("rk2", lb.pdg_ext2d_rk_stage_cols, h, 2, ptr(W2), ptr(Sw), ptr(Sw), dt2, p.g, p.rho0,
                    ptr(self.f3d2d), ptr(self.qbar), ptr(intr), intr.numel(), s)
-                yield ("finish", [Sw])
+                yield ("finish", [Sw], "state2d")
             tm("sub_end", lb.pdg_ext2d_subcycle_end, h, ptr(Sw), ptr(self.f3d2d), m_s, dt2, ptr(self.qbar),
                ptr(self.f2d), s)
         eta1 = Sw[0]
         tm("mismatch", lb.pdg_mismatch, h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s)
         if part:
-            yield ("all", [self.mis])
+            yield ("all", [self.mis], "mis")
         tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
            ptr(self.wt), s)
         if self.fuse_rhs:
@@ -314,14 +321,14 @@ class ImexStepper:
                p.kappa_h, self.kv, p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u),
                ptr(out_T), ptr(T), ptr(out_T), s)
             if part:
-                yield ("all", [out_u, out_T])
+                yield ("all", [out_u, out_T], "uT")
             return eta1
         tm(f"vertical_u_{tag}", lb.pdg_step_vertical, h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
         tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
         if part:
-            yield ("all", [out_u, out_T])
+            yield ("all", [out_u, out_T], "uT")
         return eta1
 
     def _step_gen(self, t0):
@@ -335,13 +342,89 @@ class ImexStepper:
         self.S.copy_(self.Sw[1])
 
     def _launch_step(self, t0):
-        for phase, fields in self._step_gen(t0):
-            if phase in ("all", "deep"):
+        tr = self.phase_trace
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if tr is not None else None
+        last = None
+        if tr is not None:
+            last = ev()
+            last.record()
+        for phase, fields, name in self._step_gen(t0):
+            if tr is not None:     # compute since the previous exchange point, then the exchange call
+                e = ev()
+                e.record()
+                seg = {"start": "boundary", "finish": "interior"}.get(phase, "compute")
+                tr.append((f"{seg}:{name}", last, e))
+                last = e
+            if name in self._skip_exchanges:          # tests: a deliberately broken schedule
+                pass
+            elif phase in ("all", "deep"):
                 self.halo.exchange(fields, deep=phase == "deep")
             elif phase == "start":
                 self.halo.start(fields, True)
             else:
                 self.halo.finish(fields, True)
+            if tr is not None:
+                e = ev()
+                e.record()
+                tr.append(({"start": "pack+post", "finish": "join+unpack"}.get(phase, "exchange") + f":{name}", last,
+                           e))
+                last = e
+        if tr is not None:
+            e = ev()
+            e.record()
+            tr.append(("compute:tail", last, e))
+
+    # ------------------------------------------------------------------ schedule checking (debug)
+    def _poison(self, fields, deep):
+        """schedule_check: fill the ghost slots a pending exchange will refresh with NaN, so a kernel
+        that reads them before the exchange joins produces non-finite owned values."""
+        if not (self.schedule_check and self.part is not None):
+            return
+        idx = self._ghost_slots(deep)
+        if idx.numel() == 0:
+            return
+        lb = _lib.lib()
+        for f in fields:
+            npl = f.numel() // self.nt
+            need = npl * idx.numel()
+            if getattr(self, "_nan", None) is None or self._nan.numel() < need:
+                self._nan = torch.full((need,), float("nan"), dtype=F64, device=self.dev)
+            _lib.check(lb.pdg_halo_unpack(ptr(self._nan), npl, self.nt, ptr(idx), idx.numel(), ptr(f), stream_ptr()),
+                       "poison")
+
+    def _ghost_slots(self, deep):
+        key = "_gs_deep" if deep else "_gs_ring1"
+        if getattr(self, key, None) is None:
+            rv = self.part.recv if deep else self.part.recv1
+            arr = np.concatenate([np.asarray(v, np.int32) for _, v in sorted(rv.items())]) if rv else \
+                np.zeros(0, np.int32)
+            setattr(self, key, torch.as_tensor(arr, device=self.dev))
+        return getattr(self, key)
+
+    def check_schedule(self):
+        """schedule_check: raise ScheduleViolation if a poisoned ghost reached an owned value."""
+        from .errors import ScheduleViolation
+        n = self.part.n_own if self.part is not None else self.nt
+        bad = [k for k, f in (("eta/qx/qy", self.S[..., :n]), ("u", self.U[self.cur][..., :n]),
+                              ("T", self.T[self.cur][..., :n])) if not bool(torch.isfinite(f).all())]
+        if bad:
+            r = self.part.rank if self.part is not None else 0
+            raise ScheduleViolation(f"rank {r}: owned {', '.join(bad)} read a ghost slot before its exchange joined "
+                                    f"(step ending t={self.t})")
+
+    def phase_csv(self, path, step: int, rank: int | None = None):
+        """Append this step's phases (phase_trace = [] before the step; eager stepping) as SPEC.md:616
+        rows step,rank,phase,micros (CUDA events on the launching stream)."""
+        import os
+        torch.cuda.synchronize(self.dev)
+        r = (self.part.rank if self.part is not None else 0) if rank is None else rank
+        new = not os.path.exists(path)
+        with open(path, "a") as f:
+            if new:
+                f.write("step,rank,phase,micros\n")
+            for name, a, b in self.phase_trace or []:
+                f.write(f"{step},{r},{name},{a.elapsed_time(b) * 1e3:.3f}\n")
+        self.phase_trace = []
 
     def _advance(self):
         self.cur = (self.cur + 2) % 3
@@ -354,7 +437,8 @@ class ImexStepper:
                 torch.cuda.current_stream(self.dev).wait_stream(self._iost.dt)
             for _ in range(n):
                 wind_varies = self.p.tau_x1 is not None
-                if self.use_graph and not wind_varies and self.part is None:
+                capturable = self.part is None or getattr(self.halo, "capturable", False)
+                if self.use_graph and not wind_varies and capturable and not self.schedule_check:
                     g = self.graphs.get(self.cur)
                     if g is None:
                         g = self._capture()
@@ -362,6 +446,8 @@ class ImexStepper:
                 else:
                     self._launch_step(self.t)
                 self._advance()
+                if self.schedule_check:
+                    self.check_schedule()
 
     def _capture(self):
         # warm the workspace (block-Thomas scratch is sized on first use), then capture

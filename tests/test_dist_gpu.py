@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _run(tmp, nproc):
     out = os.path.join(tmp, f"s{nproc}")
     base = [sys.executable, "bench.py", "--config", "c3", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e",
-            "--dump", out]
+            "--dump", out, "--phase-csv", out + ".phases.csv"]
     if nproc == 1:
         cmd = base
     else:
@@ -39,3 +39,11 @@ def test_two_process_partition_matches_single(tmp_path):
         a = p1[0][k]
         b = np.concatenate([p[k] for p in p2])   # rank ranges are contiguous and ascending
         assert np.array_equal(a, b), k
+    # SPEC.md:616 phase timings of every rank: step,rank,phase,micros with the boundary-first phases
+    for r in range(2):
+        rows = open(os.path.join(str(tmp_path), f"s2.phases.csv.{r}")).read().splitlines()
+        assert rows[0] == "step,rank,phase,micros"
+        names = {x.split(",")[2] for x in rows[1:]}
+        assert {"boundary:state2d", "pack+post:state2d", "interior:state2d", "join+unpack:state2d",
+                "exchange:q", "exchange:uT"} <= names, names
+        assert all(float(x.split(",")[3]) >= 0.0 and x.split(",")[1] == str(r) for x in rows[1:])

@@ -127,3 +127,21 @@ def test_gloo_halo_exchange_world2():
     ret = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), 12, 8, ret), nprocs=world, join=True)
     assert ret[0] and ret[1]
+
+
+def test_amdahl_report_exact_fit(tmp_path):
+    from paper_2605_16082_b200.partition import amdahl_report
+    r = amdahl_report({p: 3.0 + 12.0 / p for p in (1, 2, 4, 8)}, str(tmp_path / "amdahl.csv"))
+    assert abs(r["a"] - 3.0) <= 1e-9 and abs(r["b"] - 12.0) <= 1e-9 and r["r2"] > 1 - 1e-12
+    lines = (tmp_path / "amdahl.csv").read_text().splitlines()
+    assert lines[0] == "P,T,T_fit,a,b,r2" and len(lines) == 5
+    c = amdahl_report({1: 2.0, 2: 2.0, 4: 2.0})
+    assert abs(c["b"]) <= 1e-12 and abs(c["a"] - 2.0) <= 1e-12
+    with pytest.raises(ValueError):
+        amdahl_report({4: 1.0})
+
+
+def test_exchange_count_of_the_step_plan():
+    from paper_2605_16082_b200.partition import PAPER_EXCHANGES_PER_STEP, exchanges_per_step
+    assert exchanges_per_step(20) == 38 and PAPER_EXCHANGES_PER_STEP == 100
+    assert exchanges_per_step(4) == 2 * 4 + 2 + 4

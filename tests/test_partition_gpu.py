@@ -30,3 +30,59 @@ def test_partition_invariance_bitwise(pdg, P):
     for k in ("eta", "qx", "qy", "ux", "uy", "T"):
         assert np.array_equal(s[k], g[k]), (P, k, float(np.abs(s[k] - g[k]).max()))
     assert run.group.exchanges == 3 * (2 * 4 + (c.m // 2 + c.m))   # q, F3D->2D, mis, u/T per stage + 2D per substep
+
+
+def _c4_small(L=5):
+    from paper_2605_16082_b200.scenarios import make_case
+    return make_case("c4", scale=0.02, L=L)
+
+
+def test_partition_graph_equals_eager(pdg):
+    """The whole P-rank lockstep step captured in one CUDA graph == eager launches, bitwise."""
+    from paper_2605_16082_b200.partition import PartitionedRun
+    c = _c4_small()
+    out = []
+    for graph in (False, True):
+        run = PartitionedRun(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v, 3)
+        run.use_graph = graph
+        run.set_state(**c.state)
+        run.step(4)
+        run.check()
+        out.append(run.get_state())
+        assert run.group.exchanges == 4 * (2 * 4 + (c.m // 2 + c.m))
+        assert bool(run.graphs) == graph
+    for k in ("eta", "qx", "qy", "ux", "uy", "T"):
+        assert np.array_equal(out[0][k], out[1][k]), k
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_schedule_check_shipped_plan(pdg, P):
+    """Debug poisoning: ghosts NaN while their exchange is pending; the shipped step
+    plan never reads one, and the poisoned run stays bitwise equal to the plain one."""
+    from paper_2605_16082_b200.partition import PartitionedRun
+    c = _c4_small()
+    ref = PartitionedRun(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v, P)
+    ref.set_state(**c.state)
+    ref.step(2)
+    g = ref.get_state()
+    run = PartitionedRun(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v, P)
+    run.schedule_check = True
+    run.set_state(**c.state)
+    run.step(2)
+    s = run.get_state()
+    for k in ("eta", "qx", "qy", "ux", "uy", "T"):
+        assert np.array_equal(s[k], g[k]), k
+
+
+@pytest.mark.parametrize("skip", ["mis", "q", "state2d", "uT", "f3d2d"])
+def test_schedule_violation_detected(pdg, skip):
+    """A step plan that leaves out one exchange reads poisoned ghosts: ScheduleViolation."""
+    from paper_2605_16082_b200.errors import ScheduleViolation
+    from paper_2605_16082_b200.partition import PartitionedRun
+    c = _c4_small()
+    run = PartitionedRun(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v, 2)
+    run.schedule_check = True
+    run._skip_exchanges = {skip}
+    run.set_state(**c.state)
+    with pytest.raises(ScheduleViolation):
+        run.step(2)
