@@ -201,6 +201,15 @@ int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, c
                           double n0, int order, const int* els, int n_els, double* d, double* u, double* w,
                           void* stream);
 
+/* ---- domain decomposition on the device (partition.py decompose(device=...)) ---- */
+/* split_ranges: raw split points k = 1..P-1 (first prefix whose prism weight reaches k W / P) of the
+ * DEVICE int64 weights [n]; raw: HOST [P-1] (the host applies the non-empty / capacity clamps) */
+int pdg_split_search(const long long* w, int n, int P, long long* raw, void* stream);
+/* ghost rings (1..depth, breadth first over edge neighbours) of the owned range [lo, hi): DEVICE
+ * ghosts (ascending global ids) and rings, capacity nt - (hi - lo); n_ghosts: HOST */
+int pdg_partition_rings(pdg_ctx* ctx, int lo, int hi, int depth, int* ghosts, int* rings, int* n_ghosts,
+                        void* stream);
+
 /* ---- halo exchange (partitioned runs): field = nplanes planes of nt doubles; buf = [nplanes][n] */
 int pdg_halo_pack(const double* field, long long nplanes, int nt, const int* idx, int n, double* buf, void* stream);
 int pdg_halo_unpack(const double* buf, long long nplanes, int nt, const int* idx, int n, double* field, void* stream);

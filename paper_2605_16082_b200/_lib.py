@@ -38,6 +38,8 @@ _SIGS = {
     "pdg_ext2d_rk_stage": (I, [P, I, P, P, P, D, D, D, P, P, P, I, D, P, P]),
     "pdg_ext2d_subcycle_end": (I, [P, P, P, I, D, P, P, P]),
     "pdg_ext2d_rk_stage_cols": (I, [P, I, P, P, P, D, D, D, P, P, P, I, P]),
+    "pdg_split_search": (I, [P, I, I, P, P]),
+    "pdg_partition_rings": (I, [P, I, I, I, P, P, ctypes.POINTER(I), P]),
     "pdg_halo_pack": (I, [P, LL, I, P, I, P, P]),
     "pdg_halo_unpack": (I, [P, LL, I, P, I, P, P]),
     "pdg_comm_load": (I, [ctypes.c_char_p]),

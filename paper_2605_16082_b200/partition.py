@@ -49,19 +49,11 @@ class Part:
         return np.concatenate([np.arange(self.lo, self.hi), self.ghosts])
 
 
-def split_ranges(weights, P):
-    """Greedy prefix split: boundary k is the first prefix whose weight reaches k W / P (exact integers)."""
-    w = np.asarray(weights, dtype=np.int64)
-    n = w.size
-    if P < 1:
-        raise ValueError("P must be >= 1")
-    if P > n:
-        raise TooManyRanks(f"{P} ranks for {n} columns")
-    cum = np.cumsum(w)
-    W = int(cum[-1])
+def _clamp_bounds(raw, n, P):
+    """Apply the non-empty / capacity clamps to the raw split points (sequential in k)."""
     bounds = [0]
     for k in range(1, P):
-        b = int(np.searchsorted(cum * P, k * W, side="left")) + 1
+        b = int(raw[k - 1]) + 1
         b = max(b, bounds[-1] + 1)            # never an empty part
         b = min(b, n - (P - k))
         bounds.append(b)
@@ -69,36 +61,98 @@ def split_ranges(weights, P):
     return np.asarray(bounds, dtype=np.int64)
 
 
-def decompose(mesh, P: int, layers=None, depth: int = 1):
+def split_ranges(weights, P, device=None):
+    """Greedy prefix split: boundary k is the first prefix whose weight reaches k W / P (exact integers).
+    device: the prefix sum and split search run on that GPU (csrc/partition.cu pdg_split_search)."""
+    w = np.asarray(weights, dtype=np.int64)
+    n = w.size
+    if P < 1:
+        raise ValueError("P must be >= 1")
+    if P > n:
+        raise TooManyRanks(f"{P} ranks for {n} columns")
+    if device is not None:
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        from .device import ptr, stream_ptr
+        with torch.cuda.device(device):
+            wd = torch.as_tensor(w, device=device)
+            raw = np.zeros(max(P - 1, 1), np.int64)
+            _lib.check(_lib.lib().pdg_split_search(ptr(wd), n, P, raw.ctypes.data_as(ctypes.c_void_p), stream_ptr()),
+                       "split_search")
+        return _clamp_bounds(raw, n, P)
+    cum = np.cumsum(w)
+    W = int(cum[-1])
+    raw = [int(np.searchsorted(cum * P, k * W, side="left")) for k in range(1, P)]
+    return _clamp_bounds(raw, n, P)
+
+
+def _rings_host(nbr, nt, lo, hi, depth):
+    local = np.zeros(nt, bool)
+    local[lo:hi] = True
+    front = np.arange(lo, hi)
+    rings = []
+    for _ in range(depth):
+        nb = nbr[front].ravel()
+        nb = np.unique(nb[nb >= 0])
+        nb = nb[~local[nb]]
+        local[nb] = True
+        rings.append(nb)
+        front = nb
+    ghosts = np.concatenate(rings) if rings else np.zeros(0, np.int64)
+    ring = np.concatenate([np.full(g.size, k + 1, np.int32) for k, g in enumerate(rings)]) if rings else \
+        np.zeros(0, np.int32)
+    order = np.argsort(ghosts, kind="stable")
+    return ghosts[order], ring[order]
+
+
+def _rings_device(dm, lo, hi, depth):
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import ptr, stream_ptr
+    cap = max(dm.nt - (hi - lo), 1)
+    with torch.cuda.device(dm.device):
+        g = torch.empty(cap, dtype=torch.int32, device=dm.device)
+        r = torch.empty(cap, dtype=torch.int32, device=dm.device)
+        n = ctypes.c_int()
+        _lib.check(_lib.lib().pdg_partition_rings(dm.h, lo, hi, depth, ptr(g), ptr(r), ctypes.byref(n), stream_ptr()),
+                   "partition_rings")
+        return g[:n.value].cpu().numpy().astype(np.int64), r[:n.value].cpu().numpy().astype(np.int32)
+
+
+def decompose(mesh, P: int, layers=None, depth: int = 1, device=None):
     """list of Part for ranks 0..P-1.
 
     depth > 1 adds ghost rings: ring k+1 = the edge neighbours of ring k not already local.  The
     2D sub-cycle then exchanges once per substep (its three RK stages run redundantly on rings
-    1-2 and 1) while the 3D fields only ever need ring 1 (send1 / recv1)."""
+    1-2 and 1) while the 3D fields only ever need ring 1 (send1 / recv1).
+
+    device: run the O(nt) parts -- the weight prefix sum / split search and every rank's ring
+    search -- on that GPU (csrc/partition.cu; bit-exact with the host path, which stays for the
+    CPU-only multi-process tests)."""
     nt = mesh.nt
     weights = np.ones(nt, np.int64) if layers is None else np.asarray(layers, np.int64)
-    b = split_ranges(weights, P)
+    b = split_ranges(weights, P, device=device)
     owner = np.repeat(np.arange(P), np.diff(b))
     parts = []
-    nbr = np.asarray(mesh.nbr)
+    if device is not None:
+        import torch
+
+        from .device import DeviceMesh
+        dm = DeviceMesh(mesh, torch.device(device).index)
+        rings_of = lambda lo, hi: _rings_device(dm, lo, hi, depth)  # noqa: E731
+    else:
+        nbr = np.asarray(mesh.nbr)
+        rings_of = lambda lo, hi: _rings_host(nbr, nt, lo, hi, depth)  # noqa: E731
     for r in range(P):
         lo, hi = int(b[r]), int(b[r + 1])
-        local = np.zeros(nt, bool)
-        local[lo:hi] = True
-        front = np.arange(lo, hi)
-        rings = []
-        for _ in range(depth):
-            nb = nbr[front].ravel()
-            nb = np.unique(nb[nb >= 0])
-            nb = nb[~local[nb]]
-            local[nb] = True
-            rings.append(nb)
-            front = nb
-        ghosts = np.concatenate(rings) if rings else np.zeros(0, np.int64)
-        ring = np.concatenate([np.full(g.size, k + 1, np.int32) for k, g in enumerate(rings)]) if rings else \
-            np.zeros(0, np.int32)
-        order = np.argsort(ghosts, kind="stable")
-        parts.append(Part(r, P, lo, hi, ghosts[order], ring=ring[order]))
+        ghosts, ring = rings_of(lo, hi)
+        parts.append(Part(r, P, lo, hi, ghosts, ring=ring))
     for r, p in enumerate(parts):
         for s in np.unique(owner[p.ghosts]) if p.ghosts.size else []:
             s = int(s)
@@ -422,9 +476,9 @@ class PartitionedRun:
         import torch
         from .stepper import ImexStepper
         self.mesh, self.L, self.P = mesh, L, P
-        self.parts = decompose(mesh, P, np.full(mesh.nt, L), depth=GHOST_DEPTH)
-        self.local = [local_mesh(mesh, p) for p in self.parts]
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.parts = decompose(mesh, P, np.full(mesh.nt, L), depth=GHOST_DEPTH, device=dev)
+        self.local = [local_mesh(mesh, p) for p in self.parts]
         ranks = range(P) if transport == "virtual" else [rank]
         self.ranks = list(ranks)
         self.st = {r: ImexStepper(self.local[r], L, params, dt, m, kv, nu_v, part=self.parts[r], device=dev.index)

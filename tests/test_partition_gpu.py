@@ -86,3 +86,26 @@ def test_schedule_violation_detected(pdg, skip):
     run.set_state(**c.state)
     with pytest.raises(ScheduleViolation):
         run.step(2)
+
+
+@pytest.mark.parametrize("nx,ny,P,var", [(8, 6, 3, False), (32, 32, 4, True), (40, 17, 7, True), (12, 9, 1, False)])
+def test_gpu_decomposition_bit_exact(pdg, nx, ny, P, var):
+    """decompose(device=...) (csrc/partition.cu: prefix-sum split + ring BFS on the GPU) equals the
+    host restatement map for map, including variable layer weights and 3 ghost rings."""
+    import torch
+    from paper_2605_16082_b200.partition import decompose, split_ranges
+    m = pdg.mesh.hilbert_reorder(pdg.mesh.generate_basin_mesh(nx, ny, 1e4, 8e3, lambda x, y: -20.0 + 0 * x))
+    rng = np.random.default_rng(nx * ny + P)
+    layers = rng.integers(1, 40, m.nt) if var else np.full(m.nt, 10)
+    dev = torch.device("cuda", 0)
+    assert np.array_equal(split_ranges(layers, P, device=dev), split_ranges(layers, P))
+    for depth in (1, 3):
+        h = decompose(m, P, layers, depth=depth)
+        g = decompose(m, P, layers, depth=depth, device=dev)
+        for a, b in zip(h, g):
+            assert (a.lo, a.hi) == (b.lo, b.hi)
+            assert np.array_equal(a.ghosts, b.ghosts) and np.array_equal(a.ring, b.ring)
+            for d in ("send", "recv", "send1", "recv1"):
+                da, db = getattr(a, d), getattr(b, d)
+                assert sorted(da) == sorted(db)
+                assert all(np.array_equal(da[k], db[k]) for k in da)
