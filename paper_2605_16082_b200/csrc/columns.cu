@@ -1844,7 +1844,8 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
-  if (kh == 0.0 && (implicit ? tune_get(TUNE_VSPLIT) >= 2 : tune_get(TUNE_VSPLIT) >= 3)) {
+  // the sigma-form column constants are read by the tracer (NC = 1) kernels only
+  if (ncomp == 1 && kh == 0.0 && (implicit ? tune_get(TUNE_VSPLIT) >= 2 : tune_get(TUNE_VSPLIT) >= 3)) {
     double* vc = ctx->vcol();
     if (!vc) return PDG_ERR_CUDA;
     k_vcol<<<nblocks(ctx->nown, 256), 256, 0, strm>>>(m, eta_u, vc);
@@ -1852,7 +1853,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     a.vc = vc;
   }
   if (implicit && tune_get(TUNE_VSPLIT) == 4 && kh == 0.0) {
-    double* Gs = ctx->ws3((size_t)18 * ctx->L * nt);
+    double* Gs = ctx->ws3((size_t)18 * ctx->L * nt, ncomp);
     if (!Gs) return PDG_ERR_CUDA;
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
     static unsigned long long attr = 0;
@@ -1873,7 +1874,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
       k_vimpl_bwd_r<1><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
     }
   } else if (implicit && tune_get(TUNE_VSPLIT) >= 2) {
-    double* Gs = ctx->ws3((size_t)VT * ctx->L * nt);
+    double* Gs = ctx->ws3((size_t)VT * ctx->L * nt, ncomp);
     if (!Gs) return PDG_ERR_CUDA;
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
 #define LAUNCH_FWD(NCV, MB)                                                                       \
@@ -1903,7 +1904,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     else
       k_vimpl_bwd<1><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
   } else if (implicit) {
-    double* Gs = ctx->ws3((size_t)36 * ctx->L * nt);
+    double* Gs = ctx->ws3((size_t)36 * ctx->L * nt, ncomp);
     if (!Gs) return PDG_ERR_CUDA;
 #define LAUNCH_ARGS m, a, dt, rhs, Gs, x
     if (ncomp == 2) {

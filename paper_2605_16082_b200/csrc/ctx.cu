@@ -107,7 +107,7 @@ int pdg_ctx_create(const pdg_mesh_desc* d, int device, pdg_ctx** out) {
 int pdg_ctx_destroy(pdg_ctx* c) {
   if (!c) return PDG_OK;
   void* ptrs[] = {c->j2d, c->dphx, c->dphy, c->elen, c->enx, c->eny, c->b, c->fracs, c->nbr, c->nbrk, c->btag,
-                  c->ninfo, c->err, c->red, c->ws2d, c->ws3d, c->tiles[0].tslot, c->tiles[0].halo,
+                  c->ninfo, c->err, c->red, c->ws2d, c->ws3d, c->ws3t, c->tiles[0].tslot, c->tiles[0].halo,
                   c->tiles[0].hoff, c->tiles[1].tslot, c->tiles[1].halo, c->tiles[1].hoff,
                   c->vc};
   for (void* p : ptrs)

@@ -16,8 +16,10 @@ struct pdg_ctx {
   pdg_err* err = nullptr;     // device error word
   double* red = nullptr;      // reduction scratch (device)
   double* ws2d = nullptr;     // 2D subcycle workspace: 2 stage states + q0
-  double* ws3d = nullptr;     // 3D workspace (block-Thomas propagation tiles)
+  double* ws3d = nullptr;     // 3D workspace (block-Thomas propagation tiles), momentum solves
   size_t ws3d_doubles = 0;
+  double* ws3t = nullptr;     // a second one for the tracer solves, so the two can run concurrently
+  size_t ws3t_doubles = 0;
   long long launches = 0;
   std::vector<double> fracs_host;
   // tile maps of the shared-memory-staged face kernels (int3d.cu k_*_t): for tiles of tw
@@ -56,18 +58,19 @@ struct pdg_ctx {
     return vc;
   }
   // grows the 3D workspace (never on the hot path once sized)
-  double* ws3(size_t n) {
-    if (n > ws3d_doubles) {
-      if (ws3d) cudaFree(ws3d);
-      ws3d = nullptr;
-      if (cudaMalloc(&ws3d, n * sizeof(double)) != cudaSuccess) {
-        ws3d_doubles = 0;
+  static double* grow(double*& p, size_t& have, size_t n) {
+    if (n > have) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      if (cudaMalloc(&p, n * sizeof(double)) != cudaSuccess) {
+        have = 0;
         return nullptr;
       }
-      ws3d_doubles = n;
+      have = n;
     }
-    return ws3d;
+    return p;
   }
+  double* ws3(size_t n, int ncomp = 2) { return ncomp == 1 ? grow(ws3t, ws3t_doubles, n) : grow(ws3d, ws3d_doubles, n); }
 };
 
 namespace pdg {

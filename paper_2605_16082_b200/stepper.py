@@ -91,6 +91,8 @@ class ImexStepper:
         self.schedule_check = False  # debug: poison in-flight ghost slots (partitioned runs)
         self._skip_exchanges = set()  # tests only: exchange names to leave out (a broken schedule)
         self.phase_trace = None      # list -> per-phase CUDA events of eager steps (phase_csv)
+        import os
+        self.concurrent_vertical = os.environ.get("PDG_CONC_VERT", "0") == "1"
 
     def _c(self, name, rc):
         _lib.check(rc, name)
@@ -323,10 +325,22 @@ class ImexStepper:
             if part:
                 yield ("all", [out_u, out_T], "uT")
             return eta1
+        conc = self.concurrent_vertical and self.prof is None
+        if conc:   # the tracer solve on a second stream (own workspace): overlaps the momentum solve
+            main = torch.cuda.current_stream(self.dev)
+            side = self._side_stream()
+            side.wait_stream(main)
         tm(f"vertical_u_{tag}", lb.pdg_step_vertical, h, 2, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
            ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u), s)
-        tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
-           ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
+        if conc:
+            with torch.cuda.stream(side):
+                _lib.check(lb.pdg_step_vertical(h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
+                                                ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T),
+                                                ptr(T), ptr(out_T), stream_ptr()), "vertical_T")
+            main.wait_stream(side)
+        else:
+            tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
+               ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
         if part:
             yield ("all", [out_u, out_T], "uT")
         return eta1
@@ -373,6 +387,11 @@ class ImexStepper:
             e = ev()
             e.record()
             tr.append(("compute:tail", last, e))
+
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.dev, priority=-1)
+        return self._side
 
     # ------------------------------------------------------------------ schedule checking (debug)
     def _poison(self, fields, deep):
