@@ -1028,6 +1028,52 @@ __device__ __forceinline__ void cs_get(const double* csp, int t, Col& C, double 
   }
 }
 
+// M1 - dt A_d of layer l and the coupling U = -dt u to layer l-1, assembled block-symmetrically.
+// Every 3x3 block of vop_blocks is a combination of symmetric 3x3 pieces (Sa_m, R, Ft, Fi, MHQ,
+// M1h); with DV = (1/2, -1/2) the diagonal block d = KM (x) M1h - dt A_d is
+//   d_00 = K00 M1h - dt ( Sa0/2 + r00 R - Ft - pt MHQ)      r00 = -cvol/4 + [l>0]   ct/2
+//   d_01 = K01 M1h - dt ( Sa1/2 + r01 R)                    r01 =  cvol/4 - [l>0]   ct/2
+//   d_10 = K10 M1h - dt (-Sa0/2 + r10 R)                    r10 =  cvol/4 - [l<L-1] cb/2
+//   d_11 = K11 M1h - dt (-Sa1/2 + r11 R + Fi - pb MHQ)      r11 = -cvol/4 + [l<L-1] cb/2
+// so 24 entries are formed (the mirrored ones are copies) instead of 36 general ones, and the
+// coupling U = -dt [ ca Rp/2 , -ca Rp/2 + pt MHQ - Fn ] is two symmetric blocks (Uc0, Uc1).
+// Same values as vop_blocks + the d = KM M1h - dt d combination up to rounding.
+__device__ __forceinline__ void vimpl_blocks(int l, int L, const VG& Vp, const VG& V, const VAdv& A, const VDif& D,
+                                             const double M1h[3][3], double dt, double d[6][6], double Uc0[3][3],
+                                             double Uc1[3][3]) {
+  const double c = -dt;
+  const double q4 = 0.25 * D.cvol;
+  const double ht = l > 0 ? 0.5 * D.ct : 0.0, hb = l < L - 1 ? 0.5 * D.cb : 0.0;
+  const double r00 = ht - q4, r01 = q4 - ht, r10 = q4 - hb, r11 = hb - q4;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      const double R = V.R[a][b], mh = MHQ[a][b], m1 = M1h[a][b];
+      const double s0 = 0.5 * A.Sa[0][a][b], s1 = 0.5 * A.Sa[1][a][b];
+      const double v00 = KM[0][0] * m1 + c * (((s0 + r00 * R) - A.Ft[a][b]) - D.pt * mh);
+      const double v01 = KM[0][1] * m1 + c * (s1 + r01 * R);
+      const double v10 = KM[1][0] * m1 + c * (r10 * R - s0);
+      const double v11 = KM[1][1] * m1 + c * (((r11 * R - s1) + A.Fi[a][b]) - D.pb * mh);
+      d[a][b] = v00;
+      d[b][a] = v00;
+      d[a][3 + b] = v01;
+      d[b][3 + a] = v01;
+      d[3 + a][b] = v10;
+      d[3 + b][a] = v10;
+      d[3 + a][3 + b] = v11;
+      d[3 + b][3 + a] = v11;
+      if (l > 0) {
+        const double u0 = c * (0.5 * D.ca * Vp.R[a][b]);
+        const double u1 = c * ((D.pt * mh - A.Fn[a][b]) - 0.5 * D.ca * Vp.R[a][b]);
+        Uc0[a][b] = u0;
+        Uc0[b][a] = u0;
+        Uc1[a][b] = u1;
+        Uc1[b][a] = u1;
+      }
+    }
+}
+
 // FORWARD: assembles M1 - dt A per layer, eliminates, writes the compact tile and g_l (into x).
 // Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
 // (each thread stages and reads only its own words: no barriers), issued two layers ahead;
@@ -1101,8 +1147,6 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     }
     VPieces P;
     vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
-    double d[6][6], u[3][6], w[3][6];
-    vop_blocks(l, L, Vp, V, Vn, P, P, d, u, w);
     double jz1[3], M1h[3][3];
     layer_jz(C.b, e1, ft, fb, jz1);
 #pragma unroll
@@ -1113,17 +1157,15 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
         M1h[p][q] = s;
         M1h[q][p] = s;
       }
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int j = 0; j < 6; ++j) d[i][j] = KM[i / 3][j / 3] * M1h[i % 3][j % 3] - dt * d[i][j];
+    double d[6][6], Uc[2][3][3];
+    vimpl_blocks(l, L, Vp, V, P, P, M1h, dt, d, Uc[0], Uc[1]);
     double g[6][NC];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) g[i][cc] = cur[(cc * 6 + i) * VBLK];
     if (l > 0) {
-      // Dt = D - U G_{l-1} = D - (U E_{l-1}) W_{l-1},  U = -dt u
+      // Dt = D - U G_{l-1} = D - (U E_{l-1}) W_{l-1},  U = -dt u = [Uc0, Uc1]
       double Pm[3][3];
 #pragma unroll
       for (int i = 0; i < 3; ++i)
@@ -1131,7 +1173,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
         for (int j = 0; j < 3; ++j) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * tl[(k * 3 + j) * VBLK + t];
+          for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][i][k % 3] * tl[(k * 3 + j) * VBLK + t];
           Pm[i][j] = acc;
         }
       double S0[3][3], S1h[3][3];
@@ -1162,7 +1204,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
         for (int cc = 0; cc < NC; ++cc) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * gp[k][cc];
+          for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][i][k % 3] * gp[k][cc];
           g[i][cc] = g[i][cc] - acc;
         }
     }
