@@ -1749,7 +1749,35 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
           for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jm * mo[cc][n % 3];
       }
       double acc[NC][6];
-      {
+      // MODE 1 only needs the column sum acc[p] + acc[3+p] of every contribution: the sums over the
+      // two levels of the phi_z test functions collapse (sum_m K3[m] = KM, sum_lev VS[v][lev] = 1,
+      // KM column sums = 1), so the volume, lateral and mass terms are formed per horizontal node
+      // only (cs[cc][p]); the values equal the per-node forms summed, up to rounding.
+      double cs[NC][3];
+      if constexpr (MODE == 1) {
+        double z[2][2][3];
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+          for (int lev = 0; lev < 2; ++lev) mhq_vec(qv[d] + 3 * lev, z[d][lev]);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          double Sd[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            double dot[2][2];
+#pragma unroll
+            for (int l1 = 0; l1 < 2; ++l1)
+#pragma unroll
+              for (int l2 = 0; l2 < 2; ++l2)
+                dot[l1][l2] =
+                    u[cc][3 * l1] * z[d][l2][0] + u[cc][3 * l1 + 1] * z[d][l2][1] + u[cc][3 * l1 + 2] * z[d][l2][2];
+            Sd[d] = KM[0][0] * dot[0][0] + KM[0][1] * dot[0][1] + KM[1][0] * dot[1][0] + KM[1][1] * dot[1][1];
+          }
+#pragma unroll
+          for (int p = 0; p < 3; ++p) cs[cc][p] = j2d * (C.dx[p] * Sd[0] + C.dy[p] * Sd[1]);
+        }
+      } else {
         double z[2][2][3];
 #pragma unroll
         for (int d = 0; d < 2; ++d)
@@ -1816,7 +1844,13 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
           for (int vv = 0; vv < 2; ++vv)
 #pragma unroll
             for (int h = 0; h < 2; ++h) x[vv][h] = (f[vv][h] >= 0.0 ? ti[vv][h] : te[vv][h]) * f[vv][h];
-          lat_add(acc[cc], k, x, je);
+          if constexpr (MODE == 1) {   // both levels of edge node hn: sum_vh ES[h][hn] x[v][h]
+            const double x0 = x[0][0] + x[1][0], x1 = x[0][1] + x[1][1];
+            cs[cc][EV0(k)] += je * (ES[0][0] * x0 + ES[1][0] * x1);
+            cs[cc][EV1(k)] += je * (ES[0][1] * x0 + ES[1][1] * x1);
+          } else {
+            lat_add(acc[cc], k, x, je);
+          }
         }
       }
       if constexpr (NC >= 2) {
@@ -1827,6 +1861,26 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
         layer_jz(C.b, eta, ft, fb, jz);
         mjz(jz, Mu);
         const double ir = 1.0 / a.rho0;
+        if constexpr (MODE == 1) {   // column sum of (K (x) J2D Mjz) y = J2D Mjz (y_top + y_bot)
+          double ys0[3], ys1[3];
+#pragma unroll
+          for (int n = 0; n < 3; ++n) {
+            ys0[n] = a.f * (u[1][n] + u[1][3 + n]) - (rr[0][n] + rr[0][3 + n]) * ir;
+            ys1[n] = -a.f * (u[0][n] + u[0][3 + n]) - (rr[1][n] + rr[1][3 + n]) * ir;
+          }
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            cs[0][p] += j2d * (Mu[p][0] * ys0[0] + Mu[p][1] * ys0[1] + Mu[p][2] * ys0[2]);
+            cs[1][p] += j2d * (Mu[p][0] * ys1[0] + Mu[p][1] * ys1[1] + Mu[p][2] * ys1[2]);
+          }
+          if (l == 0) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              cs[0][k] += j2d / 6.0 * a.tsx;
+              cs[1][k] += j2d / 6.0 * a.tsy;
+            }
+          }
+        } else {
         double y0[6], y1[6], m0[6], m1[6];
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
@@ -1847,6 +1901,7 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
             acc[1][k] += j2d / 6.0 * a.tsy;
           }
         }
+        }
         if (l == L - 1 && a.cd != 0.0) {
           double dx3[3], dy3[3], mx[3], my[3];
 #pragma unroll
@@ -1860,16 +1915,21 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
           mh_apply3(dy3, j2d, my);
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            acc[0][3 + k] += mx[k];
-            acc[1][3 + k] += my[k];
+            if constexpr (MODE == 1) {
+              cs[0][k] += mx[k];
+              cs[1][k] += my[k];
+            } else {
+              acc[0][3 + k] += mx[k];
+              acc[1][3 + k] += my[k];
+            }
           }
         }
       }
-      if (MODE == 1) {
+      if constexpr (MODE == 1) {
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-          for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
+          for (int k = 0; k < 3; ++k) csum[cc][k] += cs[cc][k];
       } else {
         double j0[3], M0[3][3];
         layer_jz(C.b, eta0, ft, fb, j0);

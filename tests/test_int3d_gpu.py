@@ -97,8 +97,13 @@ def test_horizontal_rhs(pdg, case):
     assert rel(I.tracer_horizontal_rhs(c["G"], c["T"], c["qb"], c["facb"], c["p"]), Ft) <= TOL
     st = O.stress_rhs(c["OG"], 1e-4, -3e-5, 2.5e-3, c["ux"], c["uy"])
     assert rel(I.stress_rhs(c["G"], 1e-4, -3e-5, 2.5e-3, c["ux"], c["uy"]), st) <= TOL
-    with pytest.raises(NotImplementedError):
-        I.horizontal_rhs(c["G"], c["ux"], c["uy"], c["q"], c["fac"], c["r"], c["M"], pdg.PhysParams(kappa_h=1.0))
+    # explicit horizontal viscosity: the patched oracle (tests/test_hdiff_gpu.py has the golden vectors)
+    pv = pdg.PhysParams(f=c["p"].f, kappa_h=3.0, nu_h=2.0)
+    assert rel(I.horizontal_rhs(c["G"], c["ux"], c["uy"], c["q"], c["fac"], c["r"], c["M"], pv),
+               O.horizontal_rhs(c["OG"], c["ux"], c["uy"], c["q"], c["fac"], c["r"], c["M"],
+                                pv)) <= TOL
+    assert rel(I.tracer_horizontal_rhs(c["G"], c["T"], c["qb"], c["facb"], pv),
+               O.tracer_horizontal_rhs(c["OG"], c["T"], c["qb"], c["facb"], pv)) <= TOL
 
 
 def test_vertical_operator_and_solvers(pdg, case):

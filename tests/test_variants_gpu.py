@@ -9,8 +9,9 @@ library for A/B runs (scripts/ab_tune.py) and must keep producing the same answe
   key 11 r / w~: 0 register kernels, 64 / 128 tile-staged
   key 5  stage RHS: 1 register kernel (128-thread blocks), 8 shared-memory column constants
   key 6  2D RK stage occupancy variant (register allocation can change FMA contraction)
-Tile-staged and register kernels do the same arithmetic (bitwise equal); the split Thomas and the
-branch-free reciprocals of the staged vertical kernels differ at rounding level.
+Tile-staged and register kernels do the same arithmetic (bitwise equal), except the tile-staged
+F3D->2D kernel, which forms the column sum per horizontal node (rounding-level difference); the
+split Thomas and the branch-free reciprocals of the staged vertical kernels differ at rounding level.
 """
 import numpy as np
 import pytest
@@ -55,7 +56,7 @@ def rel(a, b):
 
 @pytest.mark.parametrize("setting,tol", [
     ({7: 1}, 1e-11), ({7: 2}, 1e-11), ({7: 3}, 1e-13),
-    ({9: 0}, 0.0), ({9: 64}, 0.0),
+    ({9: 0}, 1e-12), ({9: 64}, 0.0),
     ({11: 0}, 0.0), ({11: 64}, 0.0),
     ({5: 1}, 1e-12), ({10: 128}, 1e-12),
     ({6: 0}, 1e-12), ({6: 3}, 1e-12),
