@@ -1078,7 +1078,12 @@ __device__ __forceinline__ void vimpl_blocks(int l, int L, const VG& Vp, const V
 // Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
 // (each thread stages and reads only its own words: no barriers), issued two layers ahead;
 // the previous layer's tile lives in shared memory, not in registers or L2.
-template <int NC, int MINB, bool KH0, bool CT = false>
+//
+// BULK (nt even): the ring is filled by the copy engine instead -- per layer one thread issues NE
+// cp.async.bulk copies of the block's contiguous plane segments (1 KB each) completing on the
+// slot's mbarrier; the threads wait on it, and one __syncthreads per layer frees the slot read two
+// layers earlier (threads past the owned range stay for the barriers).
+template <int NC, int MINB, bool KH0, bool CT = false, bool BULK = false>
 __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, double dt, const double* rhs,
                                                         double* __restrict__ Gs, double* x) {
   
@@ -1088,15 +1093,43 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   double* tl = smem + 3 * NE * VBLK;         // [VT][VBLK]
   double* cst = tl + VT * VBLK;              // [NCS][VBLK] column constants
   double* fr = cst + NCS * VBLK;             // [L+1]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(fr + m.L + 1);   // [3] (BULK)
   const int t = threadIdx.x;
-  const int c = blockIdx.x * VBLK + t;
+  // BULK: every thread runs the layer loop (the block barriers must be met by all of them, also
+  // inside a warp); threads past the owned range repeat the last owned column and store nothing
+  const bool act = blockIdx.x * VBLK + t < m.nown;
+  const int c = act ? blockIdx.x * VBLK + t : m.nown - 1;
   const int nt = m.nt, L = m.L;
+  const int c0 = blockIdx.x * VBLK;
   for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
+  if (BULK && t == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mbar_init(bars + k, 1);
+    mbar_init_fence();
+  }
   __syncthreads();
-  if (c >= m.nown) return;
+  if (!BULK && !act) return;
   const size_t P6 = (size_t)6 * L * nt;
+  // 16-byte multiple of the block's owned columns (nt even: at most one column past nown, < nt)
+  const unsigned seg = (unsigned)(min(VBLK, m.nown - c0) * 8 + 15) & ~15u;
   // plane stride hidden from the optimiser (see k_vexpl2)
   auto stage = [&](int l) {
+    if (BULK) {
+      if (t == 0 && l < L) {
+        unsigned long long* bar = bars + l % 3;
+        const unsigned ln = (unsigned)L * (unsigned)nt, lo = (unsigned)l * (unsigned)nt + (unsigned)c0;
+        double* s = ring + (l % 3) * NE * VBLK;
+        fence_proxy_async();
+        mbar_expect_tx(bar, NE * seg);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int i = 0; i < 6; ++i) bulk_g2s(s + (cc * 6 + i) * VBLK, rhs + cc * P6 + (i * ln + lo), seg, bar);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) bulk_g2s(s + (6 * NC + i) * VBLK, a.wt + (i * ln + lo), seg, bar);
+      }
+      return;
+    }
     if (l < L) {
       unsigned ln = (unsigned)L * (unsigned)nt;
       asm volatile("" : "+r"(ln));
@@ -1129,10 +1162,16 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   Vn = V;
   double gp[6][NC];
   for (int l = 0; l < L; ++l) {
+    if (BULK) __syncthreads();   // every thread is done with layer l-1: its slot may be refilled
     cs_get(cst, t, C, eta, e0, e1);
     const double j2d = C.j2d;
     stage(l + 2);
-    cp_async_wait1();  // layers l and l+1 have landed
+    if (BULK) {                  // layers l and l+1 have landed
+      mbar_wait(bars + l % 3, (unsigned)(l / 3) & 1u);
+      if (l + 1 < L) mbar_wait(bars + (l + 1) % 3, (unsigned)((l + 1) / 3) & 1u);
+    } else {
+      cp_async_wait1();
+    }
     const double* cur = ring + (l % 3) * NE * VBLK + t;
     const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
     const double ft = fr[l], fb = fr[l + 1];
@@ -1212,7 +1251,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     const int bad = lu6r_bf(d, rp);
     if (bad >= 0) {
       report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
-      return;
+      if (!BULK) return;          // (BULK: keep meeting the block barriers; the step is void anyway)
     }
     lu6r_solve<NC>(d, rp, g);
     {
@@ -1223,7 +1262,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
       for (int i = 0; i < 6; ++i)
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
-          x[cc * P6 + (i * ln + lo)] = g[i][cc];
+          if (act) x[cc * P6 + (i * ln + lo)] = g[i][cc];
           gp[i][cc] = g[i][cc];
         }
     }
@@ -1246,7 +1285,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
           tl[(i * 3 + j) * VBLK + t] = e[i];
-          gt[(size_t)(i * 3 + j) * nt] = e[i];
+          if (act) gt[(size_t)(i * 3 + j) * nt] = e[i];
         }
       }
       // S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}  (symmetric, packed)
@@ -1259,7 +1298,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
           const double s1 = -dt * (P.cn * Vn.R[p][q]);
           tl[(18 + k) * VBLK + t] = s0;
           tl[(24 + k) * VBLK + t] = s1;
-          if (!CT) {
+          if (!CT && act) {
             gt[(size_t)(18 + k) * nt] = s0;
             gt[(size_t)(24 + k) * nt] = s1;
           }
@@ -1408,7 +1447,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
   }
 }
 
-inline size_t vimpl_fwd_smem(int nc, int L) { return ((size_t)3 * (6 * nc + 6) * VBLK + (VT + NCS) * VBLK + L + 1) * 8; }
+inline size_t vimpl_fwd_smem(int nc, int L) { return ((size_t)3 * (6 * nc + 6) * VBLK + (VT + NCS) * VBLK + L + 1 + 3) * 8; }
 
 // EXPLICIT: x = M1^-1 (rhs + dt A xin), A applied matrix free; M1^-1 = K^-1 (x) (J2D Mjz)^-1.
 template <int NC, int MINB>
@@ -1904,14 +1943,25 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
                            (int)vimpl_fwd_smem(2, 4096));
       cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)vimpl_fwd_smem(1, 4096));
-      
+      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)vimpl_fwd_smem(2, 4096));
+      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)vimpl_fwd_smem(1, 4096));
     }
+    // bulk-copy ring: plane segments are 16-byte aligned when nt is even (TUNE_BULK bit 1 = on)
+    const bool bulk = nt % 2 == 0 && (tune_get(TUNE_BULK) & 2);
     if (ncomp == 2) {
-      k_vimpl_fwd<2, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+      if (bulk)
+        k_vimpl_fwd<2, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+      else
+        k_vimpl_fwd<2, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
       if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
       k_vimpl_bwd_r<2><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
     } else {
-      k_vimpl_fwd<1, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+      if (bulk)
+        k_vimpl_fwd<1, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+      else
+        k_vimpl_fwd<1, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
       if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
       k_vimpl_bwd_r<1><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
     }

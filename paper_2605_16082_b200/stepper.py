@@ -109,7 +109,7 @@ class ImexStepper:
         self.prof.setdefault(name, []).append((e0, e1))
 
     # ------------------------------------------------------------------ state I/O (reference layouts)
-    IO_CHUNK_BYTES = 128 << 20   # DMA granularity of the host I/O pipeline
+    IO_CHUNK_BYTES = 256 << 20   # DMA granularity of the host I/O pipeline (scripts/e2e_sweep.py: 241 vs 243 ms at 128 MB)
     IO_SLOTS = 4                 # device staging buffers per direction
 
     def _io_plan(self):

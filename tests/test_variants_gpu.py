@@ -9,6 +9,8 @@ library for A/B runs (scripts/ab_tune.py) and must keep producing the same answe
   key 11 r / w~: 0 register kernels, 64 / 128 tile-staged
   key 5  stage RHS: 1 register kernel (128-thread blocks), 8 shared-memory column constants
   key 6  2D RK stage occupancy variant (register allocation can change FMA contraction)
+  key 12 bit 1: cp.async.bulk (copy-engine) staging ring + mbarriers in the implicit forward
+         elimination instead of per-thread cp.async (900 columns: the last block splits a warp)
 Tile-staged and register kernels do the same arithmetic (bitwise equal), except the tile-staged
 F3D->2D kernel, which forms the column sum per horizontal node (rounding-level difference); the
 split Thomas and the branch-free reciprocals of the staged vertical kernels differ at rounding level.
@@ -18,7 +20,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-KEYS = (1, 2, 5, 6, 7, 9, 10, 11)
+KEYS = (1, 2, 5, 6, 7, 9, 10, 11, 12)
 
 
 @pytest.fixture(scope="module")
@@ -60,6 +62,7 @@ def rel(a, b):
     ({11: 0}, 0.0), ({11: 64}, 0.0),
     ({5: 1}, 1e-12), ({10: 128}, 1e-12),
     ({6: 0}, 1e-12), ({6: 3}, 1e-12),
+    ({12: 3}, 0.0),     # bulk-copy (TMA) ring of the implicit forward elimination: same arithmetic
 ])
 def test_variant_matches_default(case, setting, tol):
     pdg, c, lib, defaults = case
