@@ -101,8 +101,8 @@ def _rhs_worker(args):
     else:
         raise ValueError(fname)
     dt = time.perf_counter() - t0
-    rows = np.asarray(out).reshape((nt, L) + np.asarray(out).shape[1:])[els] if fname != \
-        "assemble_vertical_operator" else np.asarray(out)
+    o = np.asarray(out)
+    rows = o.reshape(nt, L, -1)[els] if fname != "assemble_vertical_operator" else o
     return dt, rows.nbytes
 
 
@@ -142,11 +142,16 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_cpu_baseline.json"))
     ap.add_argument("--procs", type=int, default=os.cpu_count())
     ap.add_argument("--skip-c3-step", action="store_true")
+    ap.add_argument("--single-from", default=None, help="reuse the (i) legs of an earlier report")
     a = ap.parse_args()
     rep = {"host": _host(), "kind": "reference (unmodified prismdg functions; oracle/stepper.py orchestration)"}
-    rep["single"] = [leg_single("c1", 100), leg_single("c2", 2)]
-    if not a.skip_c3_step:
-        rep["single"].append(leg_single("c3", 1))
+    if a.single_from:
+        with open(a.single_from) as f:
+            rep["single"] = json.load(f)["single"]
+    else:
+        rep["single"] = [leg_single("c1", 100), leg_single("c2", 2)]
+        if not a.skip_c3_step:
+            rep["single"].append(leg_single("c3", 1))
     print(json.dumps(rep["single"]), flush=True)
     c3 = leg_chunked("c3", a.procs)
     rep["chunked"] = [c3]
