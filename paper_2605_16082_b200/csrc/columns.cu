@@ -480,6 +480,61 @@ struct VDif {
 };
 struct VPieces : VAdv, VDif {};
 
+// advective volume pieces Sa only
+__device__ __forceinline__ void vop_adv_vol(double j2d, const double wt[6], const double wm[6], VAdv& P) {
+  double dwt[3], dwb[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    dwt[c] = wt[c] - wm[c];
+    dwb[c] = wt[3 + c] - wm[3 + c];
+  }
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    double y[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c] = j2d * (KM[mm][0] * dwt[c] + KM[mm][1] * dwb[c]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = a; b < 3; ++b) {
+        const double s = T3[a][b][0] * y[0] + T3[a][b][1] * y[1] + T3[a][b][2] * y[2];
+        P.Sa[mm][a][b] = s;
+        P.Sa[mm][b][a] = s;
+      }
+  }
+}
+// bottom face of layer l < L-1 (the interface with layer l+1): outflow part Fo (positive speed,
+// point-wise) and inflow part Fi = whole - Fo (closed-form P1 face mass)
+__device__ __forceinline__ void vop_adv_bot(double j2d, const double wm[6], const double wtn[3], VAdv& P) {
+  double a3[6], b3[6], sout[6], e3[3];
+  hq(wtn, a3);
+  hq(wm + 3, b3);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const double sb = a3[q] - b3[q];
+    sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
+  }
+  face3(sout, P.Fo);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) e3[c] = wtn[c] - wm[3 + c];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      const double w = j2d * (T3[a][b][0] * e3[0] + T3[a][b][1] * e3[1] + T3[a][b][2] * e3[2]);
+      P.Fi[a][b] = w - P.Fo[a][b];
+      P.Fi[b][a] = P.Fi[a][b];
+    }
+}
+// surface (l == 0): the whole speed leaves through the top face; Fn unused
+__device__ __forceinline__ void vop_adv_surf(double j2d, const double wt[6], const double wm[6], VAdv& P) {
+  double sp[6], d3[3] = {wt[0] - wm[0], wt[1] - wm[1], wt[2] - wm[2]};
+  hq(d3, sp);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) sp[q] = j2d * sp[q];
+  face3(sp, P.Ft);
+}
+
 __device__ __forceinline__ void vop_adv(double j2d, int l, int L, const double wt[6], const double wm[6],
                                         const double wtn[3], VAdv& P) {
   double dwt[3], dwb[3];
@@ -1184,8 +1239,34 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = nxt[(6 * NC + k) * VBLK];
     }
+    // Advective pieces with the interface face masses carried: the top face of layer l is the
+    // bottom face of layer l-1 (same speed and mesh velocity), so Ft / Fn are that layer's Fo / Fi
+    // (tile words 18..29) and only the bottom face is integrated here.
     VPieces P;
-    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
+    vop_adv_vol(j2d, wt, wm, P);
+    if (l == 0) {
+      vop_adv_surf(j2d, wt, wm, P);
+    } else {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          P.Ft[p][q] = tl[(18 + sym6(p, q)) * VBLK + t];
+          P.Fn[p][q] = tl[(24 + sym6(p, q)) * VBLK + t];
+        }
+    }
+    if (l < L - 1) {
+      vop_adv_bot(j2d, wm, wtn, P);
+    } else {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          P.Fi[p][q] = 0.0;
+          P.Fo[p][q] = 0.0;
+        }
+    }
+    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, P);
     double jz1[3], M1h[3][3];
     layer_jz(C.b, e1, ft, fb, jz1);
 #pragma unroll
@@ -1215,14 +1296,18 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
           for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][i][k % 3] * tl[(k * 3 + j) * VBLK + t];
           Pm[i][j] = acc;
         }
+      // coupling of layer l-1 to l rebuilt from this layer's top-face pieces (bitwise the values
+      // layer l-1 would form: Fo_{l-1} = Ft_l, pb_{l-1} = pt_l, cn_{l-1} = ct_l, R_l):
+      // S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l}
       double S0[3][3], S1h[3][3];
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const double s0 = tl[(18 + sym6(p, q)) * VBLK + t], s1 = tl[(24 + sym6(p, q)) * VBLK + t];
-          S1h[p][q] = DV[1] * s1;                 // W_bot = -DV1 S1  (sign folded below)
-          S0[p][q] = s0 - DV[0] * s1;             // W_top = S0 - DV0 S1
+        for (int q = p; q < 3; ++q) {
+          const double s0 = -dt * (P.Ft[p][q] + P.pt * MHQ[p][q]);
+          const double s1 = -dt * (P.ct * V.R[p][q]);
+          S1h[p][q] = S1h[q][p] = DV[1] * s1;    // W_bot = -DV1 S1  (sign folded below)
+          S0[p][q] = S0[q][p] = s0 - DV[0] * s1; // W_top = S0 - DV0 S1
         }
 #pragma unroll
       for (int i = 0; i < 3; ++i)
@@ -1288,19 +1373,18 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
           if (act) gt[(size_t)(i * 3 + j) * nt] = e[i];
         }
       }
-      // S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}  (symmetric, packed)
+      // the bottom-face pieces become the next layer's top-face pieces (packed symmetric);
+      // !CT: the global tile also holds S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
         for (int q = p; q < 3; ++q) {
           const int k = sym6(p, q);
-          const double s0 = -dt * (P.Fo[p][q] + P.pb * MHQ[p][q]);
-          const double s1 = -dt * (P.cn * Vn.R[p][q]);
-          tl[(18 + k) * VBLK + t] = s0;
-          tl[(24 + k) * VBLK + t] = s1;
+          tl[(18 + k) * VBLK + t] = P.Fo[p][q];
+          tl[(24 + k) * VBLK + t] = P.Fi[p][q];
           if (!CT && act) {
-            gt[(size_t)(18 + k) * nt] = s0;
-            gt[(size_t)(24 + k) * nt] = s1;
+            gt[(size_t)(18 + k) * nt] = -dt * (P.Fo[p][q] + P.pb * MHQ[p][q]);
+            gt[(size_t)(24 + k) * nt] = -dt * (P.cn * Vn.R[p][q]);
           }
         }
     }
@@ -1572,6 +1656,8 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
   double* ring = smem;             // [3][NE][VBLK]
   double* cst = smem + 3 * NE * VBLK;  // [NCS][VBLK] column constants
   double* fr = cst + NCS * VBLK;
+  constexpr bool FCS = NC == 1;
+  double* fc = fr + m.L + 1;       // [12][VBLK] carried face pieces (FCS)
   const int t = threadIdx.x;
   const int c = blockIdx.x * VBLK + t;
   const int nt = m.nt, L = m.L;
@@ -1664,8 +1750,45 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = nxt[(12 * NC + k) * VBLK];
     }
+    // interface face masses carried from the layer above (see k_vimpl_fwd), parked in shared
+    // memory; the register-tight NC == 2 kernel has no room for 12 KB more shared memory (two
+    // blocks per SM) and spills when it carries them in registers, so it integrates both faces
     VPieces P;
-    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
+    if (!FCS) {
+      vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
+    } else {
+    vop_adv_vol(j2d, wt, wm, P);
+    if (l == 0) {
+      vop_adv_surf(j2d, wt, wm, P);
+    } else {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          P.Ft[p][q] = fc[sym6(p, q) * VBLK + t];
+          P.Fn[p][q] = fc[(6 + sym6(p, q)) * VBLK + t];
+        }
+    }
+    if (l < L - 1) {
+      vop_adv_bot(j2d, wm, wtn, P);
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = p; q < 3; ++q) {
+          fc[sym6(p, q) * VBLK + t] = P.Fo[p][q];
+          fc[(6 + sym6(p, q)) * VBLK + t] = P.Fi[p][q];
+        }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          P.Fi[p][q] = 0.0;
+          P.Fo[p][q] = 0.0;
+        }
+    }
+    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, P);
+    }
     double jz1[3], A1[3][3];
     layer_jz(C.b, e1, ft, fb, jz1);
 #pragma unroll
@@ -1729,7 +1852,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
     V = Vn;
   }
 }
-inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1) * 8; }
+inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1 + (nc == 1 ? 12 * VBLK : 0)) * 8; }
 
 // EXPLICIT stage for momentum (2 comps) AND tracer in one pass: the geometry window, the
 // advective pieces of A and the M1 factorisation are shared; only the diffusion pieces differ.
