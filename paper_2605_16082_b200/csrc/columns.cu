@@ -449,6 +449,10 @@ __device__ __forceinline__ double pen_sigma(const VG& A, const VG& B, double n0,
   return n0 * ((order + 1.0) * (order + 3.0) / 6.0) * fmax(A.rhgt, B.rhgt);
 }
 
+__device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmetric 3x3
+  return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
+}
+
 // F(x) for x at the 6 points, symmetric
 __device__ __forceinline__ void face3(const double x[6], double F[3][3]) {
 #pragma unroll
@@ -533,6 +537,74 @@ __device__ __forceinline__ void vop_adv_surf(double j2d, const double wt[6], con
 #pragma unroll
   for (int q = 0; q < 6; ++q) sp[q] = j2d * sp[q];
   face3(sp, P.Ft);
+}
+
+// The same pieces pre-multiplied by a scale (the implicit elimination passes c = -dt, so every
+// block entry of M1 - dt A is one FMA chain without the final -dt multiplication): Sa comes out
+// as scale/2 * Sa (the 1/2 of DV folded in), the face masses as scale * F.
+__device__ __forceinline__ void vop_adv_vol_s(double sj, const double wt[6], const double wm[6], double Sa[2][6]) {
+  double dwt[3], dwb[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    dwt[c] = wt[c] - wm[c];
+    dwb[c] = wt[3 + c] - wm[3 + c];
+  }
+  const double hs = 0.5 * sj;
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    double y[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c] = hs * (KM[mm][0] * dwt[c] + KM[mm][1] * dwb[c]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = a; b < 3; ++b) Sa[mm][sym6(a, b)] = T3[a][b][0] * y[0] + T3[a][b][1] * y[1] + T3[a][b][2] * y[2];
+  }
+}
+// face mass of the positive part of a P1 speed s = a - b given at the corners (packed symmetric)
+__device__ __forceinline__ void face_pos_s(double sj, const double e3[3], double F[6]) {
+  double sp[6], sq[6];
+  hq(e3, sp);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) sq[q] = sj * (sp[q] > 0.0 ? sp[q] : 0.0);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) acc += (QW[q] * BARY[q][a] * BARY[q][b]) * sq[q];
+      F[sym6(a, b)] = acc;
+    }
+}
+// scaled bottom face of layer l < L-1: Fo (outflow, point-wise positive part), Fi = whole - Fo
+__device__ __forceinline__ void vop_adv_bot_s(double sj, const double wm[6], const double wtn[3], double Fo[6],
+                                              double Fi[6]) {
+  double e3[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) e3[c] = wtn[c] - wm[3 + c];
+  face_pos_s(sj, e3, Fo);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b)
+      Fi[sym6(a, b)] = sj * (T3[a][b][0] * e3[0] + T3[a][b][1] * e3[1] + T3[a][b][2] * e3[2]) - Fo[sym6(a, b)];
+}
+// scaled surface face (l == 0): the whole speed
+__device__ __forceinline__ void vop_adv_surf_s(double sj, const double wt[6], const double wm[6], double Ft[6]) {
+  double sp[6], d3[3] = {wt[0] - wm[0], wt[1] - wm[1], wt[2] - wm[2]};
+  hq(d3, sp);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) sp[q] = sj * sp[q];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) acc += (QW[q] * BARY[q][a] * BARY[q][b]) * sp[q];
+      Ft[sym6(a, b)] = acc;
+    }
 }
 
 __device__ __forceinline__ void vop_adv(double j2d, int l, int L, const double wt[6], const double wm[6],
@@ -1047,9 +1119,6 @@ constexpr int VT = 30;
 constexpr int VBLK = 128;
 
 
-__device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmetric 3x3
-  return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
-}
 
 // Per-thread column constants parked in shared memory and re-read (volatile) inside the layer
 // loop: J2D, grad phi, bed and the three free surfaces are used every layer but would otherwise
@@ -1239,46 +1308,62 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = nxt[(6 * NC + k) * VBLK];
     }
-    // Advective pieces with the interface face masses carried: the top face of layer l is the
-    // bottom face of layer l-1 (same speed and mesh velocity), so Ft / Fn are that layer's Fo / Fi
-    // (tile words 18..29) and only the bottom face is integrated here.
-    VPieces P;
-    vop_adv_vol(j2d, wt, wm, P);
+    // Advective pieces scaled by c = -dt (every block entry of M1 - dt A is then one FMA chain),
+    // with the interface face masses carried: the top face of layer l is the bottom face of layer
+    // l-1 (same speed and mesh velocity), so Ft / Fn are that layer's Fo / Fi (tile words 18..29,
+    // packed symmetric) and only the bottom face is integrated here.
+    const double cdt = -dt, sj = cdt * j2d;
+    double Sa[2][6], Ft[6], Fn[6], Fo[6], Fi[6];
+    vop_adv_vol_s(sj, wt, wm, Sa);
     if (l == 0) {
-      vop_adv_surf(j2d, wt, wm, P);
+      vop_adv_surf_s(sj, wt, wm, Ft);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Fn[k] = 0.0;
     } else {
 #pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          P.Ft[p][q] = tl[(18 + sym6(p, q)) * VBLK + t];
-          P.Fn[p][q] = tl[(24 + sym6(p, q)) * VBLK + t];
-        }
+      for (int k = 0; k < 6; ++k) {
+        Ft[k] = tl[(18 + k) * VBLK + t];
+        Fn[k] = tl[(24 + k) * VBLK + t];
+      }
     }
     if (l < L - 1) {
-      vop_adv_bot(j2d, wm, wtn, P);
+      vop_adv_bot_s(sj, wm, wtn, Fo, Fi);
     } else {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Fo[k] = Fi[k] = 0.0;
+    }
+    VDif D;
+    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, D);
+    // M1 - dt A_d of layer l and the coupling U = -dt u to layer l-1 (vimpl_blocks, with the
+    // -dt folded into the pieces): 24 entries of d, 12 of U (two symmetric blocks, packed)
+    double d[6][6], Uc[2][6];
+    {
+      double jz1[3];
+      layer_jz(C.b, e1, ft, fb, jz1);
+      const double q4 = 0.25 * D.cvol;
+      const double ht = l > 0 ? 0.5 * D.ct : 0.0, hb = l < L - 1 ? 0.5 * D.cb : 0.0;
+      const double r00 = ht - q4, r01 = q4 - ht, r10 = q4 - hb, r11 = hb - q4;
+      const double ptc = cdt * D.pt, pbc = cdt * D.pb, hca = 0.5 * cdt * D.ca;
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          P.Fi[p][q] = 0.0;
-          P.Fo[p][q] = 0.0;
+        for (int q = p; q < 3; ++q) {
+          const int k = sym6(p, q);
+          const double m1 = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+          const double Rc = cdt * V.R[p][q], mh = MHQ[p][q];
+          const double v00 = KM[0][0] * m1 + (((Sa[0][k] + r00 * Rc) - Ft[k]) - ptc * mh);
+          const double v01 = KM[0][1] * m1 + (Sa[1][k] + r01 * Rc);
+          const double v10 = KM[1][0] * m1 + (r10 * Rc - Sa[0][k]);
+          const double v11 = KM[1][1] * m1 + (((r11 * Rc - Sa[1][k]) + Fi[k]) - pbc * mh);
+          d[p][q] = d[q][p] = v00;
+          d[p][3 + q] = d[q][3 + p] = v01;
+          d[3 + p][q] = d[3 + q][p] = v10;
+          d[3 + p][3 + q] = d[3 + q][3 + p] = v11;
+          const double u0 = hca * Vp.R[p][q];
+          Uc[0][k] = u0;
+          Uc[1][k] = (ptc * mh - Fn[k]) - u0;
         }
     }
-    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, P);
-    double jz1[3], M1h[3][3];
-    layer_jz(C.b, e1, ft, fb, jz1);
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int q = p; q < 3; ++q) {
-        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
-        M1h[p][q] = s;
-        M1h[q][p] = s;
-      }
-    double d[6][6], Uc[2][3][3];
-    vimpl_blocks(l, L, Vp, V, P, P, M1h, dt, d, Uc[0], Uc[1]);
     double g[6][NC];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
@@ -1293,22 +1378,25 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
         for (int j = 0; j < 3; ++j) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][i][k % 3] * tl[(k * 3 + j) * VBLK + t];
+          for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][sym6(i, k % 3)] * tl[(k * 3 + j) * VBLK + t];
           Pm[i][j] = acc;
         }
-      // coupling of layer l-1 to l rebuilt from this layer's top-face pieces (bitwise the values
-      // layer l-1 would form: Fo_{l-1} = Ft_l, pb_{l-1} = pt_l, cn_{l-1} = ct_l, R_l):
-      // S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l}
+      // coupling of layer l-1 to l rebuilt from this layer's top-face pieces (the values layer l-1
+      // would form: Fo_{l-1} = Ft_l, pb_{l-1} = pt_l, cn_{l-1} = ct_l, R_l):
+      // S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_l
       double S0[3][3], S1h[3][3];
+      {
+        const double ptc = cdt * D.pt, ctc = cdt * D.ct;
 #pragma unroll
-      for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < 3; ++p)
 #pragma unroll
-        for (int q = p; q < 3; ++q) {
-          const double s0 = -dt * (P.Ft[p][q] + P.pt * MHQ[p][q]);
-          const double s1 = -dt * (P.ct * V.R[p][q]);
-          S1h[p][q] = S1h[q][p] = DV[1] * s1;    // W_bot = -DV1 S1  (sign folded below)
-          S0[p][q] = S0[q][p] = s0 - DV[0] * s1; // W_top = S0 - DV0 S1
-        }
+          for (int q = p; q < 3; ++q) {
+            const double s0 = Ft[sym6(p, q)] + ptc * MHQ[p][q];
+            const double s1 = ctc * V.R[p][q];
+            S1h[p][q] = S1h[q][p] = DV[1] * s1;    // W_bot = -DV1 S1  (sign folded below)
+            S0[p][q] = S0[q][p] = s0 - DV[0] * s1; // W_top = S0 - DV0 S1
+          }
+      }
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -1328,7 +1416,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
         for (int cc = 0; cc < NC; ++cc) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][i][k % 3] * gp[k][cc];
+          for (int k = 0; k < 6; ++k) acc = acc + Uc[k / 3][sym6(i, k % 3)] * gp[k][cc];
           g[i][cc] = g[i][cc] - acc;
         }
     }
@@ -1380,11 +1468,11 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
 #pragma unroll
         for (int q = p; q < 3; ++q) {
           const int k = sym6(p, q);
-          tl[(18 + k) * VBLK + t] = P.Fo[p][q];
-          tl[(24 + k) * VBLK + t] = P.Fi[p][q];
+          tl[(18 + k) * VBLK + t] = Fo[k];
+          tl[(24 + k) * VBLK + t] = Fi[k];
           if (!CT && act) {
-            gt[(size_t)(18 + k) * nt] = -dt * (P.Fo[p][q] + P.pb * MHQ[p][q]);
-            gt[(size_t)(24 + k) * nt] = -dt * (P.cn * Vn.R[p][q]);
+            gt[(size_t)(18 + k) * nt] = Fo[k] + (cdt * D.pb) * MHQ[p][q];
+            gt[(size_t)(24 + k) * nt] = D.cn * (cdt * Vn.R[p][q]);
           }
         }
     }
@@ -1484,29 +1572,27 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
     vgeo_x<true, NC == 1>(C, eta, ft, fb, a.vc, c, nt, Vl);
     double wm[6];
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
-    // Fo (vop_adv, bottom face of layer l) and the diffusion pieces cn, pb (vop_dif)
-    double Fo[3][3];
+    // Fo (bottom face of layer l, scaled by -dt as in the forward kernel) and the diffusion
+    // pieces cn, pb (vop_dif): S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}
+    const double cdt = -dt;
+    double Fo[6];
     {
-      double a3[6], b3[6], sout[6];
-      hq(wtn, a3);
-      hq(wm + 3, b3);
+      double e3[3];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const double sb = a3[q] - b3[q];
-        sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
-      }
-      face3(sout, Fo);
+      for (int k = 0; k < 3; ++k) e3[k] = wtn[k] - wm[3 + k];
+      face_pos_s(cdt * j2d, e3, Fo);
     }
     const double kb = a.kv + a.kh * Vl.bb, ktn = a.kv + a.kh * Vu.tt;
     const double cn = 0.5 * j2d * ktn;
     const double pb = 0.5 * (pen_sigma(Vu, Vl, a.n0, a.order, m.err) * fmax(ktn, kb) * Vu.nz * j2d);
+    const double pbc = cdt * pb, cnc = cdt * cn;
     double S0[3][3], S1[3][3];
 #pragma unroll
     for (int p = 0; p < 3; ++p)
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        S0[p][q] = -dt * (Fo[p][q] + pb * MHQ[p][q]);
-        S1[p][q] = -dt * (cn * Vu.R[p][q]);
+        S0[p][q] = Fo[sym6(p, q)] + pbc * MHQ[p][q];
+        S1[p][q] = cnc * Vu.R[p][q];
       }
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
@@ -1852,7 +1938,237 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, doubl
     V = Vn;
   }
 }
+inline size_t vexpl3_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1 + (nc == 1 ? 12 * VBLK : 0)) * 8; }
 inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1 + (nc == 1 ? 12 * VBLK : 0)) * 8; }
+
+// top face of layer l >= 1 (scaled): Ft (positive part, point-wise), Fn = whole - Ft
+__device__ __forceinline__ void vop_adv_top_s(double sj, const double wt[6], const double wm[6], double Ft[6],
+                                              double Fn[6]) {
+  double d3[3] = {wt[0] - wm[0], wt[1] - wm[1], wt[2] - wm[2]};
+  face_pos_s(sj, d3, Ft);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b)
+      Fn[sym6(a, b)] = sj * (T3[a][b][0] * d3[0] + T3[a][b][1] * d3[1] + T3[a][b][2] * d3[2]) - Ft[sym6(a, b)];
+}
+// y += M x for a packed symmetric 3x3 M
+__device__ __forceinline__ void smv_add(const double M[6], const double x[3], double y[3]) {
+  y[0] += M[0] * x[0] + M[3] * x[1] + M[4] * x[2];
+  y[1] += M[3] * x[0] + M[1] * x[1] + M[5] * x[2];
+  y[2] += M[4] * x[0] + M[5] * x[1] + M[2] * x[2];
+}
+
+// EXPLICIT, assembled: x = M1^-1 (rhs + dt A xin).  The blocks of dt A (the four 3x3 blocks of
+// the diagonal block, the coupling U to layer l-1 and W to layer l+1 -- all symmetric, packed:
+// vop_blocks' 72 entries as 48 words) are formed once per layer from the dt-scaled pieces and
+// applied to every component (72 FMAs per component instead of ~180 for the matrix-free form).
+// Per-layer inputs stream through the 3-deep cp.async ring of k_vexpl2; NC == 1 carries the
+// interface face masses from the layer above in shared memory (FCS, see k_vimpl_fwd).
+template <int NC, int MINB>
+__global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, double dt, const double* rhs,
+                                                     const double* __restrict__ xin, double* x) {
+  constexpr int NE = 12 * NC + 6;  // rhs, xin, w~
+  extern __shared__ double smem[];
+  double* ring = smem;             // [3][NE][VBLK]
+  double* cst = smem + 3 * NE * VBLK;  // [NCS][VBLK] column constants
+  double* fr = cst + NCS * VBLK;
+  constexpr bool FCS = NC == 1;
+  double* fc = fr + m.L + 1;       // [12][VBLK] carried face pieces (FCS)
+  const int t = threadIdx.x;
+  const int c = blockIdx.x * VBLK + t;
+  const int nt = m.nt, L = m.L;
+  for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
+  __syncthreads();
+  if (c >= m.nown) return;
+  const size_t P6 = (size_t)6 * L * nt;
+  auto stage = [&](int l) {
+    if (l < L) {
+      unsigned ln = (unsigned)L * (unsigned)nt;
+      asm volatile("" : "+r"(ln));
+      const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
+      double* s = ring + (l % 3) * NE * VBLK + t;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const size_t o = cc * P6 + (i * ln + lo);
+          cp_async8(s + (cc * 6 + i) * VBLK, rhs + o);
+          cp_async8(s + (6 * NC + cc * 6 + i) * VBLK, xin + o);
+        }
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + (i * ln + lo));
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  stage(1);
+  Col C;
+  load_col(m, c, C);
+  double eta[3], e0[3], e1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    eta[k] = a.eta_u[k * nt + c];
+    e0[k] = a.eta0[k * nt + c];
+    e1[k] = a.eta1[k * nt + c];
+  }
+  cs_put(cst, t, C, eta, e0, e1);
+  constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
+  constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
+  VG Vp, V, Vn;
+  vgeo_x<true, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
+  Vp = V;
+  Vn = V;
+  double xa[NC][6];   // xin of layer l-1: its ring slot is refilled at the top of iteration l
+  for (int l = 0; l < L; ++l) {
+    cs_get(cst, t, C, eta, e0, e1);
+    const double j2d = C.j2d;
+    if (l > 0) {
+      const double* prv = ring + ((l + 2) % 3) * NE * VBLK + t;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) xa[cc][k] = prv[(6 * NC + cc * 6 + k) * VBLK];
+    }
+    stage(l + 2);
+    cp_async_wait1();
+    const double* cur = ring + (l % 3) * NE * VBLK + t;
+    const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
+    const double ft = fr[l], fb = fr[l + 1];
+    if (l < L - 1) vgeo_x<true, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
+    double wt[6], wm[6], wtn[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
+    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if (l < L - 1) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wtn[k] = nxt[(12 * NC + k) * VBLK];
+    }
+    const double sj = dt * j2d;
+    double Sa[2][6], Ft[6], Fn[6], Fo[6], Fi[6];
+    vop_adv_vol_s(sj, wt, wm, Sa);
+    if (l == 0) {
+      vop_adv_surf_s(sj, wt, wm, Ft);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Fn[k] = 0.0;
+    } else if (FCS) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        Ft[k] = fc[k * VBLK + t];
+        Fn[k] = fc[(6 + k) * VBLK + t];
+      }
+    } else {
+      vop_adv_top_s(sj, wt, wm, Ft, Fn);
+    }
+    if (l < L - 1) {
+      vop_adv_bot_s(sj, wm, wtn, Fo, Fi);
+      if (FCS) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          fc[k * VBLK + t] = Fo[k];
+          fc[(6 + k) * VBLK + t] = Fi[k];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Fo[k] = Fi[k] = 0.0;
+    }
+    VDif D;
+    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, D);
+    // dt A: diagonal blocks B00, B01, B10, B11, coupling U0, U1 (layer l-1), W0, W1 (layer l+1)
+    double B[4][6], U[2][6], W[2][6];
+    {
+      const double q4 = 0.25 * D.cvol;
+      const double ht = l > 0 ? 0.5 * D.ct : 0.0, hb = l < L - 1 ? 0.5 * D.cb : 0.0;
+      const double r00 = ht - q4, r01 = q4 - ht, r10 = q4 - hb, r11 = hb - q4;
+      const double ptc = dt * D.pt, pbc = dt * D.pb, hca = 0.5 * dt * D.ca, hcn = 0.5 * dt * D.cn;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = p; q < 3; ++q) {
+          const int k = sym6(p, q);
+          const double Rc = dt * V.R[p][q], mh = MHQ[p][q];
+          B[0][k] = ((Sa[0][k] + r00 * Rc) - Ft[k]) - ptc * mh;
+          B[1][k] = Sa[1][k] + r01 * Rc;
+          B[2][k] = r10 * Rc - Sa[0][k];
+          B[3][k] = ((r11 * Rc - Sa[1][k]) + Fi[k]) - pbc * mh;
+          const double u0 = hca * Vp.R[p][q], w1 = hcn * Vn.R[p][q];
+          U[0][k] = u0;
+          U[1][k] = (ptc * mh - Fn[k]) - u0;
+          W[0][k] = (Fo[k] + pbc * mh) - w1;
+          W[1][k] = w1;
+        }
+    }
+    double jz1[3], A1[3][3];
+    layer_jz(C.b, e1, ft, fb, jz1);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p; q < 3; ++q) {
+        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
+        A1[p][q] = s;
+        A1[q][p] = s;
+      }
+    const double r0 = drcp(A1[0][0]);
+    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
+    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
+    const double a22p = A1[2][2] - l20 * A1[0][2];
+    const double r1 = drcp(a11);
+    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
+    const double r2 = drcp(a22p - l21 * a12);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      double yt[3], yb[3], xt[3], xb[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        yt[k] = cur[(cc * 6 + k) * VBLK];
+        yb[k] = cur[(cc * 6 + 3 + k) * VBLK];
+        xt[k] = cur[(6 * NC + cc * 6 + k) * VBLK];
+        xb[k] = cur[(6 * NC + cc * 6 + 3 + k) * VBLK];
+      }
+      smv_add(B[0], xt, yt);
+      smv_add(B[1], xb, yt);
+      smv_add(B[2], xt, yb);
+      smv_add(B[3], xb, yb);
+      if (l > 0) {
+        smv_add(U[0], xa[cc], yt);
+        smv_add(U[1], xa[cc] + 3, yt);
+      }
+      if (l < L - 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          xt[k] = nxt[(6 * NC + cc * 6 + k) * VBLK];
+          xb[k] = nxt[(6 * NC + cc * 6 + 3 + k) * VBLK];
+        }
+        smv_add(W[0], xt, yb);
+        smv_add(W[1], xb, yb);
+      }
+      double o[6];
+#pragma unroll
+      for (int lev = 0; lev < 2; ++lev) {
+        double z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) z[k] = lev == 0 ? ki00 * yt[k] + ki01 * yb[k] : ki10 * yt[k] + ki11 * yb[k];
+        z[1] -= l10 * z[0];
+        z[2] -= l20 * z[0] + l21 * z[1];
+        z[2] *= r2;
+        z[1] = (z[1] - a12 * z[2]) * r1;
+        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
+      }
+      {
+        unsigned ln = (unsigned)L * (unsigned)nt;
+        asm volatile("" : "+r"(ln));
+        const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
+#pragma unroll
+        for (int n = 0; n < 6; ++n) x[cc * P6 + (n * ln + lo)] = o[n];
+      }
+    }
+    Vp = V;
+    V = Vn;
+  }
+}
 
 // EXPLICIT stage for momentum (2 comps) AND tracer in one pass: the geometry window, the
 // advective pieces of A and the M1 factorisation are shared; only the diffusion pieces differ.
@@ -2128,6 +2444,18 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
       DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 1)
     }
 #undef LAUNCH_ARGS
+  } else if (!implicit && tune_get(TUNE_VSPLIT) >= 3 && kh == 0.0 && tune_get(TUNE_VASM) == 1) {
+    // assembled explicit stage (TUNE_VASM 1, default)
+    const size_t sm = vexpl3_smem(ncomp, ctx->L);
+    static unsigned long long attr = 0;
+    if (first_on_device(attr)) {
+      cudaFuncSetAttribute(k_vexpl3<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl3_smem(2, 4096));
+      cudaFuncSetAttribute(k_vexpl3<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl3_smem(1, 4096));
+    }
+    if (ncomp == 2)
+      k_vexpl3<2, 1><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
+    else
+      k_vexpl3<1, 1><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
   } else if (!implicit && tune_get(TUNE_VSPLIT) >= 3) {
     const size_t sm = vexpl2_smem(ncomp, ctx->L);
 #define LAUNCH_EX(NCV, MB)                                                                                           \

@@ -11,6 +11,8 @@ library for A/B runs (scripts/ab_tune.py) and must keep producing the same answe
   key 6  2D RK stage occupancy variant (register allocation can change FMA contraction)
   key 12 bit 1: cp.async.bulk (copy-engine) staging ring + mbarriers in the implicit forward
          elimination instead of per-thread cp.async (900 columns: the last block splits a warp)
+  key 13 explicit vertical stage: 1 blocks of dt A assembled once per layer and applied per
+         component (k_vexpl3), 0 matrix-free (k_vexpl2)
 Tile-staged and register kernels do the same arithmetic (bitwise equal), except the tile-staged
 F3D->2D kernel, which forms the column sum per horizontal node (rounding-level difference); the
 split Thomas and the branch-free reciprocals of the staged vertical kernels differ at rounding level.
@@ -20,7 +22,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-KEYS = (1, 2, 5, 6, 7, 9, 10, 11, 12)
+KEYS = (1, 2, 5, 6, 7, 9, 10, 11, 12, 13)
 
 
 @pytest.fixture(scope="module")
@@ -63,6 +65,7 @@ def rel(a, b):
     ({5: 1}, 1e-12), ({10: 128}, 1e-12),
     ({6: 0}, 1e-12), ({6: 3}, 1e-12),
     ({12: 3}, 0.0),     # bulk-copy (TMA) ring of the implicit forward elimination: same arithmetic
+    ({13: 0}, 1e-12),   # matrix-free explicit vertical stage
 ])
 def test_variant_matches_default(case, setting, tol):
     pdg, c, lib, defaults = case
