@@ -176,6 +176,28 @@ __device__ __forceinline__ void lat_add(double acc[6], int k, const double x[2][
     }
 }
 
+// the projection of lat_add without the accumulation: p[lev][hn] = sum_vh VS[v][lev] ES[h][hn] x[v][h]
+// (a vector face field n_d x is then projected once and added with the factors s n_d)
+__device__ __forceinline__ void lat_proj(const double x[2][2], double p[2][2]) {
+#pragma unroll
+  for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+    for (int hn = 0; hn < 2; ++hn) {
+      double t = 0.0;
+#pragma unroll
+      for (int vv = 0; vv < 2; ++vv)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) t += VS[vv][lev] * ES[h][hn] * x[vv][h];
+      p[lev][hn] = t;
+    }
+}
+__device__ __forceinline__ void lat_put(double acc[6], int k, const double p[2][2], double s) {
+#pragma unroll
+  for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+    for (int hn = 0; hn < 2; ++hn) acc[3 * lev + (hn == 0 ? EV0(k) : EV1(k))] += s * p[lev][hn];
+}
+
 // per-column neighbour data of one interior edge, loaded once per column
 struct EdgeNb {
   int e2, k2;

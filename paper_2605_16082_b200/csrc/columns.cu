@@ -376,6 +376,12 @@ __device__ __forceinline__ void vgeo(const Col& C, const double eta[3], double f
 // geometry from them with 6 multiplications and one reciprocal instead of 6 reciprocals and the
 // 6-point contractions (the values agree with vgeo to rounding).
 constexpr int NVC = 8;
+// momentum implicit solve (split forward elimination / back substitution) in the sigma form as
+// well (-82 FP64 per layer, measured -2 %); the assembled explicit stage measured +1.5 % with it
+#ifndef PDG_SIGU
+#define PDG_SIGU 1
+#endif
+constexpr bool SIGU = PDG_SIGU != 0;
 __global__ void k_vcol(DMesh m, const double* __restrict__ eta_u, double* __restrict__ vc) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
@@ -449,9 +455,6 @@ __device__ __forceinline__ double pen_sigma(const VG& A, const VG& B, double n0,
   return n0 * ((order + 1.0) * (order + 3.0) / 6.0) * fmax(A.rhgt, B.rhgt);
 }
 
-__device__ __forceinline__ int sym6(int a, int b) {  // packed index of a symmetric 3x3
-  return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
-}
 
 // F(x) for x at the 6 points, symmetric
 __device__ __forceinline__ void face3(const double x[6], double F[3][3]) {
@@ -1281,7 +1284,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   }
   cs_put(cst, t, C, eta, e0, e1);
   VG Vp, V, Vn;
-  vgeo_x<KH0, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
+  vgeo_x<KH0, (NC == 1 || SIGU)>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
   Vp = V;
   Vn = V;
   double gp[6][NC];
@@ -1299,7 +1302,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     const double* cur = ring + (l % 3) * NE * VBLK + t;
     const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
     const double ft = fr[l], fb = fr[l + 1];
-    if (l < L - 1) vgeo_x<KH0, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
+    if (l < L - 1) vgeo_x<KH0, (NC == 1 || SIGU)>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(6 * NC + i) * VBLK];
@@ -1531,7 +1534,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, con
 // the mesh velocity with the forward kernel's own functions -- 12 fewer words written and read
 // per prism for ~200 FP64 operations in a kernel whose FP64 pipe is otherwise idle.
 template <int NC>
-__global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double dt, const double* __restrict__ Gs,
+__global__ void __launch_bounds__(VBLK, NC == 1 ? 3 : 1) k_vimpl_bwd_r(DMesh m, VopArgs a, double dt, const double* __restrict__ Gs,
                                                     double* x) {
   const int c = blockIdx.x * VBLK + threadIdx.x;
   const int nt = m.nt, L = m.L;
@@ -1548,7 +1551,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
   }
   const double j2d = C.j2d;
   VG Vu;  // geometry of layer l + 1
-  vgeo_x<true, NC == 1>(C, eta, m.fracs[L - 1], m.fracs[L], a.vc, c, nt, Vu);
+  vgeo_x<true, (NC == 1 || SIGU)>(C, eta, m.fracs[L - 1], m.fracs[L], a.vc, c, nt, Vu);
   double xn[6][NC];
 #pragma unroll
   for (int i = 0; i < 6; ++i)
@@ -1569,7 +1572,7 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd_r(DMesh m, VopArgs a, double
     for (int k = 0; k < 3; ++k) wtn[k] = __ldg(a.wt + pix(k, l + 1, c, L, nt));
     const double ft = m.fracs[l], fb = m.fracs[l + 1];
     VG Vl;
-    vgeo_x<true, NC == 1>(C, eta, ft, fb, a.vc, c, nt, Vl);
+    vgeo_x<true, (NC == 1 || SIGU)>(C, eta, ft, fb, a.vc, c, nt, Vl);
     double wm[6];
     wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     // Fo (bottom face of layer l, scaled by -dt as in the forward kernel) and the diffusion
@@ -2365,7 +2368,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
   // the sigma-form column constants are read by the tracer (NC = 1) kernels only
-  if (ncomp == 1 && kh == 0.0 && (implicit ? tune_get(TUNE_VSPLIT) >= 2 : tune_get(TUNE_VSPLIT) >= 3)) {
+  if ((ncomp == 1 || (SIGU && implicit)) && kh == 0.0 && (implicit ? tune_get(TUNE_VSPLIT) >= 2 : tune_get(TUNE_VSPLIT) >= 3)) {
     double* vc = ctx->vcol();
     if (!vc) return PDG_ERR_CUDA;
     k_vcol<<<nblocks(ctx->nown, 256), 256, 0, strm>>>(m, eta_u, vc);

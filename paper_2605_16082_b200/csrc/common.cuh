@@ -176,6 +176,10 @@ __device__ __forceinline__ void load_col2(const DMesh& m, int c, Col2& C) {
   }
 }
 
+__host__ __device__ __forceinline__ constexpr int sym6(int a, int b) {  // packed index of a symmetric 3x3
+  return a == b ? a : 3 + a + b - 1;                  // (0,0)0 (1,1)1 (2,2)2 (0,1)3 (0,2)4 (1,2)5
+}
+
 // ---------------------------------------------------------------- small helpers
 // values at the 6 horizontal points of a corner field (c3 @ BARY.T)
 __device__ __forceinline__ void hq(const double c3[3], double out[6]) {

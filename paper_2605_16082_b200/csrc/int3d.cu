@@ -407,18 +407,16 @@ __global__ void __launch_bounds__(128, MINB) k_compute_r(DMesh m, const double* 
         for (int n = 0; n < 4; ++n) n4[n] = -alpha * (n4[n] - tref);
       }
       tr_jump(rho, k, n4, dj);
-      double xx[2][2], xy[2][2];
+      // one scalar face field projected once, added with g Je n_d (as k_compute_r_t: bitwise equal)
+      double xs[2][2], pr[2][2];
 #pragma unroll
       for (int vv = 0; vv < 2; ++vv)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double x = dj[vv][h] * (jm * E[k].hm[h]);
-          xx[vv][h] = C.nx[k] * x;
-          xy[vv][h] = C.ny[k] * x;
-        }
-      const double je = 0.5 * C.el[k];
-      lat_add(acc[0], k, xx, g * je);
-      lat_add(acc[1], k, xy, g * je);
+        for (int h = 0; h < 2; ++h) xs[vv][h] = dj[vv][h] * (jm * E[k].hm[h]);
+      lat_proj(xs, pr);
+      const double gje = g * (0.5 * C.el[k]);
+      lat_put(acc[0], k, pr, gje * C.nx[k]);
+      lat_put(acc[1], k, pr, gje * C.ny[k]);
     }
     // surface fold: -Mh (g rho_s grad_h eta)
     if (l == 0) {
@@ -874,18 +872,16 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
           for (int n = 0; n < 4; ++n) n4[n] = -alpha * (n4[n] - tref);
         }
         tr_jump(rho, k, n4, dj);
-        double xx[2][2], xy[2][2];
+        // g n [[rho']] {Jz} Jedge: one scalar face field projected once, added with g Je n_d
+        double xs[2][2], pr[2][2];
 #pragma unroll
         for (int vv = 0; vv < 2; ++vv)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double x = dj[vv][h] * (jm * E[k].hm[h]);
-            xx[vv][h] = C.nx[k] * x;
-            xy[vv][h] = C.ny[k] * x;
-          }
-        const double je = 0.5 * C.el[k];
-        lat_add(acc[0], k, xx, g * je);
-        lat_add(acc[1], k, xy, g * je);
+          for (int h = 0; h < 2; ++h) xs[vv][h] = dj[vv][h] * (jm * E[k].hm[h]);
+        lat_proj(xs, pr);
+        const double gje = g * (0.5 * C.el[k]);
+        lat_put(acc[0], k, pr, gje * C.nx[k]);
+        lat_put(acc[1], k, pr, gje * C.ny[k]);
       }
       if (l == 0) {
         double mr[3];
@@ -1340,7 +1336,10 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 // for the whole layer loop; 64-thread blocks keep the static footprint under 48 KB.
 namespace shf {
 enum { J2D = 0, DX = 1, DY = 4, EL = 7, NX = 10, NY = 13, B = 16, ETA = 19, STAB = 22, MO = 28, MN = 34, E0 = 46,
-       E1 = 49, F1 = 52, N = 58 };
+       E1 = 49, F1 = 52, N = 58,
+       // MODE 2: the per-column sigma-layer triangle masses Mjz(H) of the three grids (packed
+       // symmetric), over the B / ETA and E0 / E1 words (the layer loop needs only these)
+       MHU = 16, MH0 = 46, MH1 = 58, N2 = 64 };
 }
 
 __device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, double st1, int k, double jm,
@@ -1363,7 +1362,7 @@ __device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, d
 // the u words already loaded for the fluxes instead of loading them again
 template <int NC, int MODE, int MINB, bool SAME = false>
 __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
-  __shared__ double sdm[shf::N * 64];
+  __shared__ double sdm[(MODE == 2 ? shf::N2 : shf::N) * 64];
   __shared__ int sim[9 * 64];
   const int tid = threadIdx.x;
   const int i = blockIdx.x * 64 + tid;
@@ -1410,17 +1409,28 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
       }
     }
     if (MODE == 2) {
+      // sigma layers: Jz = (f_b - f_t) H / 2 = jm H at every point, so each layer's triangle mass
+      // is jm Mjz(H) with a per-column Mjz(H) (values equal the per-layer forms up to rounding)
+      double Hu[3], H0[3], H1[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        SD(shf::E0 + k) = a.eta0[k * nt + c];
         const double e1 = a.eta1[k * nt + c];
-        SD(shf::E1 + k) = e1;
+        Hu[k] = eta[k] - C.b[k];
+        H0[k] = a.eta0[k * nt + c] - C.b[k];
+        H1[k] = e1 - C.b[k];
         if constexpr (NC >= 2) {
-          const double H1 = e1 - C.b[k];
-          SD(shf::F1 + k) = a.f2d[k * nt + c] / H1;
-          SD(shf::F1 + 3 + k) = a.f2d[(3 + k) * nt + c] / H1;
+          SD(shf::F1 + k) = a.f2d[k * nt + c] / H1[k];
+          SD(shf::F1 + 3 + k) = a.f2d[(3 + k) * nt + c] / H1[k];
         }
       }
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = p; q < 3; ++q) {
+          SD(shf::MHU + sym6(p, q)) = T3[p][q][0] * Hu[0] + T3[p][q][1] * Hu[1] + T3[p][q][2] * Hu[2];
+          SD(shf::MH0 + sym6(p, q)) = T3[p][q][0] * H0[0] + T3[p][q][1] * H0[1] + T3[p][q][2] * H0[2];
+          SD(shf::MH1 + sym6(p, q)) = T3[p][q][0] * H1[0] + T3[p][q][1] * H1[1] + T3[p][q][2] * H1[2];
+        }
     }
   }
   double csum[NC][3];
@@ -1515,19 +1525,32 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         lat_add(acc[cc], k, x, je);
       }
     }
-    double bb[3], eta[3];
+    // per-layer triangle masses: MODE 2 from the per-column sigma forms (scaled by jm below)
+    auto msym = [&](int w, double M[3][3]) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      bb[k] = SD(shf::B + k);
-      eta[k] = SD(shf::ETA + k);
-    }
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) M[p][q] = SD(w + sym6(p, q));
+    };
     if constexpr (NC >= 2) {
       double rr[2][6];
       ld6g_o(a.r, lo, ln, rr[0]);
       ld6g_o(a.r + P6, lo, ln, rr[1]);
-      double jz[3], Mu[3][3];
-      layer_jz(bb, eta, ft, fb, jz);
-      mjz(jz, Mu);
+      double Mu[3][3];
+      double mscale = SD(shf::J2D);
+      if (MODE == 2) {
+        msym(shf::MHU, Mu);
+        mscale = jm * mscale;
+      } else {
+        double jz[3], bb[3], eta[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          bb[k] = SD(shf::B + k);
+          eta[k] = SD(shf::ETA + k);
+        }
+        layer_jz(bb, eta, ft, fb, jz);
+        mjz(jz, Mu);
+      }
       const double ir = 1.0 / a.rho0;
       double y0[6], y1[6], m0[6], m1[6];
 #pragma unroll
@@ -1536,8 +1559,8 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         y1[n] = -a.f * u[0][n] - rr[1][n] * ir;
       }
       const double j2d = SD(shf::J2D);
-      kron_apply(Mu, j2d, y0, m0);
-      kron_apply(Mu, j2d, y1, m1);
+      kron_apply(Mu, mscale, y0, m0);
+      kron_apply(Mu, mscale, y1, m1);
 #pragma unroll
       for (int n = 0; n < 6; ++n) {
         acc[0][n] += m0[n];
@@ -1575,19 +1598,14 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
     } else {
       const double j2d = SD(shf::J2D);
-      double e0[3], j0[3], M0[3][3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) e0[k] = SD(shf::E0 + k);
-      layer_jz(bb, e0, ft, fb, j0);
-      mjz(j0, M0);
+      const double jj = jm * j2d;
+      double M0[3][3];
+      msym(shf::MH0, M0);
       double mf[2][3] = {{0, 0, 0}, {0, 0, 0}};
       if constexpr (NC >= 2) {
-        double e1[3], j1[3], M1[3][3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) e1[k] = SD(shf::E1 + k);
-        layer_jz(bb, e1, ft, fb, j1);
-        mjz(j1, M1);
-        const double kk = (KM[0][0] + KM[0][1]) * j2d;
+        double M1[3][3];
+        msym(shf::MH1, M1);
+        const double kk = (KM[0][0] + KM[0][1]) * jj;
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const double F0 = SD(shf::F1 + cc * 3), F1v = SD(shf::F1 + cc * 3 + 1), F2 = SD(shf::F1 + cc * 3 + 2);
@@ -1604,7 +1622,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         } else {
           ld6g_o(a.u0c[cc], lo, ln, x0);
         }
-        kron_apply(M0, j2d, x0, m0x);
+        kron_apply(M0, jj, x0, m0x);
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
           if (NC >= 2 && cc < 2)
@@ -1710,11 +1728,15 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
     }
   }
   const double j2d = act ? C.j2d : 0.0;
-  double csum[NC][3];
+  double csum[NC][3], sv[NC][2], ysum[2][3];
 #pragma unroll
-  for (int cc = 0; cc < NC; ++cc)
+  for (int cc = 0; cc < NC; ++cc) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
+    sv[cc][0] = sv[cc][1] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ysum[0][k] = ysum[1][k] = 0.0;
   cp_async_wait0();
   __syncthreads();
   double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
@@ -1753,7 +1775,6 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
       // two levels of the phi_z test functions collapse (sum_m K3[m] = KM, sum_lev VS[v][lev] = 1,
       // KM column sums = 1), so the volume, lateral and mass terms are formed per horizontal node
       // only (cs[cc][p]); the values equal the per-node forms summed, up to rounding.
-      double cs[NC][3];
       if constexpr (MODE == 1) {
         double z[2][2][3];
 #pragma unroll
@@ -1774,8 +1795,9 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
                     u[cc][3 * l1] * z[d][l2][0] + u[cc][3 * l1 + 1] * z[d][l2][1] + u[cc][3 * l1 + 2] * z[d][l2][2];
             Sd[d] = KM[0][0] * dot[0][0] + KM[0][1] * dot[0][1] + KM[1][0] * dot[1][0] + KM[1][1] * dot[1][1];
           }
-#pragma unroll
-          for (int p = 0; p < 3; ++p) cs[cc][p] = j2d * (C.dx[p] * Sd[0] + C.dy[p] * Sd[1]);
+          // J2D grad phi_p . Sd is linear in Sd: summed over the layers, applied once per column
+          sv[cc][0] += Sd[0];
+          sv[cc][1] += Sd[1];
         }
       } else {
         double z[2][2][3];
@@ -1846,8 +1868,8 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
             for (int h = 0; h < 2; ++h) x[vv][h] = (f[vv][h] >= 0.0 ? ti[vv][h] : te[vv][h]) * f[vv][h];
           if constexpr (MODE == 1) {   // both levels of edge node hn: sum_vh ES[h][hn] x[v][h]
             const double x0 = x[0][0] + x[1][0], x1 = x[0][1] + x[1][1];
-            cs[cc][EV0(k)] += je * (ES[0][0] * x0 + ES[1][0] * x1);
-            cs[cc][EV1(k)] += je * (ES[0][1] * x0 + ES[1][1] * x1);
+            csum[cc][EV0(k)] += je * (ES[0][0] * x0 + ES[1][0] * x1);
+            csum[cc][EV1(k)] += je * (ES[0][1] * x0 + ES[1][1] * x1);
           } else {
             lat_add(acc[cc], k, x, je);
           }
@@ -1857,30 +1879,27 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
         double rr[2][6];
         ld6g(a.r, l, c, L, nt, rr[0]);
         ld6g(a.r + P6, l, c, L, nt, rr[1]);
-        double jz[3], Mu[3][3];
-        layer_jz(C.b, eta, ft, fb, jz);
-        mjz(jz, Mu);
         const double ir = 1.0 / a.rho0;
-        if constexpr (MODE == 1) {   // column sum of (K (x) J2D Mjz) y = J2D Mjz (y_top + y_bot)
-          double ys0[3], ys1[3];
+        if constexpr (MODE == 1) {
+          // column sum of (K (x) J2D Mjz) y = J2D Mjz (y_top + y_bot); on sigma layers
+          // Mjz = (f_b - f_t)/2 Mjz(H) = jm Mjz(H), so jm (y_top + y_bot) is summed over the
+          // layers and J2D Mjz(H) applied once per column
 #pragma unroll
           for (int n = 0; n < 3; ++n) {
-            ys0[n] = a.f * (u[1][n] + u[1][3 + n]) - (rr[0][n] + rr[0][3 + n]) * ir;
-            ys1[n] = -a.f * (u[0][n] + u[0][3 + n]) - (rr[1][n] + rr[1][3 + n]) * ir;
-          }
-#pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            cs[0][p] += j2d * (Mu[p][0] * ys0[0] + Mu[p][1] * ys0[1] + Mu[p][2] * ys0[2]);
-            cs[1][p] += j2d * (Mu[p][0] * ys1[0] + Mu[p][1] * ys1[1] + Mu[p][2] * ys1[2]);
+            ysum[0][n] += jm * (a.f * (u[1][n] + u[1][3 + n]) - (rr[0][n] + rr[0][3 + n]) * ir);
+            ysum[1][n] += jm * (-a.f * (u[0][n] + u[0][3 + n]) - (rr[1][n] + rr[1][3 + n]) * ir);
           }
           if (l == 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-              cs[0][k] += j2d / 6.0 * a.tsx;
-              cs[1][k] += j2d / 6.0 * a.tsy;
+              csum[0][k] += j2d / 6.0 * a.tsx;
+              csum[1][k] += j2d / 6.0 * a.tsy;
             }
           }
         } else {
+        double jz[3], Mu[3][3];
+        layer_jz(C.b, eta, ft, fb, jz);
+        mjz(jz, Mu);
         double y0[6], y1[6], m0[6], m1[6];
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
@@ -1916,8 +1935,8 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
             if constexpr (MODE == 1) {
-              cs[0][k] += mx[k];
-              cs[1][k] += my[k];
+              csum[0][k] += mx[k];
+              csum[1][k] += my[k];
             } else {
               acc[0][3 + k] += mx[k];
               acc[1][3 + k] += my[k];
@@ -1925,12 +1944,7 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
           }
         }
       }
-      if constexpr (MODE == 1) {
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) csum[cc][k] += cs[cc][k];
-      } else {
+      if constexpr (MODE != 1) {
         double j0[3], M0[3][3];
         layer_jz(C.b, eta0, ft, fb, j0);
         mjz(j0, M0);
@@ -1966,6 +1980,21 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
     __syncthreads();
   }
   if (MODE == 1 && act) {
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) csum[cc][p] += j2d * (C.dx[p] * sv[cc][0] + C.dy[p] * sv[cc][1]);
+    if constexpr (NC >= 2) {
+      double H[3], MH[3][3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) H[k] = eta[k] - C.b[k];
+      mjz(H, MH);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        csum[0][p] += j2d * (MH[p][0] * ysum[0][0] + MH[p][1] * ysum[0][1] + MH[p][2] * ysum[0][2]);
+        csum[1][p] += j2d * (MH[p][0] * ysum[1][0] + MH[p][1] * ysum[1][1] + MH[p][2] * ysum[1][2]);
+      }
+    }
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
