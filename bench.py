@@ -48,7 +48,6 @@ KERNEL_BYTES = {
     "vertical_T_impl": 48 + 48 + 48,
     "vertical_u_expl": 96 + 48 + 96 + 96,   # + u for A u
     "vertical_T_expl": 48 + 48 + 48 + 48,
-    "vertical_uT_expl": 96 + 48 + 96 + 96 + 48 * 3,
 }
 # 2D sub-cycle, SURVEY.md section 8d model M2: per triangle and SSP-RK3 substep 3 evaluations x
 # (state 72 + geometry incl. b 194) + 2 x 72 substep-start reads + 3 x 72 writes + 96 Qbar = 1254 B.

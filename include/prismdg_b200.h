@@ -271,10 +271,6 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
 int pdg_step_diagnostics(pdg_ctx* ctx, const double* S, const double* u, const double* T, double g, double* work,
                          double* out, void* stream);
 int pdg_diagnostics_work_doubles(pdg_ctx* ctx);
-int pdg_step_vertical_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, double dt_mesh,
-                         const double* wt, double kh_u, double kv_u, double kh_T, double kv_T, double n0, int order,
-                         double dt, const double* rhs_u, const double* xin_u, double* x_u, const double* rhs_T,
-                         const double* xin_T, double* x_T, void* stream);
 
 #ifdef __cplusplus
 }

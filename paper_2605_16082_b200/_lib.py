@@ -87,7 +87,6 @@ _SIGS = {
     "pdg_step_vertical": (I, [P, I, I, P, P, P, D, P, D, D, D, I, D, P, P, P, P]),
     "pdg_step_diagnostics": (I, [P, P, P, P, D, P, P, P]),
     "pdg_diagnostics_work_doubles": (I, [P]),
-    "pdg_step_vertical_ut": (I, [P, P, P, P, D, P, D, D, D, D, D, I, D, P, P, P, P, P, P, P]),
 }
 
 _lib = None

@@ -487,60 +487,6 @@ struct VDif {
 };
 struct VPieces : VAdv, VDif {};
 
-// advective volume pieces Sa only
-__device__ __forceinline__ void vop_adv_vol(double j2d, const double wt[6], const double wm[6], VAdv& P) {
-  double dwt[3], dwb[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    dwt[c] = wt[c] - wm[c];
-    dwb[c] = wt[3 + c] - wm[3 + c];
-  }
-#pragma unroll
-  for (int mm = 0; mm < 2; ++mm) {
-    double y[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) y[c] = j2d * (KM[mm][0] * dwt[c] + KM[mm][1] * dwb[c]);
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = a; b < 3; ++b) {
-        const double s = T3[a][b][0] * y[0] + T3[a][b][1] * y[1] + T3[a][b][2] * y[2];
-        P.Sa[mm][a][b] = s;
-        P.Sa[mm][b][a] = s;
-      }
-  }
-}
-// bottom face of layer l < L-1 (the interface with layer l+1): outflow part Fo (positive speed,
-// point-wise) and inflow part Fi = whole - Fo (closed-form P1 face mass)
-__device__ __forceinline__ void vop_adv_bot(double j2d, const double wm[6], const double wtn[3], VAdv& P) {
-  double a3[6], b3[6], sout[6], e3[3];
-  hq(wtn, a3);
-  hq(wm + 3, b3);
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    const double sb = a3[q] - b3[q];
-    sout[q] = j2d * (sb > 0.0 ? sb : 0.0);
-  }
-  face3(sout, P.Fo);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) e3[c] = wtn[c] - wm[3 + c];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = a; b < 3; ++b) {
-      const double w = j2d * (T3[a][b][0] * e3[0] + T3[a][b][1] * e3[1] + T3[a][b][2] * e3[2]);
-      P.Fi[a][b] = w - P.Fo[a][b];
-      P.Fi[b][a] = P.Fi[a][b];
-    }
-}
-// surface (l == 0): the whole speed leaves through the top face; Fn unused
-__device__ __forceinline__ void vop_adv_surf(double j2d, const double wt[6], const double wm[6], VAdv& P) {
-  double sp[6], d3[3] = {wt[0] - wm[0], wt[1] - wm[1], wt[2] - wm[2]};
-  hq(d3, sp);
-#pragma unroll
-  for (int q = 0; q < 6; ++q) sp[q] = j2d * sp[q];
-  face3(sp, P.Ft);
-}
 
 // The same pieces pre-multiplied by a scale (the implicit elimination passes c = -dt, so every
 // block entry of M1 - dt A is one FMA chain without the final -dt multiplication): Sa comes out
@@ -749,59 +695,6 @@ __device__ __forceinline__ void mv3(const double M[3][3], const double x[3], dou
   for (int a = 0; a < 3; ++a) y[a] = M[a][0] * x[0] + M[a][1] * x[1] + M[a][2] * x[2];
 }
 
-// y = A x for layer l, matrix free: x rows of layers l-1 (xa), l (xc), l+1 (xb), 6 nodes each
-__device__ __forceinline__ void vop_apply(int l, int L, const VG& Vp, const VG& V, const VG& Vn, const VAdv& A,
-                                          const VDif& D, const double xa[6], const double xc[6], const double xb[6],
-                                          double y[6]) {
-  struct {
-    const double (&Sa)[2][3][3];
-    const double (&Ft)[3][3];
-    const double (&Fn)[3][3];
-    const double (&Fi)[3][3];
-    const double (&Fo)[3][3];
-    double cvol, ct, ca, cb, cn, pt, pb;
-  } P{A.Sa, A.Ft, A.Fn, A.Fi, A.Fo, D.cvol, D.ct, D.ca, D.cb, D.cn, D.pt, D.pb};
-  double t[3], s[3], dzc[3], r[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) dzc[a] = DV[0] * xc[a] + DV[1] * xc[3 + a];
-  // advective volume + diffusion volume
-  mv3(P.Sa[0], xc, t);
-  mv3(P.Sa[1], xc + 3, s);
-  mv3(V.R, dzc, r);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double av = t[a] + s[a];
-    y[a] = DV[0] * av - DV[0] * P.cvol * r[a];
-    y[3 + a] = DV[1] * av - DV[1] * P.cvol * r[a];
-  }
-  // top face
-  mv3(P.Ft, xc, t);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) y[a] -= t[a];
-  if (l > 0) {
-    double dza[3], ra[3], mt[3], ma[3], fn[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) dza[a] = DV[0] * xa[a] + DV[1] * xa[3 + a];
-    mv3(Vp.R, dza, ra);
-    mv3(MHQ, xc, mt);
-    mv3(MHQ, xa + 3, ma);
-    mv3(P.Fn, xa + 3, fn);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) y[a] += P.ct * r[a] + P.ca * ra[a] - P.pt * mt[a] + P.pt * ma[a] - fn[a];
-  }
-  if (l < L - 1) {
-    double dzb[3], rb[3], mb[3], mn[3], fi[3], fo[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) dzb[a] = DV[0] * xb[a] + DV[1] * xb[3 + a];
-    mv3(Vn.R, dzb, rb);
-    mv3(MHQ, xc + 3, mb);
-    mv3(MHQ, xb, mn);
-    mv3(P.Fi, xc + 3, fi);
-    mv3(P.Fo, xb, fo);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) y[3 + a] += fi[a] - P.cb * r[a] - P.cn * rb[a] - P.pb * mb[a] + P.pb * mn[a] + fo[a];
-  }
-}
 
 struct VopArgs {
   const double* eta_u;  // grid the operator is assembled on (C3)
@@ -877,22 +770,6 @@ __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __re
   }
 }
 
-// unpivoted 6x6 LU that keeps the reciprocal pivots (solves then multiply instead of divide)
-__device__ __forceinline__ int lu6r(double a[6][6], double rp[6]) {
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    if (a[k][k] == 0.0) return k;
-    const double inv = 1.0 / a[k][k];
-    rp[k] = inv;
-#pragma unroll
-    for (int i = k + 1; i < 6; ++i) {
-      a[i][k] = a[i][k] * inv;
-#pragma unroll
-      for (int j = k + 1; j < 6; ++j) a[i][j] = a[i][j] - a[i][k] * a[k][j];
-    }
-  }
-  return -1;
-}
 // the same elimination without early exit and with branch-free reciprocals; returns the first
 // zero pivot or -1 (the caller reports it and abandons the column)
 __device__ __forceinline__ int lu6r_bf(double a[6][6], double rp[6]) {
@@ -930,186 +807,10 @@ __device__ __forceinline__ void lu6r_solve(const double a[6][6], const double rp
   }
 }
 
-// ============================================================================ fused vertical step
-// IMPLICIT: (M1 - dt A) x = rhs by block Thomas (columns.py:292-348 order) with the layer blocks
-// assembled in registers; only the propagation tile G_l (36) is kept (workspace) for the back
-// substitution; the reduced RHS g_l is parked in x.  x may alias rhs.
-template <int NC, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_vimplicit(DMesh m, VopArgs a, double dt, const double* rhs,
-                                                   double* __restrict__ Gs, double* x) {
-  asm volatile(".pragma \"enable_smem_spilling\";");
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nt = m.nt, L = m.L;
-  if (c >= m.nown) return;
-  const size_t P6 = (size_t)6 * L * nt;
-  Col C;
-  load_col(m, c, C);
-  double eta[3], e0[3], e1[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    eta[k] = a.eta_u[k * nt + c];
-    e0[k] = a.eta0[k * nt + c];
-    e1[k] = a.eta1[k * nt + c];
-  }
-  const double j2d = C.j2d;
-  VG Vp, V, Vn;
-  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
-  Vp = V;
-  Vn = V;
-  double gp[6][NC];
-  for (int l = 0; l < L; ++l) {
-    const double ft = m.fracs[l], fb = m.fracs[l + 1];
-    if (l + 2 < L) pf6(a.wt, l + 2, c, L, nt);
-    if (l + 1 < L) {
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) pf6(rhs + cc * P6, l + 1, c, L, nt);
-    }
-    if (l < L - 1) vgeo(C, eta, fb, m.fracs[l + 2], Vn);
-    double wt[6], wm[6], wtn[3] = {0, 0, 0};
-    ld6(a.wt, l, c, L, nt, wt);
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
-    if (l < L - 1) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
-    }
-    VPieces P;
-    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
-    double d[6][6], u[3][6], w[3][6];
-    vop_blocks(l, L, Vp, V, Vn, P, P, d, u, w);
-    // M1 - dt A   (M1 = K (x) J2D Mjz(eta1))
-    double jz1[3], M1h[3][3];
-    layer_jz(C.b, e1, ft, fb, jz1);
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int q = p; q < 3; ++q) {
-        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
-        M1h[p][q] = s;
-        M1h[q][p] = s;
-      }
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int j = 0; j < 6; ++j) d[i][j] = KM[i / 3][j / 3] * M1h[i % 3][j % 3] - dt * d[i][j];
-    double g[6][NC];
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) g[i][cc] = rhs[cc * P6 + pix(i, l, c, L, nt)];
-    if (l > 0) {
-      // previous layer's tile, stored contiguously per prism ([l][c][36], row-major 6x6)
-      const double2* gq = reinterpret_cast<const double2*>(Gs + ((size_t)(l - 1) * nt + c) * 36);
-      double Gp[36];
-#pragma unroll
-      for (int e = 0; e < 18; ++e) {
-        const double2 v = gq[e];
-        Gp[2 * e] = v.x;
-        Gp[2 * e + 1] = v.y;
-      }
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        double G[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) G[k] = Gp[k * 6 + j];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * G[k];
-          d[i][j] = d[i][j] - acc;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) acc = acc + (-dt * u[i][k]) * gp[k][cc];
-          g[i][cc] = g[i][cc] - acc;
-        }
-    }
-    double rp[6];
-    const int bad = lu6r(d, rp);
-    if (bad >= 0) {
-      report(m.err, PDG_ERR_ZERO_PIVOT, l, bad, 0.0);
-      return;
-    }
-    if (l < L - 1) {
-      // G_l = Dtilde^-1 [0; W]: the top three RHS rows are zero, so forward substitution
-      // starts at row 3; tiles go to the per-prism-contiguous workspace with 16-byte stores
-      double Gn[36];
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        double t3 = -dt * w[0][j], t4 = -dt * w[1][j], t5 = -dt * w[2][j];
-        t4 = t4 - d[4][3] * t3;
-        t5 = t5 - d[5][3] * t3 - d[5][4] * t4;
-        double x[6];
-        x[5] = t5 * rp[5];
-        x[4] = (t4 - d[4][5] * x[5]) * rp[4];
-        x[3] = (t3 - d[3][4] * x[4] - d[3][5] * x[5]) * rp[3];
-        x[2] = (0.0 - d[2][3] * x[3] - d[2][4] * x[4] - d[2][5] * x[5]) * rp[2];
-        x[1] = (0.0 - d[1][2] * x[2] - d[1][3] * x[3] - d[1][4] * x[4] - d[1][5] * x[5]) * rp[1];
-        x[0] = (0.0 - d[0][1] * x[1] - d[0][2] * x[2] - d[0][3] * x[3] - d[0][4] * x[4] - d[0][5] * x[5]) * rp[0];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) Gn[i * 6 + j] = x[i];
-      }
-      double2* gq = reinterpret_cast<double2*>(Gs + ((size_t)l * nt + c) * 36);
-#pragma unroll
-      for (int e = 0; e < 18; ++e) gq[e] = make_double2(Gn[2 * e], Gn[2 * e + 1]);
-    }
-    lu6r_solve<NC>(d, rp, g);
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        x[cc * P6 + pix(i, l, c, L, nt)] = g[i][cc];
-        gp[i][cc] = g[i][cc];
-      }
-    Vp = V;
-    V = Vn;
-  }
-  double xn[6][NC];
-#pragma unroll
-  for (int i = 0; i < 6; ++i)
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) xn[i][cc] = gp[i][cc];
-  for (int l = L - 2; l >= 0; --l) {
-    const double2* gq = reinterpret_cast<const double2*>(Gs + ((size_t)l * nt + c) * 36);
-    double Gt[36];
-#pragma unroll
-    for (int e = 0; e < 18; ++e) {
-      const double2 v = gq[e];
-      Gt[2 * e] = v.x;
-      Gt[2 * e + 1] = v.y;
-    }
-    double xl[6][NC];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      double G[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) G[k] = Gt[i * 6 + k];
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) acc = acc + G[k] * xn[k][cc];
-        xl[i][cc] = x[cc * P6 + pix(i, l, c, L, nt)] - acc;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        x[cc * P6 + pix(i, l, c, L, nt)] = xl[i][cc];
-        xn[i][cc] = xl[i][cc];
-      }
-  }
-}
-
 // ============================================================================ split block Thomas
-// Same elimination as k_vimplicit, but the propagation tile is kept in factored, compact form
-// and the back substitution is its own (low-register, high-occupancy) streaming kernel.
+// IMPLICIT: (M1 - dt A) x = rhs by block Thomas (columns.py:292-348 order) with the layer blocks
+// assembled in registers; the propagation tile is kept in factored, compact form (workspace) and
+// the back substitution is its own streaming kernel; the reduced RHS g_l is parked in x.
 //
 // The coupling of layer l to layer l+1 is [0; W_l] with W_l = -dt w_l (3x6) and, from
 // vop_blocks, w_l = [Fo + pb MHQ - DV0 cn R_{l+1}, -DV1 cn R_{l+1}] (all 3x3 blocks symmetric).
@@ -1155,51 +856,6 @@ __device__ __forceinline__ void cs_get(const double* csp, int t, Col& C, double 
   }
 }
 
-// M1 - dt A_d of layer l and the coupling U = -dt u to layer l-1, assembled block-symmetrically.
-// Every 3x3 block of vop_blocks is a combination of symmetric 3x3 pieces (Sa_m, R, Ft, Fi, MHQ,
-// M1h); with DV = (1/2, -1/2) the diagonal block d = KM (x) M1h - dt A_d is
-//   d_00 = K00 M1h - dt ( Sa0/2 + r00 R - Ft - pt MHQ)      r00 = -cvol/4 + [l>0]   ct/2
-//   d_01 = K01 M1h - dt ( Sa1/2 + r01 R)                    r01 =  cvol/4 - [l>0]   ct/2
-//   d_10 = K10 M1h - dt (-Sa0/2 + r10 R)                    r10 =  cvol/4 - [l<L-1] cb/2
-//   d_11 = K11 M1h - dt (-Sa1/2 + r11 R + Fi - pb MHQ)      r11 = -cvol/4 + [l<L-1] cb/2
-// so 24 entries are formed (the mirrored ones are copies) instead of 36 general ones, and the
-// coupling U = -dt [ ca Rp/2 , -ca Rp/2 + pt MHQ - Fn ] is two symmetric blocks (Uc0, Uc1).
-// Same values as vop_blocks + the d = KM M1h - dt d combination up to rounding.
-__device__ __forceinline__ void vimpl_blocks(int l, int L, const VG& Vp, const VG& V, const VAdv& A, const VDif& D,
-                                             const double M1h[3][3], double dt, double d[6][6], double Uc0[3][3],
-                                             double Uc1[3][3]) {
-  const double c = -dt;
-  const double q4 = 0.25 * D.cvol;
-  const double ht = l > 0 ? 0.5 * D.ct : 0.0, hb = l < L - 1 ? 0.5 * D.cb : 0.0;
-  const double r00 = ht - q4, r01 = q4 - ht, r10 = q4 - hb, r11 = hb - q4;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = a; b < 3; ++b) {
-      const double R = V.R[a][b], mh = MHQ[a][b], m1 = M1h[a][b];
-      const double s0 = 0.5 * A.Sa[0][a][b], s1 = 0.5 * A.Sa[1][a][b];
-      const double v00 = KM[0][0] * m1 + c * (((s0 + r00 * R) - A.Ft[a][b]) - D.pt * mh);
-      const double v01 = KM[0][1] * m1 + c * (s1 + r01 * R);
-      const double v10 = KM[1][0] * m1 + c * (r10 * R - s0);
-      const double v11 = KM[1][1] * m1 + c * (((r11 * R - s1) + A.Fi[a][b]) - D.pb * mh);
-      d[a][b] = v00;
-      d[b][a] = v00;
-      d[a][3 + b] = v01;
-      d[b][3 + a] = v01;
-      d[3 + a][b] = v10;
-      d[3 + b][a] = v10;
-      d[3 + a][3 + b] = v11;
-      d[3 + b][3 + a] = v11;
-      if (l > 0) {
-        const double u0 = c * (0.5 * D.ca * Vp.R[a][b]);
-        const double u1 = c * ((D.pt * mh - A.Fn[a][b]) - 0.5 * D.ca * Vp.R[a][b]);
-        Uc0[a][b] = u0;
-        Uc0[b][a] = u0;
-        Uc1[a][b] = u1;
-        Uc1[b][a] = u1;
-      }
-    }
-}
 
 // FORWARD: assembles M1 - dt A per layer, eliminates, writes the compact tile and g_l (into x).
 // Per-layer inputs (rhs NC x 6, w~ 6) stream through a 3-deep cp.async ring in shared memory
@@ -1239,7 +895,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   const size_t P6 = (size_t)6 * L * nt;
   // 16-byte multiple of the block's owned columns (nt even: at most one column past nown, < nt)
   const unsigned seg = (unsigned)(min(VBLK, m.nown - c0) * 8 + 15) & ~15u;
-  // plane stride hidden from the optimiser (see k_vexpl2)
+  // plane stride hidden from the optimiser (see k_vexpl3)
   auto stage = [&](int l) {
     if (BULK) {
       if (t == 0 && l < L) {
@@ -1622,327 +1278,7 @@ __global__ void __launch_bounds__(VBLK, NC == 1 ? 3 : 1) k_vimpl_bwd_r(DMesh m, 
 
 inline size_t vimpl_fwd_smem(int nc, int L) { return ((size_t)3 * (6 * nc + 6) * VBLK + (VT + NCS) * VBLK + L + 1 + 3) * 8; }
 
-// EXPLICIT: x = M1^-1 (rhs + dt A xin), A applied matrix free; M1^-1 = K^-1 (x) (J2D Mjz)^-1.
-template <int NC, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_vexplicit(DMesh m, VopArgs a, double dt, const double* rhs,
-                                                   const double* __restrict__ xin, double* x) {
-  asm volatile(".pragma \"enable_smem_spilling\";");
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nt = m.nt, L = m.L;
-  if (c >= m.nown) return;
-  const size_t P6 = (size_t)6 * L * nt;
-  Col C;
-  load_col(m, c, C);
-  double eta[3], e0[3], e1[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    eta[k] = a.eta_u[k * nt + c];
-    e0[k] = a.eta0[k * nt + c];
-    e1[k] = a.eta1[k * nt + c];
-  }
-  const double j2d = C.j2d;
-  const double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
-  VG Vp, V, Vn;
-  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
-  Vp = V;
-  Vn = V;
-  double xa[NC][6], xc[NC][6], xb[NC][6];
-#pragma unroll
-  for (int cc = 0; cc < NC; ++cc) {
-    ld6(xin + cc * P6, 0, c, L, nt, xc[cc]);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      xa[cc][k] = 0.0;
-      xb[cc][k] = 0.0;
-    }
-  }
-  for (int l = 0; l < L; ++l) {
-    const double ft = m.fracs[l], fb = m.fracs[l + 1];
-    if (l + 2 < L) {
-      pf6(a.wt, l + 2, c, L, nt);
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) pf6(xin + cc * P6, l + 2, c, L, nt);
-    }
-    if (l + 1 < L) {
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) pf6(rhs + cc * P6, l + 1, c, L, nt);
-    }
-    if (l < L - 1) {
-      vgeo(C, eta, fb, m.fracs[l + 2], Vn);
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) ld6(xin + cc * P6, l + 1, c, L, nt, xb[cc]);
-    }
-    double wt[6], wm[6], wtn[3] = {0, 0, 0};
-    ld6(a.wt, l, c, L, nt, wt);
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
-    if (l < L - 1) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
-    }
-    VPieces P;
-    vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
-    double jz1[3], A1[3][3];
-    layer_jz(C.b, e1, ft, fb, jz1);
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int q = p; q < 3; ++q) {
-        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
-        A1[p][q] = s;
-        A1[q][p] = s;
-      }
-    // LDL-free 3x3 factorisation of J2D Mjz(eta1), shared by every component
-    double r0 = 1.0 / A1[0][0];
-    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
-    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
-    const double a22p = A1[2][2] - l20 * A1[0][2];
-    const double r1 = 1.0 / a11;
-    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
-    const double r2 = 1.0 / (a22p - l21 * a12);
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      double y[6], g[6];
-      vop_apply(l, L, Vp, V, Vn, P, P, xa[cc], xc[cc], xb[cc], y);
-      ld6(rhs + cc * P6, l, c, L, nt, g);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) y[k] = g[k] + dt * y[k];
-      double o[6];
-#pragma unroll
-      for (int lev = 0; lev < 2; ++lev) {
-        double z[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          z[k] = lev == 0 ? (KM[1][1] * y[k] - KM[0][1] * y[3 + k]) / det : (-KM[1][0] * y[k] + KM[0][0] * y[3 + k]) / det;
-        z[1] -= l10 * z[0];
-        z[2] -= l20 * z[0] + l21 * z[1];
-        z[2] *= r2;
-        z[1] = (z[1] - a12 * z[2]) * r1;
-        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
-      }
-      st6(x + cc * P6, l, c, L, nt, o);
-    }
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        xa[cc][k] = xc[cc][k];
-        xc[cc][k] = xb[cc][k];
-      }
-    Vp = V;
-    V = Vn;
-  }
-}
-
-// EXPLICIT, staged: as k_vexplicit, with the per-layer inputs (rhs, xin, w~) streamed through a
-// 3-deep cp.async ring two layers ahead (each thread stages and reads only its own words).
-template <int NC, int MINB, bool KH0>
-__global__ void __launch_bounds__(VBLK, MINB) k_vexpl2(DMesh m, VopArgs a, double dt, const double* rhs,
-                                                     const double* __restrict__ xin, double* x) {
-  constexpr int NE = 12 * NC + 6;  // rhs, xin, w~
-  extern __shared__ double smem[];
-  double* ring = smem;             // [3][NE][VBLK]
-  double* cst = smem + 3 * NE * VBLK;  // [NCS][VBLK] column constants
-  double* fr = cst + NCS * VBLK;
-  constexpr bool FCS = NC == 1;
-  double* fc = fr + m.L + 1;       // [12][VBLK] carried face pieces (FCS)
-  const int t = threadIdx.x;
-  const int c = blockIdx.x * VBLK + t;
-  const int nt = m.nt, L = m.L;
-  for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
-  __syncthreads();
-  if (c >= m.nown) return;
-  const size_t P6 = (size_t)6 * L * nt;
-  // plane stride L * nt hidden from the optimiser: otherwise it keeps the five k * L * nt plane
-  // offsets live across the layer loop, which spills this 255-register kernel
-  auto stage = [&](int l) {
-    if (l < L) {
-      unsigned ln = (unsigned)L * (unsigned)nt;
-      asm volatile("" : "+r"(ln));
-      const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
-      double* s = ring + (l % 3) * NE * VBLK + t;
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const size_t o = cc * P6 + (i * ln + lo);
-          cp_async8(s + (cc * 6 + i) * VBLK, rhs + o);
-          cp_async8(s + (6 * NC + cc * 6 + i) * VBLK, xin + o);
-        }
-#pragma unroll
-      for (int i = 0; i < 6; ++i) cp_async8(s + (12 * NC + i) * VBLK, a.wt + (i * ln + lo));
-    }
-    cp_async_commit();
-  };
-  stage(0);
-  stage(1);
-  Col C;
-  load_col(m, c, C);
-  double eta[3], e0[3], e1[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    eta[k] = a.eta_u[k * nt + c];
-    e0[k] = a.eta0[k * nt + c];
-    e1[k] = a.eta1[k * nt + c];
-  }
-  cs_put(cst, t, C, eta, e0, e1);
-  constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
-  constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
-  VG Vp, V, Vn;
-  vgeo_x<KH0, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
-  Vp = V;
-  Vn = V;
-  // xin of layers l-1 (registers: its ring slot is refilled at the top of iteration l), l and
-  // l+1 (read from the ring where they are used)
-  // (NC == 1 keeps all three in registers: no pressure there, and the smem reads cost more)
-  constexpr bool XR = NC >= 2;
-  double xa[NC][6], xcr[NC][6];
-#pragma unroll
-  for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-    for (int k = 0; k < 6; ++k) xa[cc][k] = 0.0;
-  for (int l = 0; l < L; ++l) {
-    cs_get(cst, t, C, eta, e0, e1);
-    const double j2d = C.j2d;
-    if (XR && l > 0) {
-      const double* prv = ring + ((l + 2) % 3) * NE * VBLK + t;   // slot of layer l-1
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) xa[cc][k] = prv[(6 * NC + cc * 6 + k) * VBLK];
-    }
-    stage(l + 2);
-    cp_async_wait1();
-    const double* cur = ring + (l % 3) * NE * VBLK + t;
-    const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
-    const double ft = fr[l], fb = fr[l + 1];
-    if (!XR && l == 0) {
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) xcr[cc][k] = cur[(6 * NC + cc * 6 + k) * VBLK];
-    }
-    double xbr[NC][6];
-    if (!XR) {
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) xbr[cc][k] = l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0;
-    }
-    if (l < L - 1) vgeo_x<KH0, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
-    double wt[6], wm[6], wtn[3] = {0, 0, 0};
-#pragma unroll
-    for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
-    if (l < L - 1) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = nxt[(12 * NC + k) * VBLK];
-    }
-    // interface face masses carried from the layer above (see k_vimpl_fwd), parked in shared
-    // memory; the register-tight NC == 2 kernel has no room for 12 KB more shared memory (two
-    // blocks per SM) and spills when it carries them in registers, so it integrates both faces
-    VPieces P;
-    if (!FCS) {
-      vop_pieces(j2d, l, L, Vp, V, Vn, wt, wm, wtn, a.kh, a.kv, a.n0, a.order, m.err, P);
-    } else {
-    vop_adv_vol(j2d, wt, wm, P);
-    if (l == 0) {
-      vop_adv_surf(j2d, wt, wm, P);
-    } else {
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          P.Ft[p][q] = fc[sym6(p, q) * VBLK + t];
-          P.Fn[p][q] = fc[(6 + sym6(p, q)) * VBLK + t];
-        }
-    }
-    if (l < L - 1) {
-      vop_adv_bot(j2d, wm, wtn, P);
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int q = p; q < 3; ++q) {
-          fc[sym6(p, q) * VBLK + t] = P.Fo[p][q];
-          fc[(6 + sym6(p, q)) * VBLK + t] = P.Fi[p][q];
-        }
-    } else {
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          P.Fi[p][q] = 0.0;
-          P.Fo[p][q] = 0.0;
-        }
-    }
-    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, P);
-    }
-    double jz1[3], A1[3][3];
-    layer_jz(C.b, e1, ft, fb, jz1);
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int q = p; q < 3; ++q) {
-        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
-        A1[p][q] = s;
-        A1[q][p] = s;
-      }
-    const double r0 = drcp(A1[0][0]);
-    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
-    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
-    const double a22p = A1[2][2] - l20 * A1[0][2];
-    const double r1 = drcp(a11);
-    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
-    const double r2 = drcp(a22p - l21 * a12);
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      double y[6], xc[6], xb[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        xc[k] = XR ? cur[(6 * NC + cc * 6 + k) * VBLK] : xcr[cc][k];
-        xb[k] = XR ? (l < L - 1 ? nxt[(6 * NC + cc * 6 + k) * VBLK] : 0.0) : xbr[cc][k];
-      }
-      vop_apply(l, L, Vp, V, Vn, P, P, xa[cc], xc, xb, y);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) y[k] = cur[(cc * 6 + k) * VBLK] + dt * y[k];
-      double o[6];
-#pragma unroll
-      for (int lev = 0; lev < 2; ++lev) {
-        double z[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) z[k] = lev == 0 ? ki00 * y[k] + ki01 * y[3 + k] : ki10 * y[k] + ki11 * y[3 + k];
-        z[1] -= l10 * z[0];
-        z[2] -= l20 * z[0] + l21 * z[1];
-        z[2] *= r2;
-        z[1] = (z[1] - a12 * z[2]) * r1;
-        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
-      }
-      {
-        unsigned ln = (unsigned)L * (unsigned)nt;
-        asm volatile("" : "+r"(ln));
-        const unsigned lo = (unsigned)l * (unsigned)nt + (unsigned)c;
-#pragma unroll
-        for (int n = 0; n < 6; ++n) x[cc * P6 + (n * ln + lo)] = o[n];
-      }
-    }
-    if (!XR) {
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          xa[cc][k] = xcr[cc][k];
-          xcr[cc][k] = xbr[cc][k];
-        }
-    }
-    Vp = V;
-    V = Vn;
-  }
-}
 inline size_t vexpl3_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1 + (nc == 1 ? 12 * VBLK : 0)) * 8; }
-inline size_t vexpl2_smem(int nc, int L) { return ((size_t)3 * (12 * nc + 6) * VBLK + NCS * VBLK + L + 1 + (nc == 1 ? 12 * VBLK : 0)) * 8; }
 
 // top face of layer l >= 1 (scaled): Ft (positive part, point-wise), Fn = whole - Ft
 __device__ __forceinline__ void vop_adv_top_s(double sj, const double wt[6], const double wm[6], double Ft[6],
@@ -1966,9 +1302,10 @@ __device__ __forceinline__ void smv_add(const double M[6], const double x[3], do
 // the diagonal block, the coupling U to layer l-1 and W to layer l+1 -- all symmetric, packed:
 // vop_blocks' 72 entries as 48 words) are formed once per layer from the dt-scaled pieces and
 // applied to every component (72 FMAs per component instead of ~180 for the matrix-free form).
-// Per-layer inputs stream through the 3-deep cp.async ring of k_vexpl2; NC == 1 carries the
-// interface face masses from the layer above in shared memory (FCS, see k_vimpl_fwd).
-template <int NC, int MINB>
+// Per-layer inputs (rhs, xin, w~) stream through a 3-deep cp.async ring issued two layers ahead
+// (each thread stages and reads only its own words); NC == 1 carries the interface face masses
+// from the layer above in shared memory (FCS, see k_vimpl_fwd).  KH0: kh == 0 geometry.
+template <int NC, int MINB, bool KH0>
 __global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, double dt, const double* rhs,
                                                      const double* __restrict__ xin, double* x) {
   constexpr int NE = 12 * NC + 6;  // rhs, xin, w~
@@ -2019,7 +1356,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, doubl
   constexpr double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
   constexpr double ki00 = KM[1][1] / det, ki01 = -KM[0][1] / det, ki10 = -KM[1][0] / det, ki11 = KM[0][0] / det;
   VG Vp, V, Vn;
-  vgeo_x<true, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
+  vgeo_x<KH0, NC == 1>(C, eta, fr[0], fr[1], a.vc, c, nt, V);
   Vp = V;
   Vn = V;
   double xa[NC][6];   // xin of layer l-1: its ring slot is refilled at the top of iteration l
@@ -2038,7 +1375,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, doubl
     const double* cur = ring + (l % 3) * NE * VBLK + t;
     const double* nxt = ring + ((l + 1) % 3) * NE * VBLK + t;
     const double ft = fr[l], fb = fr[l + 1];
-    if (l < L - 1) vgeo_x<true, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
+    if (l < L - 1) vgeo_x<KH0, NC == 1>(C, eta, fb, fr[l + 2], a.vc, c, nt, Vn);
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
@@ -2173,128 +1510,9 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, doubl
   }
 }
 
-// EXPLICIT stage for momentum (2 comps) AND tracer in one pass: the geometry window, the
-// advective pieces of A and the M1 factorisation are shared; only the diffusion pieces differ.
-template <int MINB>
-__global__ void __launch_bounds__(128, MINB) k_vexplicit_ut(DMesh m, VopArgs a, double khT, double kvT, double dt,
-                                                            const double* rhs_u, const double* __restrict__ xin_u,
-                                                            double* x_u, const double* rhs_T,
-                                                            const double* __restrict__ xin_T, double* x_T) {
-  asm volatile(".pragma \"enable_smem_spilling\";");
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nt = m.nt, L = m.L;
-  if (c >= m.nown) return;
-  const size_t P6 = (size_t)6 * L * nt;
-  Col C;
-  load_col(m, c, C);
-  double eta[3], e0[3], e1[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    eta[k] = a.eta_u[k * nt + c];
-    e0[k] = a.eta0[k * nt + c];
-    e1[k] = a.eta1[k * nt + c];
-  }
-  const double j2d = C.j2d;
-  const double det = KM[0][0] * KM[1][1] - KM[0][1] * KM[1][0];
-  const double* xin[3] = {xin_u, xin_u + P6, xin_T};
-  const double* rhs[3] = {rhs_u, rhs_u + P6, rhs_T};
-  double* xo[3] = {x_u, x_u + P6, x_T};
-  VG Vp, V, Vn;
-  vgeo(C, eta, m.fracs[0], m.fracs[1], V);
-  Vp = V;
-  Vn = V;
-  double xa[3][6], xc[3][6], xb[3][6];
-#pragma unroll
-  for (int cc = 0; cc < 3; ++cc) {
-    ld6(xin[cc], 0, c, L, nt, xc[cc]);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      xa[cc][k] = 0.0;
-      xb[cc][k] = 0.0;
-    }
-  }
-  for (int l = 0; l < L; ++l) {
-    const double ft = m.fracs[l], fb = m.fracs[l + 1];
-    if (l < L - 1) {
-      vgeo(C, eta, fb, m.fracs[l + 2], Vn);
-#pragma unroll
-      for (int cc = 0; cc < 3; ++cc) ld6(xin[cc], l + 1, c, L, nt, xb[cc]);
-    }
-    double wt[6], wm[6], wtn[3] = {0, 0, 0};
-    ld6(a.wt, l, c, L, nt, wt);
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
-    if (l < L - 1) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) wtn[k] = a.wt[pix(k, l + 1, c, L, nt)];
-    }
-    VAdv A;
-    VDif Du, Dt;
-    vop_adv(j2d, l, L, wt, wm, wtn, A);
-    vop_dif(j2d, l, L, Vp, V, Vn, a.kh, a.kv, a.n0, a.order, m.err, Du);
-    vop_dif(j2d, l, L, Vp, V, Vn, khT, kvT, a.n0, a.order, m.err, Dt);
-    double jz1[3], A1[3][3];
-    layer_jz(C.b, e1, ft, fb, jz1);
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int q = p; q < 3; ++q) {
-        const double s = j2d * (T3[p][q][0] * jz1[0] + T3[p][q][1] * jz1[1] + T3[p][q][2] * jz1[2]);
-        A1[p][q] = s;
-        A1[q][p] = s;
-      }
-    const double r0 = 1.0 / A1[0][0];
-    const double l10 = A1[1][0] * r0, l20 = A1[2][0] * r0;
-    const double a11 = A1[1][1] - l10 * A1[0][1], a12 = A1[1][2] - l10 * A1[0][2];
-    const double a22p = A1[2][2] - l20 * A1[0][2];
-    const double r1 = 1.0 / a11;
-    const double l21 = (A1[2][1] - l20 * A1[0][1]) * r1;
-    const double r2 = 1.0 / (a22p - l21 * a12);
-#pragma unroll
-    for (int cc = 0; cc < 3; ++cc) {
-      double y[6], g[6];
-      vop_apply(l, L, Vp, V, Vn, A, cc < 2 ? Du : Dt, xa[cc], xc[cc], xb[cc], y);
-      ld6(rhs[cc], l, c, L, nt, g);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) y[k] = g[k] + dt * y[k];
-      double o[6];
-#pragma unroll
-      for (int lev = 0; lev < 2; ++lev) {
-        double z[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          z[k] = lev == 0 ? (KM[1][1] * y[k] - KM[0][1] * y[3 + k]) / det : (-KM[1][0] * y[k] + KM[0][0] * y[3 + k]) / det;
-        z[1] -= l10 * z[0];
-        z[2] -= l20 * z[0] + l21 * z[1];
-        z[2] *= r2;
-        z[1] = (z[1] - a12 * z[2]) * r1;
-        z[0] = (z[0] - A1[0][1] * z[1] - A1[0][2] * z[2]) * r0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * lev + k] = z[k];
-      }
-      st6(xo[cc], l, c, L, nt, o);
-    }
-#pragma unroll
-    for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        xa[cc][k] = xc[cc][k];
-        xc[cc][k] = xb[cc][k];
-      }
-    Vp = V;
-    V = Vn;
-  }
-}
-
 }  // namespace pdg
 
 using namespace pdg;
-
-#define DISPATCH_MINB(key, KERNEL, ...)                                          \
-  switch (tune_get(key)) {                                                      \
-    case 3: KERNEL<__VA_ARGS__, 3><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
-    case 4: KERNEL<__VA_ARGS__, 4><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
-    default: KERNEL<__VA_ARGS__, 1><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break; \
-  }
 
 extern "C" {
 
@@ -2359,155 +1577,102 @@ int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, c
 }
 
 // fused vertical stage: implicit (M1 - dt A) x = rhs, or explicit x = M1^-1 (rhs + dt A xin)
+//   implicit, kh == 0 and TUNE_VSPLIT 4 (default): k_vimpl_fwd (18-word E tiles) + k_vimpl_bwd_r
+//       (coupling blocks rebuilt); otherwise k_vimpl_fwd (30-word tiles) + k_vimpl_bwd
+//   explicit: k_vexpl3 (blocks of dt A assembled once per layer)
 int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
                       const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
                       double dt, const double* rhs, const double* xin, double* x, void* stream) {
+  if (ncomp != 1 && ncomp != 2) return PDG_ERR_SHAPE;
   VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, 1.0 / dt_mesh, kh, kv, n0, order};
   const int nt = ctx->nt;
-  const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
+  const dim3 grid(nblocks(ctx->nown, VBLK)), blk(VBLK);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
-  // the sigma-form column constants are read by the tracer (NC = 1) kernels only
-  if ((ncomp == 1 || (SIGU && implicit)) && kh == 0.0 && (implicit ? tune_get(TUNE_VSPLIT) >= 2 : tune_get(TUNE_VSPLIT) >= 3)) {
+  const bool ct = implicit && kh == 0.0 && tune_get(TUNE_VSPLIT) == 4;
+  // sigma-form column constants: the kh == 0 tracer kernels and the momentum implicit solve
+  if (kh == 0.0 && (ncomp == 1 || (SIGU && implicit))) {
     double* vc = ctx->vcol();
     if (!vc) return PDG_ERR_CUDA;
     k_vcol<<<nblocks(ctx->nown, 256), 256, 0, strm>>>(m, eta_u, vc);
     if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
     a.vc = vc;
   }
-  if (implicit && tune_get(TUNE_VSPLIT) == 4 && kh == 0.0) {
-    double* Gs = ctx->ws3((size_t)18 * ctx->L * nt, ncomp);
+  if (implicit) {
+    double* Gs = ctx->ws3((size_t)(ct ? 18 : VT) * ctx->L * nt, ncomp);
     if (!Gs) return PDG_ERR_CUDA;
     const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
     static unsigned long long attr = 0;
     if (first_on_device(attr)) {
-      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)vimpl_fwd_smem(2, 4096));
-      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)vimpl_fwd_smem(1, 4096));
-      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)vimpl_fwd_smem(2, 4096));
-      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)vimpl_fwd_smem(1, 4096));
+      const int mx = (int)vimpl_fwd_smem(2, 4096), m1 = (int)vimpl_fwd_smem(1, 4096);
+      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m1);
+      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m1);
+      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m1);
+      cudaFuncSetAttribute(k_vimpl_fwd<2, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_vimpl_fwd<1, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m1);
     }
-    // bulk-copy ring: plane segments are 16-byte aligned when nt is even (TUNE_BULK bit 1 = on)
-    const bool bulk = nt % 2 == 0 && (tune_get(TUNE_BULK) & 2);
-    if (ncomp == 2) {
-      if (bulk)
-        k_vimpl_fwd<2, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
-      else
-        k_vimpl_fwd<2, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
-      if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
-      k_vimpl_bwd_r<2><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
+    if (ct) {
+      // bulk-copy ring: plane segments are 16-byte aligned when nt is even (TUNE_BULK bit 1 = on)
+      const bool bulk = nt % 2 == 0 && (tune_get(TUNE_BULK) & 2);
+      if (ncomp == 2) {
+        if (bulk)
+          k_vimpl_fwd<2, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        else
+          k_vimpl_fwd<2, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+        k_vimpl_bwd_r<2><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
+      } else {
+        if (bulk)
+          k_vimpl_fwd<1, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        else
+          k_vimpl_fwd<1, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+        k_vimpl_bwd_r<1><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
+      }
     } else {
-      if (bulk)
-        k_vimpl_fwd<1, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
-      else
-        k_vimpl_fwd<1, 1, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
-      if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
-      k_vimpl_bwd_r<1><<<grid, blk, 0, strm>>>(m, a, dt, Gs, x);
+      if (ncomp == 2) {
+        if (kh == 0.0)
+          k_vimpl_fwd<2, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        else
+          k_vimpl_fwd<2, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+        k_vimpl_bwd<2><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
+      } else {
+        if (kh == 0.0)
+          k_vimpl_fwd<1, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        else
+          k_vimpl_fwd<1, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
+        if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
+        k_vimpl_bwd<1><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
+      }
     }
-  } else if (implicit && tune_get(TUNE_VSPLIT) >= 2) {
-    double* Gs = ctx->ws3((size_t)VT * ctx->L * nt, ncomp);
-    if (!Gs) return PDG_ERR_CUDA;
-    const size_t sm = vimpl_fwd_smem(ncomp, ctx->L);
-#define LAUNCH_FWD(NCV, MB)                                                                       \
-  {                                                                                               \
-    static unsigned long long attr = 0;                                                                     \
-    if (first_on_device(attr)) {                                                                                  \
-      cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)vimpl_fwd_smem(NCV, 4096));                                       \
-      cudaFuncSetAttribute(k_vimpl_fwd<NCV, MB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)vimpl_fwd_smem(NCV, 4096));                                       \
-                                                                                      \
-    }                                                                                             \
-    if (a.kh == 0.0)                                                                              \
-      k_vimpl_fwd<NCV, MB, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                  \
-    else                                                                                          \
-      k_vimpl_fwd<NCV, MB, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);                 \
-  }
-    if (ncomp == 2) {
-      if (tune_get(TUNE_VIMPL) == 3) LAUNCH_FWD(2, 3) else LAUNCH_FWD(2, 1)
-    } else {
-      if (tune_get(TUNE_VIMPL) == 3) LAUNCH_FWD(1, 3) else LAUNCH_FWD(1, 1)
-    }
-#undef LAUNCH_FWD
-    if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
-    if (ncomp == 2)
-      k_vimpl_bwd<2><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
-    else
-      k_vimpl_bwd<1><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
-  } else if (implicit) {
-    double* Gs = ctx->ws3((size_t)36 * ctx->L * nt, ncomp);
-    if (!Gs) return PDG_ERR_CUDA;
-#define LAUNCH_ARGS m, a, dt, rhs, Gs, x
-    if (ncomp == 2) {
-      DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 2)
-    } else {
-      DISPATCH_MINB(TUNE_VIMPL, k_vimplicit, 1)
-    }
-#undef LAUNCH_ARGS
-  } else if (!implicit && tune_get(TUNE_VSPLIT) >= 3 && kh == 0.0 && tune_get(TUNE_VASM) == 1) {
-    // assembled explicit stage (TUNE_VASM 1, default)
+  } else {
     const size_t sm = vexpl3_smem(ncomp, ctx->L);
     static unsigned long long attr = 0;
     if (first_on_device(attr)) {
-      cudaFuncSetAttribute(k_vexpl3<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl3_smem(2, 4096));
-      cudaFuncSetAttribute(k_vexpl3<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl3_smem(1, 4096));
+      const int mx = (int)vexpl3_smem(2, 4096), m1 = (int)vexpl3_smem(1, 4096);
+      cudaFuncSetAttribute(k_vexpl3<2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_vexpl3<1, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m1);
+      cudaFuncSetAttribute(k_vexpl3<2, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_vexpl3<1, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m1);
     }
-    if (ncomp == 2)
-      k_vexpl3<2, 1><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
-    else
-      k_vexpl3<1, 1><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
-  } else if (!implicit && tune_get(TUNE_VSPLIT) >= 3) {
-    const size_t sm = vexpl2_smem(ncomp, ctx->L);
-#define LAUNCH_EX(NCV, MB)                                                                                           \
-  {                                                                                                                \
-    static unsigned long long attr = 0;                                                                                      \
-    if (first_on_device(attr)) {                                                                                                   \
-      cudaFuncSetAttribute(k_vexpl2<NCV, MB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
-      cudaFuncSetAttribute(k_vexpl2<NCV, MB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vexpl2_smem(NCV, 4096)); \
-                                                                                                       \
-    }                                                                                                              \
-    if (a.kh == 0.0)                                                                                               \
-      k_vexpl2<NCV, MB, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                      \
-    else                                                                                                           \
-      k_vexpl2<NCV, MB, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);                                     \
-  }
     if (ncomp == 2) {
-      if (tune_get(TUNE_VEXPL) == 3) LAUNCH_EX(2, 3) else LAUNCH_EX(2, 1)
+      if (kh == 0.0)
+        k_vexpl3<2, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
+      else
+        k_vexpl3<2, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
     } else {
-      if (tune_get(TUNE_VEXPL) == 3) LAUNCH_EX(1, 3) else LAUNCH_EX(1, 1)
+      if (kh == 0.0)
+        k_vexpl3<1, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
+      else
+        k_vexpl3<1, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, xin, x);
     }
-#undef LAUNCH_EX
-  } else {
-#define LAUNCH_ARGS m, a, dt, rhs, xin, x
-    if (ncomp == 2) {
-      DISPATCH_MINB(TUNE_VEXPL, k_vexplicit, 2)
-    } else {
-      DISPATCH_MINB(TUNE_VEXPL, k_vexplicit, 1)
-    }
-#undef LAUNCH_ARGS
   }
   return check_launch(ctx);
 }
 
-// explicit vertical stage of momentum and tracer together (shared geometry / advective operator)
-int pdg_step_vertical_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, double dt_mesh,
-                         const double* wt, double kh_u, double kv_u, double kh_T, double kv_T, double n0, int order,
-                         double dt, const double* rhs_u, const double* xin_u, double* x_u, const double* rhs_T,
-                         const double* xin_T, double* x_T, void* stream) {
-  VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, 1.0 / dt_mesh, kh_u, kv_u, n0, order};
-  const dim3 grid(nblocks(ctx->nown, 128)), blk(128);
-  cudaStream_t strm = (cudaStream_t)stream;
-#define LAUNCH_ARGS ctx->view(), a, kh_T, kv_T, dt, rhs_u, xin_u, x_u, rhs_T, xin_T, x_T
-  switch (tune_get(TUNE_VEXPL)) {
-    case 3: k_vexplicit_ut<3><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break;
-    case 4: k_vexplicit_ut<4><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break;
-    default: k_vexplicit_ut<1><<<grid, blk, 0, strm>>>(LAUNCH_ARGS); break;
-  }
-#undef LAUNCH_ARGS
-  return check_launch(ctx);
-}
 
 }  // extern "C"

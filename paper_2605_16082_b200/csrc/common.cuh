@@ -358,7 +358,8 @@ inline bool first_on_device(unsigned long long& seen) {
 // occupancy variants of the heavy thread-per-column kernels: __launch_bounds__(128, MINB)
 // (MINB 1 -> up to 255 regs / 8 warps per SM, 3 -> 168 regs, 4 -> 128 regs); chosen per
 // kernel family at run time through pdg_tune() so one binary can be measured in every variant.
-enum TuneKey { TUNE_HRHS = 0, TUNE_VIMPL = 1, TUNE_VEXPL = 2, TUNE_R = 3, TUNE_WT = 4, TUNE_HRHS2 = 5, TUNE_RK = 6, TUNE_VSPLIT = 7, TUNE_PF = 8, TUNE_TILE_PRED = 9, TUNE_TILE_STAGE = 10, TUNE_TILE_COL = 11, TUNE_BULKPF = 12, TUNE_VASM = 13, TUNE_NKEYS = 16 };
+// keys 1, 2 and 13 are retired (superseded vertical-kernel variants, removed)
+enum TuneKey { TUNE_HRHS = 0, TUNE_R = 3, TUNE_WT = 4, TUNE_HRHS2 = 5, TUNE_RK = 6, TUNE_VSPLIT = 7, TUNE_PF = 8, TUNE_TILE_PRED = 9, TUNE_TILE_STAGE = 10, TUNE_TILE_COL = 11, TUNE_BULKPF = 12, TUNE_NKEYS = 16 };
 constexpr int TUNE_BULK = TUNE_BULKPF;   // bit 0: F3D->2D L2 bulk prefetch; bit 1: bulk-copy rings
 int tune_get(int key);
 

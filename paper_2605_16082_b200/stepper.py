@@ -25,6 +25,7 @@ from __future__ import annotations
 from types import SimpleNamespace
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -86,12 +87,10 @@ class ImexStepper:
         self.use_graph = True
         self.prof = None       # {name: [(start_event, end_event), ...]} when profiling
         self.fuse_rhs = True   # momentum + tracer stage right-hand sides in one kernel
-        self.fuse_vexpl = False  # momentum + tracer explicit vertical in one kernel (slower: register spills)
         self._pending_d2h = {}   # host buffer address -> event of the download filling it
         self.schedule_check = False  # debug: poison in-flight ghost slots (partitioned runs)
         self._skip_exchanges = set()  # tests only: exchange names to leave out (a broken schedule)
         self.phase_trace = None      # list -> per-phase CUDA events of eager steps (phase_csv)
-        import os
         self.concurrent_vertical = os.environ.get("PDG_CONC_VERT", "0") == "1"
 
     def _c(self, name, rc):
@@ -318,13 +317,6 @@ class ImexStepper:
             tm("hdiff_T", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(T), 1, p.nu_h, 0, dt_s, 0, None, 0,
                ptr(out_T), s)
         pe = self.pen
-        if not implicit and self.fuse_vexpl:
-            tm("vertical_uT_expl", lb.pdg_step_vertical_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), dt_s, ptr(self.wt),
-               p.kappa_h, self.kv, p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u), ptr(out_u),
-               ptr(out_T), ptr(T), ptr(out_T), s)
-            if part:
-                yield ("all", [out_u, out_T], "uT")
-            return eta1
         conc = self.concurrent_vertical and self.prof is None
         if conc:   # the tracer solve on a second stream (own workspace): overlaps the momentum solve
             main = torch.cuda.current_stream(self.dev)

@@ -2,6 +2,7 @@
 graph-replayed step, each build in its own process (PDG_LIB), alternated A B A B.
 
     python scripts/ab_lib.py build/lib_a.so paper_2605_16082_b200/libprismdg_b200.so
+    python scripts/ab_lib.py lib.so lib.so:PDG_FUSE_VEXPL=1      # same build, stepper option via env
 """
 import json
 import os
@@ -42,14 +43,15 @@ if __name__ == "__main__":
     res = {lib: [] for lib in libs}
     for rep in range(2):
         for lib in libs:
-            env = dict(os.environ, PDG_LIB=os.path.abspath(lib))
+            path, *kv = lib.split(":")
+            env = dict(os.environ, PDG_LIB=os.path.abspath(path), **dict(x.split("=", 1) for x in kv))
             p = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
             line = [ln for ln in p.stdout.splitlines() if ln.startswith("ABJSON")]
             if not line:
                 print(p.stdout[-2000:], p.stderr[-3000:])
                 sys.exit(1)
             res[lib].append(json.loads(line[0][6:]))
-    keys = list(res[libs[0]][0].keys())
-    print(f"{'kernel':22s}" + "".join(f"{os.path.basename(lib)[:18]:>20s}" for lib in libs))
+    keys = list(dict.fromkeys(k for lib in libs for r in res[lib] for k in r))
+    print(f"{'kernel':22s}" + "".join(f"{os.path.basename(lib)[-18:]:>20s}" for lib in libs))
     for k in keys:
-        print(f"{k:22s}" + "".join(f"{' / '.join(str(r[k]) for r in res[lib]):>20s}" for lib in libs))
+        print(f"{k:22s}" + "".join(f"{' / '.join(str(r.get(k, '-')) for r in res[lib]):>20s}" for lib in libs))
