@@ -1,0 +1,42 @@
+"""FP64 issue floor per kernel family from a --set full raw CSV export: executed DFMA + DMUL + DADD
+warp instructions (the FP64 pipe issues 2 warp instructions per SM per cycle on B200: 64 FP64
+lanes), the time they need at the pipe's peak at a given SM clock, and the kernel's measured
+duration -- the share of the step the FP64 pipe alone accounts for.
+
+    python scripts/fp64_floor.py profiles/r2_opt1_raw/full3d.csv [sm_mhz]
+"""
+import csv
+import sys
+
+SMS = 148
+PER_CLK = 2          # FP64 warp instructions per SM per cycle
+
+
+def rows(path):
+    r = list(csv.reader(open(path)))
+    hdr, units = r[0], r[1]
+    return hdr, units, [x for x in r[1:] if x and x[0].isdigit()]
+
+
+def main(path, mhz=1750.0):
+    hdr, units, data = rows(path)
+    ix = {h: i for i, h in enumerate(hdr)}
+    ops = ["smsp__sass_thread_inst_executed_op_%s_pred_on.sum.per_cycle_elapsed" % o for o in ("dfma", "dmul", "dadd")]
+    seen = set()
+    print(f"| kernel | ms (ncu) | FP64 warp inst | FP64 floor ms @ {mhz:.0f} MHz | floor / time |")
+    print("|---|---:|---:|---:|---:|")
+    for x in data:
+        name = x[ix["Kernel Name"]].split("(")[0].replace("void ", "")
+        if name in seen:
+            continue
+        seen.add(name)
+        cyc = float(x[ix["sm__cycles_elapsed.avg"]])
+        per_cycle = sum(float(x[ix[o]]) for o in ops) / 32.0       # warp instructions per cycle, all SMSPs
+        inst = per_cycle * cyc
+        ms = float(x[ix["gpu__time_duration.sum"]]) * {"ms": 1.0, "us": 1e-3, "ns": 1e-6}[units[ix["gpu__time_duration.sum"]]]
+        floor = inst / (SMS * PER_CLK) / (mhz * 1e3)
+        print(f"| `{name}` | {ms:.3f} | {inst:.3e} | {floor:.3f} | {floor / ms:.2f} |")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1750.0)

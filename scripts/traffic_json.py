@@ -17,8 +17,8 @@ KEYS = {
     "rhs_uT_s2": ["k_hrhs_s<3, 2, 1, 0"],
     "vertical_u_impl": ["k_vimpl_fwd<2", "k_vimpl_bwd_r<2"],
     "vertical_T_impl": ["k_vimpl_fwd<1", "k_vimpl_bwd_r<1"],
-    "vertical_u_expl": ["k_vexpl2<2"],
-    "vertical_T_expl": ["k_vexpl2<1"],
+    "vertical_u_expl": ["k_vexpl3<2"],
+    "vertical_T_expl": ["k_vexpl3<1"],
     "rk_stage0": ["k_rk_stage<0"],
     "rk_stage1": ["k_rk_stage<1"],
     "rk_stage2": ["k_rk_stage<2"],
