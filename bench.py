@@ -273,8 +273,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--backend", default="nccl", help="process group for N>1 (gloo: host-staged halos, testing)")
-    ap.add_argument("--halo", default="capi", choices=["capi", "torch"],
-                    help="N>1 halo transport: the library's NCCL plans (graph-captured step) or torch.distributed")
+    ap.add_argument("--halo", default="capi", choices=["capi", "p2p", "torch"],
+                    help="N>1 halo transport: the library's NCCL plans (graph-captured step), NVLink peer "
+                         "stores (csrc/p2p.cu, CUDA IPC inboxes; graph-captured) or torch.distributed")
     ap.add_argument("--phase-csv", default=None, help="append step,rank,phase,micros rows of one eager step")
     ap.add_argument("--dump", default=None, help="write the final local state to this .npz (testing)")
     args = ap.parse_args()
@@ -310,7 +311,8 @@ def main():
     else:
         # strong scaling: the one C4 mesh split into `world` Hilbert ranges, halos over NCCL
         run = PartitionedRun(case.mesh, case.L, case.params, case.dt, case.m, case.kv, case.nu_v, world,
-                             transport=("nccl" if args.backend == "nccl" and args.halo == "capi" else "dist"),
+                             transport=("p2p" if args.halo == "p2p" else
+                                        "nccl" if args.backend == "nccl" and args.halo == "capi" else "dist"),
                              rank=rank, device=local)
         st = run.st[rank]
         stepper = run
@@ -469,7 +471,9 @@ def main():
                                       f"m={case.m}, dt2d={case.dt2d} s, momentum+tracer, FP64",
                           "nt": case.mesh.nt, "L": case.L, "m": case.m, "prism_dof_per_step": dof_per_step,
                           "parallelism": (f"column partition x{world} (Hilbert ranges, 3 ghost rings, "
-                                          + ("library NCCL halo plans, one CUDA graph per rank and step"
+                                          + ("NVLink peer-store halos (CUDA IPC inboxes), one CUDA graph per rank "
+                                             "and step" if args.halo == "p2p" else
+                                             "library NCCL halo plans, one CUDA graph per rank and step"
                                              if args.backend == "nccl" and args.halo == "capi" else
                                              f"{'NCCL' if args.backend == 'nccl' else 'gloo host-staged'} "
                                              "torch.distributed send/recv, eager")

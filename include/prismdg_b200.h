@@ -235,6 +235,23 @@ int pdg_halo_plan_destroy(pdg_halo_plan* plan);
 int pdg_halo_start(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
 int pdg_halo_finish(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
 
+/* ---- device-initiated halo exchange over NVLink peer memory (csrc/p2p.cu; SURVEY.md section 8e
+ * "LSA peer stores (2D)").  No NCCL: every rank owns an inbox (per peer: an epoch flag and a
+ * double-buffered receive window) that its peers map -- pdg_p2p_local exports the CUDA IPC handle
+ * (64 bytes) or raw pointer and the per-peer offsets, pdg_p2p_connect maps a peer's inbox.
+ * start: per peer one kernel stores the packed boundary values into the peer's window and
+ * publishes the epoch (release, system scope); finish: per peer one kernel waits for the epoch
+ * (acquire) and unpacks.  Epochs are device-resident: stream ordered, CUDA-graph capturable. */
+typedef struct pdg_p2p pdg_p2p;
+int pdg_p2p_create(int nt, int npeers, const int* peers, const int* nsend, const int* const* send_idx,
+                   const int* nrecv, const int* const* recv_idx, int max_planes, int device, pdg_p2p** out);
+int pdg_p2p_destroy(pdg_p2p* plan);
+int pdg_p2p_local(pdg_p2p* plan, void* ipc_handle64, void** raw, long long* win_off, long long* flag_off);
+int pdg_p2p_connect(pdg_p2p* plan, int slot, const void* ipc_handle64, void* raw, long long win_off,
+                    long long flag_off);
+int pdg_p2p_start(pdg_p2p* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
+int pdg_p2p_finish(pdg_p2p* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
+
 /* ---- host I/O layout conversion (set_state / get_state of the drop-in; csrc/hostio.cu):
  * rows [ncols][L][nk] = columns [c0, c0 + ncols) of a reference-layout field ((P, nk) with
  * p = c L + l, or (nt, nk) with L = 1) in a device staging buffer  <->  planes [nk][L][nt] */

@@ -51,6 +51,12 @@ _SIGS = {
     "pdg_halo_plan_destroy": (I, [P]),
     "pdg_halo_start": (I, [P, I, P, P, P]),
     "pdg_halo_finish": (I, [P, I, P, P, P]),
+    "pdg_p2p_create": (I, [I, I, P, P, P, P, P, I, I, P]),
+    "pdg_p2p_destroy": (I, [P]),
+    "pdg_p2p_local": (I, [P, P, P, P, P]),
+    "pdg_p2p_connect": (I, [P, I, P, P, LL, LL]),
+    "pdg_p2p_start": (I, [P, I, P, P, P]),
+    "pdg_p2p_finish": (I, [P, I, P, P, P]),
     "pdg_rows_to_planes": (I, [P, I, I, I, P, I, I, P]),
     "pdg_planes_to_rows": (I, [P, I, I, I, I, I, P, P]),
     "pdg_ext2d_eval": (I, [P, P, P, P, P, P, P, I, D, D, D, P, I, I, P, P, P, P]),

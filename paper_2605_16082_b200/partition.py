@@ -465,10 +465,142 @@ class NcclHalo:
         self.exchanges += 1
 
 
+# ----------------------------------------------------------------------------- NVLink peer stores
+
+class P2PPlan:
+    """One rank's device-initiated exchange plan for one message shape (csrc/p2p.cu): an inbox of
+    per-peer epoch flags and double-buffered windows that the peers write into directly."""
+
+    def __init__(self, send, recv, nt, device, max_planes):
+        import ctypes
+        from . import _lib
+        self.peers = sorted(set(send) | set(recv))
+        lists = []
+        for d in (send, recv):
+            lists.append([np.ascontiguousarray(d.get(q, np.zeros(0, np.int32)), dtype=np.int32) for q in self.peers])
+        self._keep = lists
+        n = len(self.peers)
+        IntArr = ctypes.c_int * max(n, 1)
+        PtrArr = ctypes.POINTER(ctypes.c_int) * max(n, 1)
+        sp = PtrArr(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_int)) for a in lists[0]])
+        rp = PtrArr(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_int)) for a in lists[1]])
+        self.h = ctypes.c_void_p()
+        idx = device.index if device.index is not None else 0
+        _lib.check(_lib.lib().pdg_p2p_create(nt, n, IntArr(*self.peers), IntArr(*[a.size for a in lists[0]]), sp,
+                                             IntArr(*[a.size for a in lists[1]]), rp, max_planes, idx,
+                                             ctypes.byref(self.h)), "pdg_p2p_create")
+
+    def local(self, ipc: bool):
+        """(64-byte IPC handle or None, raw inbox pointer, {peer: (window offset, flag offset)})."""
+        import ctypes
+        from . import _lib
+        n = max(len(self.peers), 1)
+        handle = (ctypes.c_char * 64)() if ipc else None
+        raw = ctypes.c_void_p()
+        wo, fo = (ctypes.c_longlong * n)(), (ctypes.c_longlong * n)()
+        _lib.check(_lib.lib().pdg_p2p_local(self.h, handle, ctypes.byref(raw), wo, fo), "pdg_p2p_local")
+        offs = {q: (wo[i], fo[i]) for i, q in enumerate(self.peers)}
+        return (bytes(handle) if ipc else None), raw.value, offs
+
+    def connect(self, peer, handle, raw, offs_of_peer, me):
+        """Map `peer`'s inbox (IPC handle, or raw pointer in this process); my window / flag in it
+        are at the offsets the peer computed for me."""
+        import ctypes
+        from . import _lib
+        wo, fo = offs_of_peer[me]
+        hb = (ctypes.c_char * 64).from_buffer_copy(handle) if handle is not None else None
+        _lib.check(_lib.lib().pdg_p2p_connect(self.h, self.peers.index(peer), hb, ctypes.c_void_p(raw), wo, fo),
+                   "pdg_p2p_connect")
+
+    def run(self, which, fields, nt):
+        import ctypes
+        from . import _lib
+        from .device import stream_ptr
+        fp = (ctypes.c_void_p * len(fields))(*[f.data_ptr() for f in fields])
+        npl = (ctypes.c_longlong * len(fields))(*[f.numel() // nt for f in fields])
+        fn = _lib.lib().pdg_p2p_start if which == "start" else _lib.lib().pdg_p2p_finish
+        _lib.check(fn(self.h, len(fields), fp, npl, stream_ptr()), "pdg_p2p_" + which)
+
+    def __del__(self):
+        try:
+            from . import _lib
+            _lib.lib().pdg_p2p_destroy(self.h)
+        except Exception:
+            pass
+
+
+def _p2p_plans(part, nt, device, L):
+    # ring-1 messages carry at most u and T (18 L planes per column); deep ones the 2D state (9)
+    return {True: P2PPlan(part.send, part.recv, nt, device, 9),
+            False: P2PPlan(part.send1, part.recv1, nt, device, 18 * L)}
+
+
+class P2PHalo:
+    """One rank's halo exchange by NVLink peer stores (csrc/p2p.cu): the
+    peers' inboxes are mapped with CUDA IPC (handles all-gathered over torch.distributed once);
+    start = one push kernel per peer (pack + remote stores + epoch release), finish = one pull
+    kernel per peer (epoch acquire + unpack).  No NCCL, no host synchronisation: the rank's step
+    is captured in one CUDA graph like the single-GPU step."""
+
+    capturable = True
+
+    def __init__(self, part: Part, nt_local: int, device, L: int):
+        import torch.distributed as dist
+        self.nt, self.exchanges = nt_local, 0
+        self.plans = _p2p_plans(part, nt_local, device, L)
+        mine = {d: pl.local(ipc=True) for d, pl in self.plans.items()}
+        allinfo = [None] * dist.get_world_size()
+        dist.all_gather_object(allinfo, {d: (h, o) for d, (h, _, o) in mine.items()})
+        for d, pl in self.plans.items():
+            for q in pl.peers:
+                h, offs = allinfo[q][d]
+                pl.connect(q, h, 0, offs, part.rank)
+        dist.barrier()
+
+    def exchange(self, fields, deep=False):
+        self.start(fields, deep)
+        self.finish(fields, deep)
+
+    def start(self, fields, deep=True):
+        self.plans[deep].run("start", fields, self.nt)
+
+    def finish(self, fields, deep=True):
+        self.plans[deep].run("finish", fields, self.nt)
+        self.exchanges += 1
+
+
+class P2PGroup:
+    """P ranks in one process on one device, exchanging through the peer-store protocol with raw
+    pointers (the same push / pull kernels, epochs and windows as P2PHalo without IPC)."""
+
+    capturable = True
+
+    def __init__(self, parts, nts, device, L):
+        self.nts = nts
+        self.exchanges = 0
+        self.plans = [_p2p_plans(p, nt, device, L) for p, nt in zip(parts, nts)]
+        info = [{d: pl.local(ipc=False) for d, pl in r.items()} for r in self.plans]
+        for r, pls in enumerate(self.plans):
+            for d, pl in pls.items():
+                for q in pl.peers:
+                    _, raw, offs = info[q][d]
+                    pl.connect(q, None, raw, offs, r)
+
+    def exchange_all(self, fields_per_rank, deep=False):
+        for r, fields in enumerate(fields_per_rank):
+            self.plans[r][deep].run("start", fields, self.nts[r])
+        for r, fields in enumerate(fields_per_rank):
+            self.plans[r][deep].run("finish", fields, self.nts[r])
+        self.exchanges += 1
+
+
 class PartitionedRun:
     """P partitions of one mesh, each an ImexStepper over its owned + ghost columns.
 
     transport "virtual": all ranks in this process on one device (VirtualGroup);
+    transport "p2p-virtual": the same, exchanging through the peer-store kernels (P2PGroup);
+    transport "nccl": this process is rank `rank`; the library's NCCL plans (NcclHalo);
+    transport "p2p": this process is rank `rank`; NVLink peer stores (P2PHalo, CUDA IPC);
     transport "dist": this process is rank `rank` of a torch.distributed job (DistHalo).
     """
 
@@ -479,12 +611,17 @@ class PartitionedRun:
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.parts = decompose(mesh, P, np.full(mesh.nt, L), depth=GHOST_DEPTH, device=dev)
         self.local = [local_mesh(mesh, p) for p in self.parts]
-        ranks = range(P) if transport == "virtual" else [rank]
+        ranks = range(P) if transport in ("virtual", "p2p-virtual") else [rank]
         self.ranks = list(ranks)
         self.st = {r: ImexStepper(self.local[r], L, params, dt, m, kv, nu_v, part=self.parts[r], device=dev.index)
                    for r in ranks}
         if transport == "virtual":
             self.group = VirtualGroup(self.parts, [lm.nt for lm in self.local], dev)
+        elif transport == "p2p-virtual":   # all ranks here, peer-store protocol with raw pointers
+            self.group = P2PGroup(self.parts, [lm.nt for lm in self.local], dev, L)
+        elif transport == "p2p":     # NVLink peer stores between processes (CUDA IPC inboxes)
+            self.group = None
+            self.st[rank].halo = P2PHalo(self.parts[rank], self.local[rank].nt, dev, L)
         elif transport == "nccl":    # the library's NCCL halo plans (csrc/comm.cu): graph-captured steps
             self.group = None
             self.st[rank].halo = NcclHalo(self.parts[rank], self.local[rank].nt, dev, L)

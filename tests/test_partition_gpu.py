@@ -109,3 +109,27 @@ def test_gpu_decomposition_bit_exact(pdg, nx, ny, P, var):
                 da, db = getattr(a, d), getattr(b, d)
                 assert sorted(da) == sorted(db)
                 assert all(np.array_equal(da[k], db[k]) for k in da)
+
+
+@pytest.mark.parametrize("P,graph", [(2, False), (3, True), (4, True)])
+def test_peer_store_halos_bitwise(pdg, P, graph):
+    """Device-initiated halos (csrc/p2p.cu: push kernels store into the peers' inbox windows and
+    release an epoch flag, pull kernels acquire it and unpack), virtual ranks with raw pointers,
+    eager and graph-replayed (device-resident epochs): bitwise equal to P = 1."""
+    from paper_2605_16082_b200.partition import P2PGroup, PartitionedRun
+    c = _c4_small()
+    ref = pdg.stepper.ImexStepper(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v)
+    ref.use_graph = False
+    ref.set_state(**c.state)
+    ref.step(4)
+    g = ref.get_state()
+    run = PartitionedRun(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v, P, transport="p2p-virtual")
+    assert isinstance(run.group, P2PGroup)
+    run.use_graph = graph
+    run.set_state(**c.state)
+    run.step(4)
+    run.check()
+    s = run.get_state()
+    for k in ("eta", "qx", "qy", "ux", "uy", "T"):
+        assert np.array_equal(s[k], g[k]), (P, k, float(np.abs(s[k] - g[k]).max()))
+    assert bool(run.graphs) == graph
