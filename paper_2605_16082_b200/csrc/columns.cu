@@ -725,6 +725,20 @@ __device__ __forceinline__ void wm_layer(const VopArgs& a, const double b[3], co
   }
 }
 
+// node values of w_m at layer l on sigma layers: z = (1 - f) eta + f b, so z(eta1) - z(eta0) =
+// (1 - f)(eta1 - eta0) exactly and w_m = (1 - f) (eta1 - eta0) / dtm (b cancels; the reference's
+// difference of two depths agrees to rounding).  The stepper's vertical kernels.
+__device__ __forceinline__ void wm_sigma(const VopArgs& a, const double e0[3], const double e1[3], double ft,
+                                         double fb, double wm[6]) {
+  const double gt = 1.0 - ft, gb = 1.0 - fb;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double d = (e1[i] - e0[i]) * a.rdtm;
+    wm[i] = gt * d;
+    wm[3 + i] = gb * d;
+  }
+}
+
 // assemble_vertical_operator (API): writes d [36][L][n], u/w [18][L][n] (compact over els)
 __global__ void __launch_bounds__(128) k_vop(DMesh m, VopArgs a, const int* __restrict__ els, int n,
                                              double* __restrict__ od, double* __restrict__ ou,
@@ -962,7 +976,10 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(6 * NC + i) * VBLK];
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if constexpr (NC == 1)
+      wm_sigma(a, e0, e1, ft, fb, wm);
+    else   // (measured: the momentum forward elimination runs 1.7 % slower with wm_sigma)
+      wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     if (l < L - 1) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = nxt[(6 * NC + k) * VBLK];
@@ -1230,7 +1247,10 @@ __global__ void __launch_bounds__(VBLK, NC == 1 ? 3 : 1) k_vimpl_bwd_r(DMesh m, 
     VG Vl;
     vgeo_x<true, (NC == 1 || SIGU)>(C, eta, ft, fb, a.vc, c, nt, Vl);
     double wm[6];
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    if constexpr (NC == 1)
+      wm_sigma(a, e0, e1, ft, fb, wm);
+    else   // (measured: the momentum forward elimination runs 1.7 % slower with wm_sigma)
+      wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
     // Fo (bottom face of layer l, scaled by -dt as in the forward kernel) and the diffusion
     // pieces cn, pb (vop_dif): S0 = -dt (Fo + pb MHQ), S1 = -dt cn R_{l+1}
     const double cdt = -dt;
@@ -1379,7 +1399,7 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, doubl
     double wt[6], wm[6], wtn[3] = {0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 6; ++i) wt[i] = cur[(12 * NC + i) * VBLK];
-    wm_layer(a, C.b, e0, e1, ft, fb, l, c, L, nt, wm);
+    wm_sigma(a, e0, e1, ft, fb, wm);
     if (l < L - 1) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) wtn[k] = nxt[(12 * NC + k) * VBLK];

@@ -1439,6 +1439,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
     for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
   double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
+  const double rdt = MODE == 2 ? 1.0 / a.dt : 0.0;
   for (int l = 0; l < L; ++l) {
     const double ft = fcur, fb = fnext;
     fcur = fnext;
@@ -1459,6 +1460,89 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         for (int n = 0; n < 6; ++n) qv[cc][n] = qv[cc][n] + jm * SD(shf::MO + cc * 3 + n % 3);
     }
     double acc[NC][6];
+    // per-layer triangle masses: MODE 2 from the per-column sigma forms (scaled by jm)
+    auto msym = [&](int w, double M[3][3]) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) M[p][q] = SD(w + sym6(p, q));
+    };
+    if constexpr (MODE == 2) {
+      // the mass terms first, so their own loads (r, u0) issue together with u and q instead of
+      // at the end of the layer:  out = dt (M0 u0 / dt + M (f u^perp - r / rho0) + M1 F2D/H1
+      // + stresses + volume + lateral)
+      const double j2d = SD(shf::J2D), jj = jm * j2d;
+      double M0[3][3];
+      msym(shf::MH0, M0);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double x0[6], m0x[6];
+        if (SAME) {
+#pragma unroll
+          for (int n = 0; n < 6; ++n) x0[n] = u[cc][n];
+        } else {
+          ld6g_o(a.u0c[cc], lo, ln, x0);
+        }
+        kron_apply(M0, jj, x0, m0x);
+#pragma unroll
+        for (int n = 0; n < 6; ++n) acc[cc][n] = m0x[n] * rdt;
+      }
+      if constexpr (NC >= 2) {
+        double rr[2][6];
+        ld6g_o(a.r, lo, ln, rr[0]);
+        ld6g_o(a.r + P6, lo, ln, rr[1]);
+        double Mu[3][3];
+        msym(shf::MHU, Mu);
+        const double ir = 1.0 / a.rho0;
+        double y0[6], y1[6], m0[6], m1[6];
+#pragma unroll
+        for (int n = 0; n < 6; ++n) {
+          y0[n] = a.f * u[1][n] - rr[0][n] * ir;
+          y1[n] = -a.f * u[0][n] - rr[1][n] * ir;
+        }
+        kron_apply(Mu, jj, y0, m0);
+        kron_apply(Mu, jj, y1, m1);
+        double M1[3][3];
+        msym(shf::MH1, M1);
+        const double kk = (KM[0][0] + KM[0][1]) * jj;
+        double mf[2][3];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const double F0 = SD(shf::F1 + cc * 3), F1v = SD(shf::F1 + cc * 3 + 1), F2 = SD(shf::F1 + cc * 3 + 2);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) mf[cc][p] = kk * (M1[p][0] * F0 + M1[p][1] * F1v + M1[p][2] * F2);
+        }
+#pragma unroll
+        for (int n = 0; n < 6; ++n) {
+          acc[0][n] += m0[n] + mf[0][n % 3];
+          acc[1][n] += m1[n] + mf[1][n % 3];
+        }
+        if (l == 0) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            acc[0][k] += j2d / 6.0 * a.tsx;
+            acc[1][k] += j2d / 6.0 * a.tsy;
+          }
+        }
+        if (l == L - 1 && a.cd != 0.0) {
+          double dx3[3], dy3[3], mx[3], my[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double ubx = u[0][3 + k], uby = u[1][3 + k];
+            const double sp = sqrt(ubx * ubx + uby * uby);
+            dx3[k] = -a.cd * sp * ubx;
+            dy3[k] = -a.cd * sp * uby;
+          }
+          mh_apply3(dx3, j2d, mx);
+          mh_apply3(dy3, j2d, my);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            acc[0][3 + k] += mx[k];
+            acc[1][3 + k] += my[k];
+          }
+        }
+      }
+    }
     {
       double z[2][2][3];
 #pragma unroll
@@ -1486,7 +1570,13 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         for (int lev = 0; lev < 2; ++lev)
 #pragma unroll
           for (int p = 0; p < 3; ++p)
-            acc[cc][3 * lev + p] = j2d * (SD(shf::DX + p) * Sm[lev][0] + SD(shf::DY + p) * Sm[lev][1]);
+          {
+            const double v = j2d * (SD(shf::DX + p) * Sm[lev][0] + SD(shf::DY + p) * Sm[lev][1]);
+            if (MODE == 2)
+              acc[cc][3 * lev + p] += v;
+            else
+              acc[cc][3 * lev + p] = v;
+          }
       }
     }
 #pragma unroll
@@ -1525,23 +1615,13 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         lat_add(acc[cc], k, x, je);
       }
     }
-    // per-layer triangle masses: MODE 2 from the per-column sigma forms (scaled by jm below)
-    auto msym = [&](int w, double M[3][3]) {
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) M[p][q] = SD(w + sym6(p, q));
-    };
-    if constexpr (NC >= 2) {
+    if constexpr (NC >= 2 && MODE != 2) {
       double rr[2][6];
       ld6g_o(a.r, lo, ln, rr[0]);
       ld6g_o(a.r + P6, lo, ln, rr[1]);
       double Mu[3][3];
-      double mscale = SD(shf::J2D);
-      if (MODE == 2) {
-        msym(shf::MHU, Mu);
-        mscale = jm * mscale;
-      } else {
+      const double mscale = SD(shf::J2D);
+      {
         double jz[3], bb[3], eta[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -1597,39 +1677,11 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 #pragma unroll
         for (int k = 0; k < 3; ++k) csum[cc][k] += acc[cc][k] + acc[cc][3 + k];
     } else {
-      const double j2d = SD(shf::J2D);
-      const double jj = jm * j2d;
-      double M0[3][3];
-      msym(shf::MH0, M0);
-      double mf[2][3] = {{0, 0, 0}, {0, 0, 0}};
-      if constexpr (NC >= 2) {
-        double M1[3][3];
-        msym(shf::MH1, M1);
-        const double kk = (KM[0][0] + KM[0][1]) * jj;
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const double F0 = SD(shf::F1 + cc * 3), F1v = SD(shf::F1 + cc * 3 + 1), F2 = SD(shf::F1 + cc * 3 + 2);
-#pragma unroll
-          for (int p = 0; p < 3; ++p) mf[cc][p] = kk * (M1[p][0] * F0 + M1[p][1] * F1v + M1[p][2] * F2);
-        }
-      }
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
-        double x0[6], m0x[6], o[6];
-        if (SAME) {
+        double o[6];
 #pragma unroll
-          for (int n = 0; n < 6; ++n) x0[n] = u[cc][n];
-        } else {
-          ld6g_o(a.u0c[cc], lo, ln, x0);
-        }
-        kron_apply(M0, jj, x0, m0x);
-#pragma unroll
-        for (int n = 0; n < 6; ++n) {
-          if (NC >= 2 && cc < 2)
-            o[n] = m0x[n] + a.dt * (acc[cc][n] + mf[cc][n % 3]);
-          else
-            o[n] = m0x[n] + a.dt * acc[cc][n];
-        }
+        for (int n = 0; n < 6; ++n) o[n] = a.dt * acc[cc][n];
         st6(a.outc[cc], l, c, L, nt, o);
       }
     }
@@ -1743,11 +1795,6 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
   for (int l = 0; l < L; ++l) {
     if (l + 1 < L) {
       stage(l + 1);
-      if (NC >= 2 && a.bulkpf && t < 12) {   // r is read per layer from global: warm it in L2
-        const int c0 = b * TW;
-        const unsigned segb = (unsigned)(min(TW, m.nown - c0) * 8 + 15) & ~15u;
-        bulk_prefetch_l2(a.r + (size_t)(t / 6) * P6 + pix(t % 6, l + 1, c0, L, nt), segb);
-      }
     }
     const double* S = sbuf + (size_t)(l & 1) * NW * tj;
     const double ft = fcur, fb = fnext;

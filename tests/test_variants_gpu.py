@@ -61,7 +61,8 @@ def rel(a, b):
     ({7: 2}, 1e-11),
     ({9: 0}, 1e-12), ({9: 64}, 0.0),
     ({11: 0}, 0.0), ({11: 64}, 0.0),
-    ({5: 1}, 1e-12), ({10: 128}, 1e-12),
+    # 5=1 / 10=128: other stage-RHS kernels (per-layer masses, another summation order)
+    ({5: 1}, 1e-11), ({10: 128}, 1e-11),
     ({6: 0}, 1e-12), ({6: 3}, 1e-12),
     ({12: 3}, 0.0),     # bulk-copy (TMA) ring of the implicit forward elimination: same arithmetic
 ])
