@@ -360,7 +360,8 @@ inline bool first_on_device(unsigned long long& seen) {
 // kernel family at run time through pdg_tune() so one binary can be measured in every variant.
 // keys 1, 2 and 13 are retired (superseded vertical-kernel variants, removed)
 enum TuneKey { TUNE_HRHS = 0, TUNE_R = 3, TUNE_WT = 4, TUNE_HRHS2 = 5, TUNE_RK = 6, TUNE_VSPLIT = 7, TUNE_PF = 8, TUNE_TILE_PRED = 9, TUNE_TILE_STAGE = 10, TUNE_TILE_COL = 11, TUNE_BULKPF = 12, TUNE_NKEYS = 16 };
-constexpr int TUNE_BULK = TUNE_BULKPF;   // bit 0: F3D->2D L2 bulk prefetch; bit 1: bulk-copy rings
+constexpr int TUNE_BULK = TUNE_BULKPF;   // bit 1: bulk-copy (cp.async.bulk) rings; bit 0 retired (the F3D->2D
+                                         // L2 bulk prefetch of r measured no gain once the stage RHS changed)
 int tune_get(int key);
 
 }  // namespace pdg

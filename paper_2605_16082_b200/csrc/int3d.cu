@@ -1037,7 +1037,6 @@ struct HArgs {
   const double* f2d;     // STAGE momentum: [2][3][nt]
   double g, f, rho0, tsx, tsy, cd, dt;
   int mass_terms;
-  int bulkpf;            // 1: L2 bulk prefetch of the tile's next-layer r planes (F3D->2D; nt even only)
   // per-component planes (momentum x, y[, tracer]); filled from u / u0 / out by the entry points
   const double* uc[3];
   const double* u0c[3];
@@ -2372,7 +2371,6 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   a.tsx = tsx;
   a.tsy = tsy;
   a.cd = cd;
-  a.bulkpf = (tune_get(TUNE_BULKPF) & 1) && ctx->nt % 2 == 0;
   Cols cs{nullptr, ctx->nown};
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
