@@ -2,7 +2,7 @@
 graph-replayed step, each build in its own process (PDG_LIB), alternated A B A B.
 
     python scripts/ab_lib.py build/lib_a.so paper_2605_16082_b200/libprismdg_b200.so
-    python scripts/ab_lib.py lib.so lib.so:PDG_FUSE_VEXPL=1      # same build, stepper option via env
+    python scripts/ab_lib.py lib.so "lib.so:PDG_TUNE=6=7"        # same build, pdg_tune key=value[,..]
 """
 import json
 import os
@@ -16,6 +16,11 @@ sys.path.insert(0, ".")
 from paper_2605_16082_b200 import stepper as S
 from paper_2605_16082_b200.scenarios import device_state_c4, make_case
 from bench import Clocks
+import os
+from paper_2605_16082_b200 import _lib
+for kv in filter(None, os.environ.get("PDG_TUNE", "").split(",")):
+    k, v = kv.split("=")
+    _lib.lib().pdg_tune(int(k), int(v))
 c = make_case("c4", with_state=False)
 st = S.ImexStepper(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v)
 device_state_c4(c, st)
