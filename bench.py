@@ -232,6 +232,34 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------------------------------- GPU
 
+def fp64_floor(prof, counts, t_ms, mhz):
+    """The step's FP64 issue floor: executed DFMA + DMUL + DADD warp instructions per launch from the
+    newest profiles/r*_fp64.json (ncu --set full, scripts/fp64_floor.py) at the SM clock measured
+    during the timed region; B200 issues 2 FP64 warp instructions per SM per cycle (64 lanes)."""
+    import glob
+    try:
+        path = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fp64.json")))[-1]
+        with open(path) as f:
+            inst = json.load(f)
+    except (IndexError, OSError, ValueError):
+        return None
+    if not mhz:
+        return None
+    rate = 148 * 2 * mhz * 1e3          # FP64 warp instructions per ms
+    tot, per = 0.0, {}
+    for k, ms in prof.items():
+        if k in inst:
+            n = inst[k]["fp64_warp_inst"]
+        elif k.startswith("subcycle") and all(f"rk_stage{i}" in inst for i in range(3)):
+            n = int(k[len("subcycle"):]) * sum(inst[f"rk_stage{i}"]["fp64_warp_inst"] for i in range(3))
+        else:
+            continue
+        tot += n * counts[k]
+        per[k] = round(n / rate / ms, 3)
+    return {"floor_ms_per_step": tot / rate, "frac_of_step": tot / rate / t_ms, "sm_mhz": mhz,
+            "per_kernel_frac": per, "source": os.path.relpath(path, ROOT)}
+
+
 def pcie_bandwidth(torch, nbytes=1 << 30, reps=3):
     """Measured pinned-host <-> device copy bandwidth (GB/s): H2D alone, D2H alone, both at once."""
     h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
@@ -483,7 +511,8 @@ def main():
                           "halo_exchanges_per_step": (exchanges_per_step(case.m) if world > 1 else 0),
                           "paper_exchanges_per_step": PAPER_EXCHANGES_PER_STEP},
                "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
-               "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+               "roofline": roofline, "fp64": fp64_floor(prof, counts, t_ms, clk.summary().get("sm_mhz")),
+               "cpu_baseline": cpu, "clocks": clk.summary(),
                "kernels": {k: {"ms": round(v["ms"], 4), "share": round(v["share"], 4),
                                "GBps": None if v["GBps"] is None else round(v["GBps"], 1)} for k, v in per.items()},
                "setup_s": setup_s}

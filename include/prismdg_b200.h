@@ -234,6 +234,10 @@ int pdg_halo_plan_create(pdg_comm* comm, int nt, int npeers, const int* peers, c
 int pdg_halo_plan_destroy(pdg_halo_plan* plan);
 int pdg_halo_start(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
 int pdg_halo_finish(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
+/* blocking exchanges under the SURVEY section 8b names: the 2D sub-cycle state (9 C3 planes, the
+ * all-rings plan) and ring-1 3D fields (start + finish) */
+int pdg_halo_2d(pdg_halo_plan* plan, double* state9, void* stream);
+int pdg_halo_3d(pdg_halo_plan* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
 
 /* ---- device-initiated halo exchange over NVLink peer memory (csrc/p2p.cu; SURVEY.md section 8e
  * "LSA peer stores (2D)").  No NCCL: every rank owns an inbox (per peer: an epoch flag and a

@@ -51,6 +51,8 @@ _SIGS = {
     "pdg_halo_plan_destroy": (I, [P]),
     "pdg_halo_start": (I, [P, I, P, P, P]),
     "pdg_halo_finish": (I, [P, I, P, P, P]),
+    "pdg_halo_2d": (I, [P, P, P]),
+    "pdg_halo_3d": (I, [P, I, P, P, P]),
     "pdg_p2p_create": (I, [I, I, P, P, P, P, P, I, I, P]),
     "pdg_p2p_destroy": (I, [P]),
     "pdg_p2p_local": (I, [P, P, P, P, P]),

@@ -245,4 +245,17 @@ int pdg_halo_finish(pdg_halo_plan* p, int nf, double* const* fields, const long 
   return PDG_OK;
 }
 
+// SURVEY.md section 8b names: blocking exchanges of the 2D sub-cycle state (the three C3 fields
+// eta, Qx, Qy: 9 planes, the all-rings plan) and of ring-1 3D fields (start + finish)
+int pdg_halo_2d(pdg_halo_plan* p, double* state9, void* stream) {
+  double* f[1] = {state9};
+  const long long np[1] = {9};
+  const int rc = pdg_halo_start(p, 1, f, np, stream);
+  return rc != PDG_OK ? rc : pdg_halo_finish(p, 1, f, np, stream);
+}
+int pdg_halo_3d(pdg_halo_plan* p, int nf, double* const* fields, const long long* nplanes, void* stream) {
+  const int rc = pdg_halo_start(p, nf, fields, nplanes, stream);
+  return rc != PDG_OK ? rc : pdg_halo_finish(p, nf, fields, nplanes, stream);
+}
+
 }  // extern "C"

@@ -4,6 +4,9 @@ lanes), the time they need at the pipe's peak at a given SM clock, and the kerne
 duration -- the share of the step the FP64 pipe alone accounts for.
 
     python scripts/fp64_floor.py profiles/r2_opt1_raw/full3d.csv [sm_mhz]
+    python scripts/fp64_floor.py --json full3d.csv full2d.csv > profiles/<round>_fp64.json
+          (FP64 warp instructions per launch of each bench.py timer key; bench.py reports the
+           step's FP64 issue floor from the newest one)
 """
 import csv
 import sys
@@ -38,5 +41,30 @@ def main(path, mhz=1750.0):
         print(f"| `{name}` | {ms:.3f} | {inst:.3e} | {floor:.3f} | {floor / ms:.2f} |")
 
 
+def per_key(paths):
+    """bench.py timer key -> FP64 warp instructions per launch (first captured launch of each kernel)."""
+    sys.path.insert(0, __import__("os").path.dirname(__file__))
+    from traffic_json import KEYS
+    inst = {}
+    for path in paths:
+        hdr, units, data = rows(path)
+        ix = {h: i for i, h in enumerate(hdr)}
+        ops = ["smsp__sass_thread_inst_executed_op_%s_pred_on.sum.per_cycle_elapsed" % o for o in ("dfma", "dmul", "dadd")]
+        for x in data:
+            name = x[ix["Kernel Name"]].split("(")[0].replace("void ", "")
+            if name not in inst:
+                inst[name] = sum(float(x[ix[o]]) for o in ops) / 32.0 * float(x[ix["sm__cycles_elapsed.avg"]])
+    out = {}
+    for key, prefixes in KEYS.items():
+        got = [n for pre in prefixes for n in inst if n.startswith(pre)][:len(prefixes)]
+        if len(got) == len(prefixes):
+            out[key] = {"fp64_warp_inst": sum(inst[n] for n in got), "kernel": " + ".join(got), "source": paths[0]}
+    return out
+
+
 if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1750.0)
+    if sys.argv[1] == "--json":
+        import json
+        print(json.dumps(per_key(sys.argv[2:]), indent=1))
+    else:
+        main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1750.0)

@@ -72,3 +72,27 @@ def test_plan_rejects_oversized_message(torch):
     npl = (ctypes.c_longlong * 1)(19)
     from paper_2605_16082_b200.device import stream_ptr
     assert _lib.lib().pdg_halo_start(halo.plans[False], 1, fp, npl, stream_ptr()) != 0
+
+
+def test_halo_2d_3d_entries(torch):
+    """pdg_halo_2d / pdg_halo_3d (the SURVEY section 8b names: blocking start + finish)."""
+    import ctypes
+    from paper_2605_16082_b200 import _lib
+    from paper_2605_16082_b200.device import stream_ptr
+    from paper_2605_16082_b200.partition import NcclHalo
+    rng = np.random.default_rng(5)
+    dev = torch.device("cuda", 0)
+    nt, n_own, L = 200, 150, 3
+    part = _loop_part(nt, n_own, rng)
+    halo = NcclHalo(part, nt, dev, L)
+    lb = _lib.lib()
+    S = torch.as_tensor(rng.standard_normal((3, 3, nt)), device=dev)
+    _lib.check(lb.pdg_halo_2d(halo.plans[True], ctypes.c_void_p(S.data_ptr()), stream_ptr()), "halo_2d")
+    a = torch.as_tensor(rng.standard_normal((6, L, nt)), device=dev)
+    fp = (ctypes.c_void_p * 1)(a.data_ptr())
+    npl = (ctypes.c_longlong * 1)(6 * L)
+    _lib.check(lb.pdg_halo_3d(halo.plans[False], 1, fp, npl, stream_ptr()), "halo_3d")
+    torch.cuda.synchronize()
+    sn, an = S.cpu().numpy(), a.cpu().numpy()
+    assert np.array_equal(sn[..., part.recv[0]], sn[..., part.send[0]])
+    assert np.array_equal(an[..., part.recv1[0]], an[..., part.send1[0]])
