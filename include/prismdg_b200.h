@@ -282,6 +282,12 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
 int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
                       const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
                       double dt, const double* rhs, const double* xin, double* x, void* stream);
+/* the same over a list of owned columns (partitioned runs: boundary columns first, then the interior
+ * while the ring-1 exchange of the boundary result is in flight) */
+int pdg_step_vertical_cols(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
+                           const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0,
+                           int order, double dt, const double* rhs, const double* xin, double* x, const int* cols,
+                           int ncols, void* stream);
 
 /* explicit vertical stage of momentum (ncomp 2) and tracer in one pass */
 /* diagnostics_2d (external2d.py:366-380) and budget_3d (internal3d.py:942-951) of the resident state

@@ -93,6 +93,7 @@ _SIGS = {
     "pdg_solve_tridiagonal": (I, [I, I, P, P, P, P, P, P, P, P]),
     "pdg_assemble_vertical": (I, [P, P, P, P, D, D, D, I, P, I, P, P, P, P]),
     "pdg_step_vertical": (I, [P, I, I, P, P, P, D, P, D, D, D, I, D, P, P, P, P]),
+    "pdg_step_vertical_cols": (I, [P, I, I, P, P, P, D, P, D, D, D, I, D, P, P, P, P, I, P]),
     "pdg_step_diagnostics": (I, [P, P, P, P, D, P, P, P]),
     "pdg_diagnostics_work_doubles": (I, [P]),
 }

@@ -382,10 +382,12 @@ constexpr int NVC = 8;
 #define PDG_SIGU 1
 #endif
 constexpr bool SIGU = PDG_SIGU != 0;
-__global__ void k_vcol(DMesh m, const double* __restrict__ eta_u, double* __restrict__ vc) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_vcol(DMesh m, const double* __restrict__ eta_u, double* __restrict__ vc,
+                       const int* __restrict__ cols, int ncols) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
-  if (c >= m.nown) return;
+  if (i >= (cols ? ncols : m.nown)) return;
+  const int c = cols ? cols[i] : i;
   double H[3], hqv[6], ih[6];
 #pragma unroll
   for (int k = 0; k < 3; ++k) H[k] = __dsub_rn(__ldg(eta_u + k * nt + c), __ldg(m.b + k * nt + c));
@@ -706,6 +708,12 @@ struct VopArgs {
   double kh, kv, n0;
   int order;
   const double* vc = nullptr;  // kh == 0 kernels: per-column sigma constants [8][nt] (k_vcol)
+  // stepper kernels: optional column list (partitioned runs: boundary columns first, so the
+  // ring-1 exchange of the result overlaps the interior columns); null = all owned columns
+  const int* cols = nullptr;
+  int ncols = 0;
+  __device__ __forceinline__ int ncol(const DMesh& m) const { return cols ? ncols : m.nown; }
+  __device__ __forceinline__ int col(int i) const { return cols ? cols[i] : i; }
 };
 
 // node values of w_m at layer l
@@ -894,8 +902,9 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
   const int t = threadIdx.x;
   // BULK: every thread runs the layer loop (the block barriers must be met by all of them, also
   // inside a warp); threads past the owned range repeat the last owned column and store nothing
-  const bool act = blockIdx.x * VBLK + t < m.nown;
-  const int c = act ? blockIdx.x * VBLK + t : m.nown - 1;
+  const int nc = a.ncol(m);
+  const bool act = blockIdx.x * VBLK + t < nc;
+  const int c = a.col(act ? blockIdx.x * VBLK + t : nc - 1);
   const int nt = m.nt, L = m.L;
   const int c0 = blockIdx.x * VBLK;
   for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
@@ -1161,9 +1170,10 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vimpl_fwd(DMesh m, VopArgs a, do
 // streaming (30 + 6 NC words in, 6 NC out per prism), high occupancy.
 template <int NC>
 __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, const double* __restrict__ Gs,
-                                                  double* x, const pdg_err* err) {
-  const int c = blockIdx.x * VBLK + threadIdx.x;
-  if (c >= nown || err->code == PDG_ERR_ZERO_PIVOT) return;
+                                                  double* x, const pdg_err* err, const int* __restrict__ cols) {
+  const int i0 = blockIdx.x * VBLK + threadIdx.x;
+  if (i0 >= nown || err->code == PDG_ERR_ZERO_PIVOT) return;
+  const int c = cols ? cols[i0] : i0;
   const size_t P6 = (size_t)6 * L * nt;
   double xn[6][NC];
 #pragma unroll
@@ -1209,9 +1219,10 @@ __global__ void __launch_bounds__(VBLK) k_vimpl_bwd(int nown, int nt, int L, con
 template <int NC>
 __global__ void __launch_bounds__(VBLK, NC == 1 ? 3 : 1) k_vimpl_bwd_r(DMesh m, VopArgs a, double dt, const double* __restrict__ Gs,
                                                     double* x) {
-  const int c = blockIdx.x * VBLK + threadIdx.x;
+  const int i0 = blockIdx.x * VBLK + threadIdx.x;
   const int nt = m.nt, L = m.L;
-  if (c >= m.nown || m.err->code == PDG_ERR_ZERO_PIVOT) return;
+  if (i0 >= a.ncol(m) || m.err->code == PDG_ERR_ZERO_PIVOT) return;
+  const int c = a.col(i0);
   const size_t P6 = (size_t)6 * L * nt;
   Col C;
   load_col(m, c, C);
@@ -1336,11 +1347,12 @@ __global__ void __launch_bounds__(VBLK, MINB) k_vexpl3(DMesh m, VopArgs a, doubl
   constexpr bool FCS = NC == 1;
   double* fc = fr + m.L + 1;       // [12][VBLK] carried face pieces (FCS)
   const int t = threadIdx.x;
-  const int c = blockIdx.x * VBLK + t;
+  const int i0 = blockIdx.x * VBLK + t;
   const int nt = m.nt, L = m.L;
   for (int i = t; i <= L; i += VBLK) fr[i] = m.fracs[i];
   __syncthreads();
-  if (c >= m.nown) return;
+  if (i0 >= a.ncol(m)) return;
+  const int c = a.col(i0);
   const size_t P6 = (size_t)6 * L * nt;
   auto stage = [&](int l) {
     if (l < L) {
@@ -1600,13 +1612,20 @@ int pdg_assemble_vertical(pdg_ctx* ctx, const double* eta_g, const double* wt, c
 //   implicit, kh == 0 and TUNE_VSPLIT 4 (default): k_vimpl_fwd (18-word E tiles) + k_vimpl_bwd_r
 //       (coupling blocks rebuilt); otherwise k_vimpl_fwd (30-word tiles) + k_vimpl_bwd
 //   explicit: k_vexpl3 (blocks of dt A assembled once per layer)
-int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
-                      const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
-                      double dt, const double* rhs, const double* xin, double* x, void* stream) {
+//   cols / ncols (optional): only the listed owned columns (partitioned runs: the boundary columns,
+//   then the interior ones while the ring-1 exchange of the first part is in flight)
+int pdg_step_vertical_cols(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
+                           const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0,
+                           int order, double dt, const double* rhs, const double* xin, double* x, const int* cols,
+                           int ncols, void* stream) {
   if (ncomp != 1 && ncomp != 2) return PDG_ERR_SHAPE;
+  if (cols && ncols <= 0) return PDG_OK;
   VopArgs a{eta_u, wt, nullptr, eta0, eta1, dt_mesh, 1.0 / dt_mesh, kh, kv, n0, order};
+  a.cols = cols;
+  a.ncols = ncols;
   const int nt = ctx->nt;
-  const dim3 grid(nblocks(ctx->nown, VBLK)), blk(VBLK);
+  const int ncol = cols ? ncols : ctx->nown;
+  const dim3 grid(nblocks(ncol, VBLK)), blk(VBLK);
   cudaStream_t strm = (cudaStream_t)stream;
   DMesh m = ctx->view();
   const bool ct = implicit && kh == 0.0 && tune_get(TUNE_VSPLIT) == 4;
@@ -1614,7 +1633,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
   if (kh == 0.0 && (ncomp == 1 || (SIGU && implicit))) {
     double* vc = ctx->vcol();
     if (!vc) return PDG_ERR_CUDA;
-    k_vcol<<<nblocks(ctx->nown, 256), 256, 0, strm>>>(m, eta_u, vc);
+    k_vcol<<<nblocks(ncol, 256), 256, 0, strm>>>(m, eta_u, vc, cols, ncols);
     if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
     a.vc = vc;
   }
@@ -1636,7 +1655,7 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     }
     if (ct) {
       // bulk-copy ring: plane segments are 16-byte aligned when nt is even (TUNE_BULK bit 1 = on)
-      const bool bulk = nt % 2 == 0 && (tune_get(TUNE_BULK) & 2);
+      const bool bulk = !cols && nt % 2 == 0 && (tune_get(TUNE_BULK) & 2);
       if (ncomp == 2) {
         if (bulk)
           k_vimpl_fwd<2, 1, true, true, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
@@ -1659,14 +1678,14 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
         else
           k_vimpl_fwd<2, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
         if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
-        k_vimpl_bwd<2><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
+        k_vimpl_bwd<2><<<grid, blk, 0, strm>>>(ncol, nt, ctx->L, Gs, x, m.err, cols);
       } else {
         if (kh == 0.0)
           k_vimpl_fwd<1, 1, true><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
         else
           k_vimpl_fwd<1, 1, false><<<grid, blk, sm, strm>>>(m, a, dt, rhs, Gs, x);
         if (check_launch(ctx) != PDG_OK) return PDG_ERR_CUDA;
-        k_vimpl_bwd<1><<<grid, blk, 0, strm>>>(ctx->nown, nt, ctx->L, Gs, x, m.err);
+        k_vimpl_bwd<1><<<grid, blk, 0, strm>>>(ncol, nt, ctx->L, Gs, x, m.err, cols);
       }
     }
   } else {
@@ -1692,6 +1711,13 @@ int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u
     }
   }
   return check_launch(ctx);
+}
+
+int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,
+                      const double* eta1, double dt_mesh, const double* wt, double kh, double kv, double n0, int order,
+                      double dt, const double* rhs, const double* xin, double* x, void* stream) {
+  return pdg_step_vertical_cols(ctx, ncomp, implicit, eta_u, eta0, eta1, dt_mesh, wt, kh, kv, n0, order, dt, rhs, xin,
+                                x, nullptr, 0, stream);
 }
 
 

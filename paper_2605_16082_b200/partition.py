@@ -691,7 +691,7 @@ class PartitionedRun:
             ph, name = phases.pop()
             if name in self._skip_exchanges:      # tests: a deliberately broken schedule
                 continue
-            if ph != "start":
+            if ph not in ("start", "start1"):     # one device: a boundary-first exchange moves at its join
                 self.group.exchange_all(fields, deep=ph in ("finish", "deep"))
 
     def _capture(self, key):
