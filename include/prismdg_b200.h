@@ -256,6 +256,9 @@ int pdg_p2p_connect(pdg_p2p* plan, int slot, const void* ipc_handle64, void* raw
 int pdg_p2p_start(pdg_p2p* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
 int pdg_p2p_finish(pdg_p2p* plan, int nfields, double* const* fields, const long long* nplanes, void* stream);
 
+/* device-to-device copy of `bytes` on `stream` (csrc/hostio.cu) */
+int pdg_copy_d2d(void* dst, const void* src, long long bytes, void* stream);
+
 /* ---- host I/O layout conversion (set_state / get_state of the drop-in; csrc/hostio.cu):
  * rows [ncols][L][nk] = columns [c0, c0 + ncols) of a reference-layout field ((P, nk) with
  * p = c L + l, or (nt, nk) with L = 1) in a device staging buffer  <->  planes [nk][L][nt] */

@@ -52,6 +52,7 @@ _SIGS = {
     "pdg_halo_start": (I, [P, I, P, P, P]),
     "pdg_halo_finish": (I, [P, I, P, P, P]),
     "pdg_halo_2d": (I, [P, P, P]),
+    "pdg_copy_d2d": (I, [P, P, LL, P]),
     "pdg_halo_3d": (I, [P, I, P, P, P]),
     "pdg_p2p_create": (I, [I, I, P, P, P, P, P, I, I, P]),
     "pdg_p2p_destroy": (I, [P]),

@@ -73,4 +73,13 @@ int pdg_rows_to_planes(const double* rows, int ncols, int L, int nk, double* pla
 int pdg_planes_to_rows(const double* planes, int nt, int c0, int ncols, int L, int nk, double* rows, void* stream) {
   return launch_rp(false, planes, rows, ncols, L, nk, nt, c0, stream);
 }
+// device-to-device copy on the caller's stream (the step's 2D working-state copies: the stepper
+// graph holds only library launches and copies, no framework kernels)
+int pdg_copy_d2d(void* dst, const void* src, long long bytes, void* stream) {
+  if (bytes <= 0) return PDG_OK;
+  return cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) == cudaSuccess
+             ? PDG_OK
+             : PDG_ERR_CUDA;
+}
+
 }  // extern "C"

@@ -284,7 +284,7 @@ class ImexStepper:
                ptr(self.f3d2d), s)
         if part:
             yield ("deep", [self.f3d2d], "f3d2d")   # the ring columns' RK stages need their forcing
-        Sw.copy_(self.S)
+        self._c("copy", lb.pdg_copy_d2d(ptr(Sw), ptr(self.S), self.S.numel() * 8, s))
         dt2 = dt_s / m_s
         if not part:
             tm(f"subcycle{m_s}", lb.pdg_ext2d_subcycle, h, ptr(Sw), m_s, dt2, p.g, p.rho0, ptr(self.f3d2d), None,
@@ -364,7 +364,7 @@ class ImexStepper:
                                        self.m // 2, True, t0)
         yield from self._stage(s, eta_h, U[b], T[b], U[a], T[a], self.Sw[1], U[c], T[c], self.dt, self.m, False,
                                t0 + 0.5 * self.dt)
-        self.S.copy_(self.Sw[1])
+        self._c("copy", _lib.lib().pdg_copy_d2d(ptr(self.S), ptr(self.Sw[1]), self.S.numel() * 8, s))
 
     def _launch_step(self, t0):
         tr = self.phase_trace
