@@ -69,7 +69,7 @@ class ImexStepper:
         # partitions (>= 3 ghost rings): the RK stages of a substep run on owned + rings 1-2, owned +
         # ring 1 and owned columns, so the 2D state is exchanged once per substep; the last stage
         # updates the columns other ranks receive first and the rest while the exchange is in flight
-        self.cols2d = self.cols3d = None
+        self.cols2d = None
         if part is not None:
             if part.ring is None or part.ring.size and part.ring.max() < 3:
                 raise ValueError("partitioned stepping needs 3 ghost rings (partition.decompose depth=3)")
@@ -81,13 +81,6 @@ class ImexStepper:
             sets = (np.flatnonzero(ring <= 2), np.flatnonzero(ring <= 1), np.flatnonzero(sent),
                     np.flatnonzero(~sent))
             self.cols2d = tuple(torch.as_tensor(x.astype(np.int32), device=self.dev) for x in sets)
-            # 3D ring-1 exchanges (q, u/T) are boundary-first too: the owned columns some other rank
-            # receives are computed first, the exchange is posted, then the interior columns
-            sent1 = np.zeros(n_own, bool)
-            for idx in part.send1.values():
-                sent1[idx] = True
-            self.cols3d = tuple(torch.as_tensor(x.astype(np.int32), device=self.dev)
-                                for x in (np.flatnonzero(sent1), np.flatnonzero(~sent1)))
         self.cur = 0
         self.t = 0.0
         self.graphs = {}
@@ -269,14 +262,13 @@ class ImexStepper:
             self._poison([self.q, self.mis, out_u, out_T], False)
             self._poison([self.f3d2d], True)
         tm("r", lb.pdg_compute_r, h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s)
-        if not part:
-            tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
-               ptr(self.qsum), ptr(self.htot), s)
-        else:   # boundary columns, post the ring-1 exchange of q, interior columns, join
-            for i, cols in enumerate(self.cols3d):
-                tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, ptr(cols),
-                   cols.numel(), ptr(self.q), ptr(self.qsum), ptr(self.htot), s)
-                yield ("start1" if i == 0 else "finish1", [self.q], "q")
+        tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
+           ptr(self.qsum), ptr(self.htot), s)
+        # the 3D ring-1 exchanges block the stream: a boundary-first split (boundary columns, post,
+        # interior) was measured slower -- the extra launch of the 50-layer column loops costs a
+        # latency-bound partial wave (~0.3-0.6 ms per call at 8 ranks) against ~30 us of transfer
+        if part:
+            yield ("all", [self.q], "q")
         tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
         if p.kappa_h:   # explicit horizontal viscosity in horizontal_rhs: its column sum (csrc/hdiff.cu)
@@ -328,16 +320,6 @@ class ImexStepper:
             tm("hdiff_T", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(T), 1, p.nu_h, 0, dt_s, 0, None, 0,
                ptr(out_T), s)
         pe = self.pen
-        if part:   # boundary columns, post the ring-1 exchange of u and T, interior columns, join
-            for i, cols in enumerate(self.cols3d):
-                tm(f"vertical_u_{tag}", lb.pdg_step_vertical_cols, h, 2, int(implicit), ptr(eta_u), ptr(eta0),
-                   ptr(eta1), dt_s, ptr(self.wt), p.kappa_h, self.kv, pe.n0, pe.order, dt_s, ptr(out_u), ptr(u),
-                   ptr(out_u), ptr(cols), cols.numel(), s)
-                tm(f"vertical_T_{tag}", lb.pdg_step_vertical_cols, h, 1, int(implicit), ptr(eta_u), ptr(eta0),
-                   ptr(eta1), dt_s, ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T),
-                   ptr(out_T), ptr(cols), cols.numel(), s)
-                yield ("start1" if i == 0 else "finish1", [out_u, out_T], "uT")
-            return eta1
         conc = self.concurrent_vertical and self.prof is None
         if conc:   # the tracer solve on a second stream (own workspace): overlaps the momentum solve
             main = torch.cuda.current_stream(self.dev)
@@ -354,6 +336,8 @@ class ImexStepper:
         else:
             tm(f"vertical_T_{tag}", lb.pdg_step_vertical, h, 1, int(implicit), ptr(eta_u), ptr(eta0), ptr(eta1), dt_s,
                ptr(self.wt), p.nu_h, self.nu_v, pe.n0, pe.order, dt_s, ptr(out_T), ptr(T), ptr(out_T), s)
+        if part:
+            yield ("all", [out_u, out_T], "uT")
         return eta1
 
     def _step_gen(self, t0):

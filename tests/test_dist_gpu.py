@@ -47,8 +47,7 @@ def test_two_process_partition_matches_single(tmp_path):
         assert rows[0] == "step,rank,phase,micros"
         names = {x.split(",")[2] for x in rows[1:]}
         assert {"boundary:state2d", "pack+post:state2d", "interior:state2d", "join+unpack:state2d",
-                "boundary:q", "pack+post:q", "interior:q", "join+unpack:q",
-                "boundary:uT", "pack+post:uT", "interior:uT", "join+unpack:uT", "exchange:mis"} <= names, names
+                "exchange:q", "exchange:uT", "exchange:mis"} <= names, names
         assert all(float(x.split(",")[3]) >= 0.0 and x.split(",")[1] == str(r) for x in rows[1:])
 
 

@@ -74,3 +74,34 @@ def test_variant_matches_default(case, setting, tol):
         err = rel(got[k], ref[k])
         assert err <= tol, (setting, k, err)
 
+
+
+@pytest.mark.parametrize("implicit", [1, 0])
+def test_vertical_column_lists_bitwise(case, implicit):
+    """pdg_step_vertical_cols over two complementary column lists == one launch over all columns
+    (per-column work; the lists may be in any order)."""
+    import torch
+    from paper_2605_16082_b200.device import ptr, stream_ptr
+    pdg, c, lib, defaults = case
+    for k, v in defaults.items():
+        lib.pdg_tune(k, v)
+    st = pdg.stepper.ImexStepper(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v)
+    st.use_graph = False
+    st.set_state(**c.state)
+    st.step(1)
+    h, pe, eta, u = st.dm.h, st.pen, st.S[0], st.U[st.cur]
+    rng = np.random.default_rng(11)
+    perm = rng.permutation(c.mesh.nt).astype(np.int32)
+    parts = [torch.as_tensor(np.sort(perm[:97])), torch.as_tensor(perm[97:])]
+    outs = []
+    for lists in (None, parts):
+        out = torch.zeros_like(u)
+        for cols in ([None] if lists is None else lists):
+            cd = None if cols is None else cols.to("cuda")
+            rc = lib.pdg_step_vertical_cols(h, 2, implicit, ptr(eta), ptr(eta), ptr(eta), 0.5 * c.dt, ptr(st.wt), 0.0,
+                                            st.kv, pe.n0, pe.order, 0.5 * c.dt, ptr(u), ptr(u), ptr(out), ptr(cd),
+                                            0 if cd is None else cd.numel(), stream_ptr())
+            assert rc == 0
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
