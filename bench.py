@@ -460,8 +460,9 @@ def main():
             te = float(tt.item())
         pcie = pcie_bandwidth(torch)
         # floor of the host round trip: a step needs its whole state uploaded before it starts and the
-        # previous state's download overlaps the next upload on the other PCIe direction
-        floor_ms = max(h2d / pcie["h2d_GBps"], h2d / pcie["d2h_GBps"]) / 1e6 + t_ms
+        # previous state's download overlaps the next upload on the other PCIe direction -- so both
+        # directions are busy at once and share the measured bidirectional bandwidth
+        floor_ms = max(h2d / pcie["h2d_GBps"], h2d / pcie["d2h_GBps"], 2 * h2d / pcie["bidir_GBps"]) / 1e6 + t_ms
         pcie.update(floor_ms=floor_ms, frac_of_floor=floor_ms / te,
                     achieved_io_GBps=h2d / max(te - t_ms, 1e-9) / 1e6)
         e2e = {"value": dof_per_step / (te * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
