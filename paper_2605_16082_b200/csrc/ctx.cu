@@ -7,7 +7,7 @@
 #include "ctx.cuh"
 
 static thread_local char g_errbuf[512] = "";
-static int g_tune[pdg::TUNE_NKEYS] = {1, 1, 1, 3, 4, 8, 2, 4, 0, 128, 0, 128, 1, 1, 0, 0};  // measured: scripts/tune.py
+static int g_tune[pdg::TUNE_NKEYS] = {1, 1, 1, 3, 4, 8, 8, 4, 0, 128, 0, 128, 1, 1, 0, 0};  // measured: scripts/tune.py
 
 namespace pdg {
 int tune_get(int key) { return (key >= 0 && key < TUNE_NKEYS) ? g_tune[key] : 1; }

@@ -204,14 +204,22 @@ __global__ void k_ext2d_eval(DMesh m, Ext2DIn a, const int* __restrict__ els, in
 // STAGE 0: Y = S0 + dt d(X);  1: Y = 3/4 S0 + 1/4 (X + dt d);  2: Y = S0/3 + 2/3 (X + dt d), qbar += Y.q
 // els (optional): the columns to update (partitioned runs split owned columns into those next to
 // ghost columns and the interior, so the halo exchange overlaps the interior update)
-template <int STAGE, int BS = 256, int MINB = 2>
+// PDL: programmatic dependent launch -- the next stage's blocks may start while this grid drains;
+// they load the (static) geometry, then wait (griddepcontrol.wait) for this grid's results
+template <int STAGE, int BS = 256, int MINB = 2, bool PDL = false>
 __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const double* S0,
                                                      double* Y, double dt, double* __restrict__ qbar,
                                                      const int* __restrict__ els = nullptr, int n_els = 0) {
+  if constexpr (PDL) asm volatile("griddepcontrol.launch_dependents;");
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int nt = m.nt;
   if (i >= (els ? n_els : m.nown)) return;
   const int c = els ? els[i] : i;
+  Col2 C;
+  if constexpr (PDL) {
+    load_col2(m, c, C);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   // issue the substep-start and Qbar loads first: they are independent of the flux work below,
   // so their latency overlaps it instead of being exposed at the end (stages 1, 2)
   double s0[3][3], qb[2][3];
@@ -226,8 +234,7 @@ __global__ void __launch_bounds__(BS, MINB) k_rk_stage(DMesh m, Ext2DIn a, const
 #pragma unroll
       for (int k = 0; k < 3; ++k) qb[f][k] = qbar[(size_t)(f * 3 + k) * nt + c];
   }
-  Col2 C;
-  load_col2(m, c, C);
+  if constexpr (!PDL) load_col2(m, c, C);
   double r[3][3], xo[9];
   ext2d_residual<Col2, true>(m, C, c, a, r[0], r[1], r[2], xo);
   const double* X = nullptr;
@@ -411,9 +418,24 @@ int pdg_ext2d_subcycle(pdg_ctx* ctx, double* S, int msub, double dt, double g, d
     return PDG_ERR_CUDA;
   if (cudaMemsetAsync(qbar, 0, (size_t)6 * nt * sizeof(double), s) != cudaSuccess) return PDG_ERR_CUDA;
   const int variant = tune_get(TUNE_RK);
-  const int bs = variant == 2 || variant == 3 || variant == 5 || variant == 6 ? 128 : 256, nb = nblocks(ctx->nown, bs);
+  const int bs = variant == 2 || variant == 3 || variant == 5 || variant == 6 || variant == 8 ? 128 : 256,
+            nb = nblocks(ctx->nown, bs);
+  // variant 8: as 2, with programmatic dependent launch between the stage kernels
+  auto pdl = [&](auto kern, auto... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(bs);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+  };
 #define RK_LAUNCH(ST, ...)                                                              \
   switch (variant) {                                                                    \
+    case 8: pdl(k_rk_stage<ST, 128, 4, true>, __VA_ARGS__, (const int*)nullptr, 0); break; \
     case 2: k_rk_stage<ST, 128, 4><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
     case 3: k_rk_stage<ST, 128, 3><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \
     case 4: k_rk_stage<ST, 256, 1><<<nb, bs, 0, s>>>(__VA_ARGS__); break;               \

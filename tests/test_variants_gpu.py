@@ -7,7 +7,8 @@ library for A/B runs (scripts/ab_tune.py) and must keep producing the same answe
   key 9  F3D->2D: 0 register kernel, 64 / 128 tile-staged (shared-memory neighbour traces)
   key 11 r / w~: 0 register kernels, 64 / 128 tile-staged
   key 5  stage RHS: 1 register kernel (128-thread blocks), 8 shared-memory column constants
-  key 6  2D RK stage occupancy variant (register allocation can change FMA contraction)
+  key 6  2D RK stage occupancy variant (register allocation can change FMA contraction); 8 (default)
+         = 2 launched with programmatic dependent launch (same kernel arithmetic)
   key 12 bit 1: cp.async.bulk (copy-engine) staging ring + mbarriers in the implicit forward
          elimination instead of per-thread cp.async (900 columns: the last block splits a warp)
 Tile-staged and register kernels do the same arithmetic (bitwise equal), except the tile-staged
@@ -63,7 +64,7 @@ def rel(a, b):
     ({11: 0}, 0.0), ({11: 64}, 0.0),
     # 5=1 / 10=128: other stage-RHS kernels (per-layer masses, another summation order)
     ({5: 1}, 1e-11), ({10: 128}, 1e-11),
-    ({6: 0}, 1e-12), ({6: 3}, 1e-12),
+    ({6: 0}, 1e-12), ({6: 3}, 1e-12), ({6: 2}, 0.0),   # default 8 = 2 + programmatic dependent launch
     ({12: 3}, 0.0),     # bulk-copy (TMA) ring of the implicit forward elimination: same arithmetic
 ])
 def test_variant_matches_default(case, setting, tol):
