@@ -506,6 +506,24 @@ int pdg_ext2d_rk_stage_cols(pdg_ctx* ctx, int stage, const double* X, const doub
   DMesh m = ctx->view();
   const int nb = nblocks(n_els, 128);
   Ext2DIn a{X, X + (size_t)3 * nt, X + (size_t)6 * nt, f3d2d, nullptr, nullptr, 0, 0.0, g, rho0};
+  if (tune_get(TUNE_RK) == 8) {   // programmatic dependent launch (see pdg_ext2d_subcycle)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (stage == 0)
+      cudaLaunchKernelEx(&cfg, k_rk_stage<0, 128, 4, true>, m, a, S0, Y, dt, qbar, els, n_els);
+    else if (stage == 1)
+      cudaLaunchKernelEx(&cfg, k_rk_stage<1, 128, 4, true>, m, a, S0, Y, dt, qbar, els, n_els);
+    else
+      cudaLaunchKernelEx(&cfg, k_rk_stage<2, 128, 4, true>, m, a, S0, Y, dt, qbar, els, n_els);
+    return check_launch(ctx);
+  }
   if (stage == 0)
     k_rk_stage<0, 128, 4><<<nb, 128, 0, s>>>(m, a, S0, Y, dt, qbar, els, n_els);
   else if (stage == 1)
