@@ -269,6 +269,15 @@ int pdg_planes_to_rows(const double* planes, int nt, int c0, int ncols, int L, i
 /* F3D->2D = column sum of horizontal_rhs(u, q, fac(q)) + stress_rhs  -> [2][3][nt] */
 int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r, double g,
                    double f, double rho0, double tsx, double tsy, double cd, double* f3d2d, void* stream);
+/* the same with rsum (optional) = the per-column layer sum of jm (r_top + r_bot) from pdg_step_r:
+ * the tile-staged kernel then loads no r (the F3D->2D mass term is linear in r) */
+int pdg_step_f3d2d_rsum(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r,
+                        const double* rsum, double g, double f, double rho0, double tsx, double tsy, double cd,
+                        double* f3d2d, void* stream);
+/* the stepper's baroclinic head from T (EOS inline) -> r [2][6][L][nt]; with the tile-staged
+ * kernel also rsum [2][3][nt] (*rsum_written = 1) */
+int pdg_step_r(pdg_ctx* ctx, const double* eta_g, const double* T, double alpha, double tref, double g, double* r,
+               double* rsum, int* rsum_written, void* stream);
 /* stage right-hand sides: ncomp 2: M0 u0 + dt (F_h(u, q + Jz mis) + stress + M1 F2D/H1);
  * ncomp 1: M0 T0 + dt F_T(T, q + Jz mis) */
 int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta0, const double* eta1,

@@ -83,6 +83,8 @@ _SIGS = {
     "pdg_mass_terms": (I, [I, I, P, P, P, D, D, P, P]),
     "pdg_stress_rhs": (I, [P, P, P, D, D, D, P, I, P, P]),
     "pdg_step_f3d2d": (I, [P, P, P, P, P, D, D, D, D, D, D, P, P]),
+    "pdg_step_f3d2d_rsum": (I, [P, P, P, P, P, P, D, D, D, D, D, D, P, P]),
+    "pdg_step_r": (I, [P, P, P, D, D, D, P, P, P, P]),
     "pdg_step_rhs": (I, [P, I, P, P, P, P, P, P, P, P, P, D, D, D, D, D, D, D, P, P]),
     "pdg_step_rhs_ut": (I, [P, P, P, P, P, P, P, P, P, P, P, P, D, D, D, D, D, D, D, P, P, P]),
     # columns (csrc/columns.cu)

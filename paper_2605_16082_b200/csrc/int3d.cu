@@ -726,7 +726,8 @@ template <bool FROM_T, int TW>
 __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const double* __restrict__ eta_g, double alpha,
                                                    double tref, double g, const __grid_constant__ StagePlanes sp,
                                                    const int* __restrict__ tslot, const int* __restrict__ halo,
-                                                   const int* __restrict__ hoff, int tj, double* __restrict__ r) {
+                                                   const int* __restrict__ hoff, int tj, double* __restrict__ r,
+                                                   double* __restrict__ rsum) {
   extern __shared__ double sbuf[];  // [2][6][tj], then the sigma fractions [L + 1], then ints [6][TW]
   TileStage<6, TW> ts;
   ts.init(m, halo, hoff);
@@ -756,6 +757,9 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
   const double j2d = ts.act ? C.j2d : 0.0;
   const double f6 = 6.0 / j2d;  // Mh^-1 factor (columns.py:59-69), once per column
   double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  // rsum (optional): sum over the layers of jm (r_top + r_bot) per corner, the only form of r the
+  // F3D->2D column sum needs (its mass term is linear in r and Mjz = jm Mjz(H) on sigma layers)
+  double rs[2][3] = {{0, 0, 0}, {0, 0, 0}};
   double prevb[3] = {0, 0, 0};
   cp_async_wait0();
   __syncthreads();
@@ -856,6 +860,7 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
           s[d][a] = s[d][a] + (gt[a] + gb[a]);
           out[a] = -s[d][a] + 2.0 * gb[a];
           out[3 + a] = -s[d][a];
+          rs[d][a] += jm * (out[a] + out[3 + a]);
         }
         st6(r + d * P6, l, c, L, nt, out);
       }
@@ -864,6 +869,12 @@ __global__ void __launch_bounds__(TW, 384 / TW) k_compute_r_t(DMesh m, const dou
     }
     cp_async_wait0();
     __syncthreads();
+  }
+  if (rsum && ts.act) {
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) rsum[(d * 3 + a) * nt + c] = rs[d][a];
   }
 }
 
@@ -995,6 +1006,7 @@ struct HArgs {
   const double* uc[3];
   const double* u0c[3];
   double* outc[3];
+  const double* rsum = nullptr;   // F3D->2D: per-column layer sum of jm (r_top + r_bot) (RS kernels)
 };
 
 __device__ __forceinline__ void mjz(const double jz[3], double M[3][3]) {
@@ -1657,7 +1669,9 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
 // neighbour -- is then read from shared memory through the precomputed slot map, so the layer
 // loop never waits on a scattered HBM/L2 gather.  Arithmetic is identical to k_hrhs (bitwise).
 
-template <int NC, int MODE, int TW>
+// RS (MODE 1): the r terms come as their per-column layer sum (k_compute_r_t rsum), so the layer
+// loop loads no r at all
+template <int NC, int MODE, int TW, bool RS = false>
 __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const __grid_constant__ StagePlanes sp,
                                                        const int* __restrict__ tslot, const int* __restrict__ halo,
                                                        const int* __restrict__ hoff, int tj, double* __restrict__ out) {
@@ -1875,7 +1889,38 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
           }
         }
       }
-      if constexpr (NC >= 2) {
+      if constexpr (NC >= 2 && MODE == 1 && RS) {
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          ysum[0][n] += jm * (a.f * (u[1][n] + u[1][3 + n]));
+          ysum[1][n] += jm * (-a.f * (u[0][n] + u[0][3 + n]));
+        }
+        if (l == 0) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            csum[0][k] += j2d / 6.0 * a.tsx;
+            csum[1][k] += j2d / 6.0 * a.tsy;
+          }
+        }
+        if (l == L - 1 && a.cd != 0.0) {   // bottom drag
+          double dx3[3], dy3[3], mx[3], my[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double ubx = u[0][3 + k], uby = u[1][3 + k];
+            const double sp = sqrt(ubx * ubx + uby * uby);
+            dx3[k] = -a.cd * sp * ubx;
+            dy3[k] = -a.cd * sp * uby;
+          }
+          mh_apply3(dx3, j2d, mx);
+          mh_apply3(dy3, j2d, my);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            csum[0][k] += mx[k];
+            csum[1][k] += my[k];
+          }
+        }
+      }
+      if constexpr (NC >= 2 && !(MODE == 1 && RS)) {
         double rr[2][6];
         ld6g(a.r, l, c, L, nt, rr[0]);
         ld6g(a.r + P6, l, c, L, nt, rr[1]);
@@ -1985,6 +2030,13 @@ __global__ void __launch_bounds__(TW, 256 / TW) k_hrhs_t(DMesh m, HArgs a, const
 #pragma unroll
       for (int p = 0; p < 3; ++p) csum[cc][p] += j2d * (C.dx[p] * sv[cc][0] + C.dy[p] * sv[cc][1]);
     if constexpr (NC >= 2) {
+      if constexpr (RS) {
+        const double ir = 1.0 / a.rho0;
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+          for (int n = 0; n < 3; ++n) ysum[d][n] -= a.rsum[(d * 3 + n) * nt + c] * ir;
+      }
       double H[3], MH[3][3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) H[k] = eta[k] - C.b[k];
@@ -2102,12 +2154,20 @@ static int launch_tile(pdg_ctx* ctx, const HArgs& a, double* out, cudaStream_t s
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
   const size_t sm = (size_t)2 * (6 * NC + 12) * tj * sizeof(double);
-  static size_t attr[64] = {};
+  static size_t attr[64] = {}, attr_rs[64] = {};
   set_smem(k_hrhs_t<NC, MODE, TW>, sm, attr);
+  if constexpr (MODE == 1 && NC >= 2) set_smem(k_hrhs_t<NC, MODE, TW, true>, sm, attr_rs);
   StagePlanes sp{};
   const size_t P6 = (size_t)6 * ctx->L * ctx->nt, LN = (size_t)ctx->L * ctx->nt;
   for (int w = 0; w < 6 * NC + 12; ++w)
     sp.p[w] = (w < 6 * NC ? a.uc[w / 6] : a.qa + (size_t)((w - 6 * NC) / 6) * P6) + (size_t)(w % 6) * LN;
+  if constexpr (MODE == 1 && NC >= 2) {
+    if (a.rsum) {
+      k_hrhs_t<NC, MODE, TW, true><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), a, sp, tm->tslot, tm->halo,
+                                                                        tm->hoff, tj, out);
+      return PDG_OK;
+    }
+  }
   k_hrhs_t<NC, MODE, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), a, sp, tm->tslot, tm->halo, tm->hoff,
                                                               tj, out);
   return PDG_OK;
@@ -2122,7 +2182,7 @@ static StagePlanes planes_of(const double* base, int nc, const pdg_ctx* ctx) {
 }
 template <bool FROM_T, int TW>
 static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, double alpha, double tref, double g,
-                         double* r, cudaStream_t s) {
+                         double* r, cudaStream_t s, double* rsum = nullptr) {
   const pdg_ctx::TileMap* tm = ensure_tiles(ctx, TW);
   if (!tm) return PDG_ERR_CUDA;
   const int tj = TW + tm->nh_max;
@@ -2131,7 +2191,7 @@ static int launch_r_tile(pdg_ctx* ctx, const double* eta_g, const double* rho, d
   set_smem(k_compute_r_t<FROM_T, TW>, sm, attr);
   k_compute_r_t<FROM_T, TW><<<nblocks(ctx->nown, TW), TW, sm, s>>>(ctx->view(), eta_g, alpha, tref, g,
                                                                  planes_of(rho, 1, ctx), tm->tslot, tm->halo,
-                                                                 tm->hoff, tj, r);
+                                                                 tm->hoff, tj, r, rsum);
   return PDG_OK;
 }
 template <int TW>
@@ -2307,9 +2367,13 @@ int pdg_stress_rhs(pdg_ctx* ctx, const double* ux, const double* uy, double tsx,
 
 // fused stepper entries ----------------------------------------------------------------
 // F3D->2D forcing: column sum of horizontal_rhs(u, q, fac(q)) + stresses  -> [2][3][nt]
-int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r, double g,
-                   double f, double rho0, double tsx, double tsy, double cd, double* f3d2d, void* stream) {
+// rsum (optional, pdg_step_r): the per-column layer sum of jm (r_top + r_bot); used by the
+// tile-staged kernel, which then loads no r
+int pdg_step_f3d2d_rsum(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r,
+                        const double* rsum, double g, double f, double rho0, double tsx, double tsy, double cd,
+                        double* f3d2d, void* stream) {
   HArgs a{};
+  a.rsum = rsum;
   a.eta_u = eta_u;
   a.u = u;
   {
@@ -2345,6 +2409,29 @@ int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const dou
   }
 #undef LAUNCH_ARGS
   return check_launch(ctx);
+}
+
+int pdg_step_f3d2d(pdg_ctx* ctx, const double* eta_u, const double* u, const double* q, const double* r, double g,
+                   double f, double rho0, double tsx, double tsy, double cd, double* f3d2d, void* stream) {
+  return pdg_step_f3d2d_rsum(ctx, eta_u, u, q, r, nullptr, g, f, rho0, tsx, tsy, cd, f3d2d, stream);
+}
+
+// the stepper's baroclinic head from T (EOS inline) and, with the tile-staged kernel, the layer
+// sum rsum [2][3][nt] the F3D->2D kernel takes instead of r; returns 1 in *rsum_written when it did
+int pdg_step_r(pdg_ctx* ctx, const double* eta_g, const double* T, double alpha, double tref, double g, double* r,
+               double* rsum, int* rsum_written, void* stream) {
+  cudaStream_t strm = (cudaStream_t)stream;
+  const int tw = tune_get(TUNE_TILE_COL);
+  if (rsum_written) *rsum_written = 0;
+  if (ctx->nown == 0) return PDG_OK;
+  if (tw == 64 || tw == 128) {
+    const int rc = tw == 64 ? launch_r_tile<true, 64>(ctx, eta_g, T, alpha, tref, g, r, strm, rsum)
+                            : launch_r_tile<true, 128>(ctx, eta_g, T, alpha, tref, g, r, strm, rsum);
+    if (rc) return rc;
+    if (rsum_written) *rsum_written = rsum != nullptr;
+    return check_launch(ctx);
+  }
+  return pdg_compute_r(ctx, eta_g, T, 1, alpha, tref, g, nullptr, 0, r, stream);
 }
 
 // stage right-hand sides: momentum  M0 u0 + dt (F(u, qbar) + stress + M1 F2D/H1),

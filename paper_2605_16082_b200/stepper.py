@@ -65,6 +65,9 @@ class ImexStepper:
         self.wt = z(6, L, nt)
         self.qsum, self.htot, self.f3d2d = z(2, 3, nt), z(3, nt), z(2, 3, nt)
         self.qbar, self.f2d, self.mis = z(2, 3, nt), z(2, 3, nt), z(2, 3, nt)
+        self.rsum = z(2, 3, nt)                  # layer sum of the baroclinic head for F3D->2D
+        self._rs_ok = ctypes.c_int(0)
+        self.use_rsum = os.environ.get("PDG_NO_RSUM", "0") != "1"   # (A/B: F3D->2D reading r instead)
         self.W12 = (z(3, 3, nt), z(3, 3, nt)) if part is not None else None   # RK stage states (partitioned)
         # partitions (>= 3 ghost rings): the RK stages of a substep run on owned + rings 1-2, owned +
         # ring 1 and owned columns, so the 2D state is exchanged once per substep; the last stage
@@ -261,7 +264,8 @@ class ImexStepper:
         if part:   # debug: ghosts of the fields this stage produces stay NaN until their exchange lands
             self._poison([self.q, self.mis, out_u, out_T], False)
             self._poison([self.f3d2d], True)
-        tm("r", lb.pdg_compute_r, h, ptr(eta_u), ptr(T), 1, p.alpha, p.t_ref, p.g, None, 0, ptr(self.r), s)
+        tm("r", lb.pdg_step_r, h, ptr(eta_u), ptr(T), p.alpha, p.t_ref, p.g, ptr(self.r),
+           ptr(self.rsum) if self.use_rsum else None, ctypes.byref(self._rs_ok), s)
         tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
            ptr(self.qsum), ptr(self.htot), s)
         # the 3D ring-1 exchanges block the stream: a boundary-first split (boundary columns, post,
@@ -269,7 +273,8 @@ class ImexStepper:
         # latency-bound partial wave (~0.3-0.6 ms per call at 8 ranks) against ~30 us of transfer
         if part:
             yield ("all", [self.q], "q")
-        tm("f3d2d", lb.pdg_step_f3d2d, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r), p.g, p.f, p.rho0, tsx, tsy,
+        tm("f3d2d", lb.pdg_step_f3d2d_rsum, h, ptr(eta_u), ptr(u), ptr(self.q), ptr(self.r),
+           ptr(self.rsum) if self._rs_ok.value else None, p.g, p.f, p.rho0, tsx, tsy,
            p.cd, ptr(self.f3d2d), s)
         if p.kappa_h:   # explicit horizontal viscosity in horizontal_rhs: its column sum (csrc/hdiff.cu)
             tm("hdiff_f3d2d", lb.pdg_horizontal_diffusion, h, ptr(eta_u), ptr(u), 2, p.kappa_h, 1, 1.0, 1, None, 0,

@@ -61,7 +61,7 @@ def rel(a, b):
 @pytest.mark.parametrize("setting,tol", [
     ({7: 2}, 1e-11),
     ({9: 0}, 1e-12), ({9: 64}, 0.0),
-    ({11: 0}, 0.0), ({11: 64}, 0.0),
+    ({11: 0}, 1e-12), ({11: 64}, 0.0),   # 11=0: register r kernel, F3D->2D then reads r (default: its layer sum)
     # 5=1 / 10=128: other stage-RHS kernels (per-layer masses, another summation order)
     ({5: 1}, 1e-11), ({10: 128}, 1e-11),
     ({6: 0}, 1e-12), ({6: 3}, 1e-12), ({6: 2}, 0.0),   # default 8 = 2 + programmatic dependent launch
