@@ -38,7 +38,7 @@ UNIT = "prism-DOF/s"
 KERNEL_BYTES = {
     "r": 48 + 96,                       # read T, write r (2 comps)
     "project": 96 + 96,                 # read u, write q
-    "f3d2d": 96 * 3,                    # read u, q, r -> 2D only
+    "f3d2d": 96 * 2,                    # read u, q -> 2D only (r enters as its per-column layer sum)
     "wtilde": 96 + 48,                  # read q, write w~
     "rhs_u": 96 * 4 + 96,               # read u, u0, q, r; write rhs
     "rhs_T": 48 + 48 + 96 + 48,         # read T, T0, q; write rhs
