@@ -1302,9 +1302,10 @@ __global__ void __launch_bounds__(128, MINB) k_hrhs(DMesh m, HArgs a, Cols cs, d
 namespace shf {
 enum { J2D = 0, DX = 1, DY = 4, EL = 7, NX = 10, NY = 13, B = 16, ETA = 19, STAB = 22, MO = 28, MN = 34, E0 = 46,
        E1 = 49, F1 = 52, N = 58,
-       // MODE 2: the per-column sigma-layer triangle masses Mjz(H) of the three grids (packed
-       // symmetric), over the B / ETA and E0 / E1 words (the layer loop needs only these)
-       MHU = 16, MH0 = 46, MH1 = 58, N2 = 64 };
+       // MODE 2: the per-column sigma-layer triangle masses Mjz(H) of the stage and start grids
+       // (packed symmetric) over the B / ETA and E0 / E1 words, and in F1 the per-column factor
+       // of the F2D/H1 term (the layer loop needs only these)
+       MHU = 16, MH0 = 46, N2 = 58 };
 }
 
 __device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, double st1, int k, double jm,
@@ -1383,19 +1384,30 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         Hu[k] = eta[k] - C.b[k];
         H0[k] = a.eta0[k * nt + c] - C.b[k];
         H1[k] = e1 - C.b[k];
-        if constexpr (NC >= 2) {
-          SD(shf::F1 + k) = a.f2d[k * nt + c] / H1[k];
-          SD(shf::F1 + 3 + k) = a.f2d[(3 + k) * nt + c] / H1[k];
-        }
       }
+      double MH1[3][3];
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
         for (int q = p; q < 3; ++q) {
           SD(shf::MHU + sym6(p, q)) = T3[p][q][0] * Hu[0] + T3[p][q][1] * Hu[1] + T3[p][q][2] * Hu[2];
           SD(shf::MH0 + sym6(p, q)) = T3[p][q][0] * H0[0] + T3[p][q][1] * H0[1] + T3[p][q][2] * H0[2];
-          SD(shf::MH1 + sym6(p, q)) = T3[p][q][0] * H1[0] + T3[p][q][1] * H1[1] + T3[p][q][2] * H1[2];
+          MH1[p][q] = MH1[q][p] = T3[p][q][0] * H1[0] + T3[p][q][1] * H1[1] + T3[p][q][2] * H1[2];
         }
+      if constexpr (NC >= 2) {
+        // the F2D/H1 broadcast term (K (x) J2D Mjz(eta1)) F summed over the two levels is
+        // jm (KM00 + KM01) J2D Mjz(H1) F: its per-column factor, scaled by jm per layer
+        const double kk = (KM[0][0] + KM[0][1]) * C.j2d;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          double F[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) F[k] = a.f2d[(cc * 3 + k) * nt + c] / H1[k];
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+            SD(shf::F1 + cc * 3 + p) = kk * (MH1[p][0] * F[0] + MH1[p][1] * F[1] + MH1[p][2] * F[2]);
+        }
+      }
     }
   }
   double csum[NC][3];
@@ -1467,16 +1479,11 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         }
         kron_apply(Mu, jj, y0, m0);
         kron_apply(Mu, jj, y1, m1);
-        double M1[3][3];
-        msym(shf::MH1, M1);
-        const double kk = (KM[0][0] + KM[0][1]) * jj;
         double mf[2][3];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const double F0 = SD(shf::F1 + cc * 3), F1v = SD(shf::F1 + cc * 3 + 1), F2 = SD(shf::F1 + cc * 3 + 2);
+        for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-          for (int p = 0; p < 3; ++p) mf[cc][p] = kk * (M1[p][0] * F0 + M1[p][1] * F1v + M1[p][2] * F2);
-        }
+          for (int p = 0; p < 3; ++p) mf[cc][p] = jm * SD(shf::F1 + cc * 3 + p);
 #pragma unroll
         for (int n = 0; n < 6; ++n) {
           acc[0][n] += m0[n] + mf[0][n % 3];
