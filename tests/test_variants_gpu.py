@@ -106,3 +106,35 @@ def test_vertical_column_lists_bitwise(case, implicit):
         torch.cuda.synchronize()
         outs.append(out.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_r_layer_sum(case):
+    """pdg_step_r's rsum is the sum over the layers of jm (r_top + r_bot) of the r it writes
+    (jm = (f_b - f_t) / 2), accumulated in layer order (the device contracts each step into an FMA:
+    equal to the host sum up to a few ulps)."""
+    import ctypes
+
+    import torch
+    from paper_2605_16082_b200.device import ptr, stream_ptr
+    pdg, c, lib, defaults = case
+    for k, v in defaults.items():
+        lib.pdg_tune(k, v)
+    st = pdg.stepper.ImexStepper(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v)
+    st.use_graph = False
+    st.set_state(**c.state)
+    st.step(1)
+    r = torch.zeros_like(st.r)
+    rsum = torch.zeros(2, 3, c.mesh.nt, dtype=torch.float64, device="cuda")
+    ok = ctypes.c_int(0)
+    p = c.params
+    assert lib.pdg_step_r(st.dm.h, ptr(st.S[0]), ptr(st.T[st.cur]), p.alpha, p.t_ref, p.g, ptr(r), ptr(rsum),
+                          ctypes.byref(ok), stream_ptr()) == 0
+    torch.cuda.synchronize()
+    assert ok.value == 1
+    rn, got = r.cpu().numpy(), rsum.cpu().numpy()          # r: [2][6][L][nt]
+    fr = st.dm._fracs                                      # the sigma fractions the kernels use
+    want = np.zeros_like(got)
+    for l in range(c.L):
+        jm = 0.5 * (fr[l + 1] - fr[l])
+        want = want + jm * (rn[:, 0:3, l, :] + rn[:, 3:6, l, :])
+    assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
