@@ -94,13 +94,25 @@ class ImexStepper:
         self.schedule_check = False  # debug: poison in-flight ghost slots (partitioned runs)
         self._skip_exchanges = set()  # tests only: exchange names to leave out (a broken schedule)
         self.phase_trace = None      # list -> per-phase CUDA events of eager steps (phase_csv)
+        self.nvtx = os.environ.get("PDG_NVTX", "0") == "1"   # NVTX range per library launch
         self.concurrent_vertical = os.environ.get("PDG_CONC_VERT", "0") == "1"
 
     def _c(self, name, rc):
         _lib.check(rc, name)
 
     def _timed(self, name, fn, *args):
-        """Launch one library entry; record CUDA events around it on the current stream when profiling."""
+        """Launch one library entry; record CUDA events around it on the current stream when profiling,
+        and an NVTX range around the launch when `nvtx` is set (nsys / ncu --nvtx phase markers)."""
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(name)
+            try:
+                self._timed_inner(name, fn, *args)
+            finally:
+                torch.cuda.nvtx.range_pop()
+            return
+        self._timed_inner(name, fn, *args)
+
+    def _timed_inner(self, name, fn, *args):
         if self.prof is None:
             _lib.check(fn(*args), name)
             return

@@ -204,3 +204,19 @@ def test_diagnostics_csv(pdg, tmp_path):
     assert rows[0][0] == 20.0 and rows[1][0] == 40.0            # stage 1 at the midpoint, stage 2 at t
     vols = [float(r.split(",")[1]) for r in d[1:]]
     assert max(vols) - min(vols) <= 1e-12 * abs(vols[0])         # closed basin: volume conserved
+
+
+def test_nvtx_ranges_do_not_change_the_step(pdg):
+    """With NVTX ranges around every library launch (ImexStepper.nvtx / PDG_NVTX=1) the step is
+    unchanged (the markers are host-side annotations for nsys / ncu --nvtx)."""
+    m, om, p, s0 = _setup(pdg, nx=6, ny=4, L=4)
+    out = []
+    for nvtx in (False, True):
+        st = pdg.stepper.ImexStepper(m, 4, p, 60.0, 4, 1e-3, 1e-4)
+        st.nvtx = nvtx
+        st.use_graph = False
+        st.set_state(**s0)
+        st.step(2)
+        out.append(st.get_state())
+    for k in ("eta", "ux", "T"):
+        assert np.array_equal(out[0][k], out[1][k])
