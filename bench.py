@@ -42,8 +42,9 @@ KERNEL_BYTES = {
     "wtilde": 96 + 48,                  # read q, write w~
     "rhs_u": 96 * 4 + 96,               # read u, u0, q, r; write rhs
     "rhs_T": 48 + 48 + 96 + 48,         # read T, T0, q; write rhs
-    "rhs_uT_s1": 96 * 3 + 48 + 96 + 48,   # stage 1 (u0 = u, T0 = T): read u, q, r, T; write rhs_u, rhs_T = 480
-    "rhs_uT_s2": 96 * 4 + 48 * 2 + 96 + 48,   # stage 2: + u0, T0 = 624
+    # the stage RHS also forms w~ (pdg_step_rhs_ut_w): + write w~ 48 (PDG_NO_FUSEWT=1: separate wtilde)
+    "rhs_uT_s1": 96 * 3 + 48 + 96 + 48 + 48,   # stage 1 (u0 = u, T0 = T): read u, q, r, T; write rhs_u, rhs_T, w~ = 528
+    "rhs_uT_s2": 96 * 4 + 48 * 2 + 96 + 48 + 48,   # stage 2: + u0, T0 = 672
     "vertical_u_impl": 96 + 48 + 96,    # read rhs, w~; write u1
     "vertical_T_impl": 48 + 48 + 48,
     "vertical_u_expl": 96 + 48 + 96 + 96,   # + u for A u
@@ -401,6 +402,8 @@ def main():
     for k, ms in prof.items():
         if k in KERNEL_BYTES:
             b = KERNEL_BYTES[k] * P_local
+            if k.startswith("rhs_uT") and os.environ.get("PDG_NO_FUSEWT", "0") == "1":
+                b -= 48 * P_local
         elif k.startswith("subcycle"):
             msub = int(k[len("subcycle"):])
             b = RK_SUBSTEP_BYTES_PER_TRI * (P_local // case.L) * msub

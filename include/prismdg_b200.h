@@ -289,6 +289,12 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
                     const double* T, const double* u0, const double* T0, const double* q, const double* mis,
                     const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
                     double cd, double dt, double* out_u, double* out_T, void* stream);
+/* pdg_step_rhs_ut and w~ of the stage into w [6][L][nt] (pdg_compute_wtilde with q~ = q + Jz mis):
+ * formed in the same bottom-up layer loop, which already forms q~ and its lateral flux factor */
+int pdg_step_rhs_ut_w(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, const double* u,
+                      const double* T, const double* u0, const double* T0, const double* q, const double* mis,
+                      const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
+                      double cd, double dt, double* out_u, double* out_T, double* w, void* stream);
 /* vertical stage: implicit (M1 - dt A) x = rhs by block Thomas, or explicit x = M1^-1 (rhs + dt A xin),
  * A = assemble_vertical_operator(eta_u, wt, w_m = (z(eta1) - z(eta0)) / dt_mesh, kh, kv) in registers */
 int pdg_step_vertical(pdg_ctx* ctx, int ncomp, int implicit, const double* eta_u, const double* eta0,

@@ -87,6 +87,7 @@ _SIGS = {
     "pdg_step_r": (I, [P, P, P, D, D, D, P, P, P, P]),
     "pdg_step_rhs": (I, [P, I, P, P, P, P, P, P, P, P, P, D, D, D, D, D, D, D, P, P]),
     "pdg_step_rhs_ut": (I, [P, P, P, P, P, P, P, P, P, P, P, P, D, D, D, D, D, D, D, P, P, P]),
+    "pdg_step_rhs_ut_w": (I, [P, P, P, P, P, P, P, P, P, P, P, P, D, D, D, D, D, D, D, P, P, P, P]),
     # columns (csrc/columns.cu)
     "pdg_solve_sweep": (I, [I, I, I, I, P, P, P, P, P, P]),
     "pdg_solve_banded": (I, [I, I, I, P, P, P, P, P, P, P, P, P]),

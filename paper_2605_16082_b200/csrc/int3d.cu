@@ -1007,6 +1007,7 @@ struct HArgs {
   const double* u0c[3];
   double* outc[3];
   const double* rsum = nullptr;   // F3D->2D: per-column layer sum of jm (r_top + r_bot) (RS kernels)
+  double* wt = nullptr;           // STAGE (WT kernels): w~ of the stage, [6][L][nt]
 };
 
 __device__ __forceinline__ void mjz(const double jz[3], double M[3][3]) {
@@ -1305,7 +1306,8 @@ enum { J2D = 0, DX = 1, DY = 4, EL = 7, NX = 10, NY = 13, B = 16, ETA = 19, STAB
        // MODE 2: the per-column sigma-layer triangle masses Mjz(H) of the stage and start grids
        // (packed symmetric) over the B / ETA and E0 / E1 words, and in F1 the per-column factor
        // of the F2D/H1 term (the layer loop needs only these)
-       MHU = 16, MH0 = 46, N2 = 58 };
+       MHU = 16, MH0 = 46, N2 = 58,
+       F6 = 58 };   // WT: 6 / J2D (the Mh^-1 factor of the w~ sweep), one word past N2
 }
 
 __device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, double st1, int k, double jm,
@@ -1325,10 +1327,14 @@ __device__ __forceinline__ void lat_factor_v(double nx, double ny, double st0, d
 }
 
 // SAME: the stage values are the step-start values (stage 1: u == u0, T == T0), so M0 u0 reuses
-// the u words already loaded for the fluxes instead of loading them again
-template <int NC, int MODE, int MINB, bool SAME = false>
+// the u words already loaded for the fluxes instead of loading them again.
+// WT (MODE 2): also w~ (compute_wtilde, internal3d.py:505-541): its right-hand side is the iso-zeta
+// volume moment of q~ and the lateral flux factor this kernel forms anyway, so the layer loop runs
+// bottom-up (the stage RHS has no vertical recurrence) and carries the bed-anchored sweep
+// (columns.py:125-151) -- q~ and its neighbour traces are read once per stage instead of twice.
+template <int NC, int MODE, int MINB, bool SAME = false, bool WT = false>
 __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, double* __restrict__ out) {
-  __shared__ double sdm[(MODE == 2 ? shf::N2 : shf::N) * 64];
+  __shared__ double sdm[(MODE == 2 ? shf::N2 + (WT ? 1 : 0) : shf::N) * 64];
   __shared__ int sim[9 * 64];
   const int tid = threadIdx.x;
   const int i = blockIdx.x * 64 + tid;
@@ -1394,6 +1400,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
           SD(shf::MH0 + sym6(p, q)) = T3[p][q][0] * H0[0] + T3[p][q][1] * H0[1] + T3[p][q][2] * H0[2];
           MH1[p][q] = MH1[q][p] = T3[p][q][0] * H1[0] + T3[p][q][1] * H1[1] + T3[p][q][2] * H1[2];
         }
+      if (WT) SD(shf::F6) = 6.0 / C.j2d;
       if constexpr (NC >= 2) {
         // the F2D/H1 broadcast term (K (x) J2D Mjz(eta1)) F summed over the two levels is
         // jm (KM00 + KM01) J2D Mjz(H1) F: its per-column factor, scaled by jm per layer
@@ -1415,12 +1422,18 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
   for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
     for (int k = 0; k < 3; ++k) csum[cc][k] = 0.0;
-  double fcur = m.fracs[0], fnext = m.fracs[1];  // sigma fractions, loaded one layer ahead
+  // sigma fractions, loaded one layer ahead (WT: bottom-up, from the bed)
+  double fcur = WT ? m.fracs[L] : m.fracs[0], fnext = WT ? m.fracs[L - 1] : m.fracs[1];
   const double rdt = MODE == 2 ? 1.0 / a.dt : 0.0;
-  for (int l = 0; l < L; ++l) {
-    const double ft = fcur, fb = fnext;
+  double ws[3] = {0.0, 0.0, 0.0};   // WT: the w~ sweep value (columns.py:125-151)
+  for (int li = 0; li < L; ++li) {
+    const int l = WT ? L - 1 - li : li;
+    const double ft = WT ? fnext : fcur, fb = WT ? fcur : fnext;
     fcur = fnext;
-    fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
+    if (WT)
+      fnext = l >= 1 ? m.fracs[l - 1] : 0.0;
+    else
+      fnext = l + 2 <= L ? m.fracs[l + 2] : 0.0;
     const double jm = 0.5 * (fb - ft);
     unsigned ln = (unsigned)L * (unsigned)nt;   // plane stride, hidden from the optimiser (see k_vexpl2)
     asm volatile("" : "+r"(ln));
@@ -1551,6 +1564,26 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
           }
       }
     }
+    // WT: w~ right-hand side, the iso-zeta volume moment of q~ first (k_compute_wtilde order)
+    double aw[6];
+    if constexpr (WT) {
+      double wq[2][2], Sm[2][2];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int lev = 0; lev < 2; ++lev)
+          wq[cc][lev] = W1[0] * qv[cc][3 * lev] + W1[1] * qv[cc][3 * lev + 1] + W1[2] * qv[cc][3 * lev + 2];
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+        Sm[mm][0] = KM[mm][0] * wq[0][0] + KM[mm][1] * wq[0][1];
+        Sm[mm][1] = KM[mm][0] * wq[1][0] + KM[mm][1] * wq[1][1];
+      }
+      const double j2d = SD(shf::J2D);
+#pragma unroll
+      for (int lev = 0; lev < 2; ++lev)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) aw[3 * lev + p] = j2d * (SD(shf::DX + p) * Sm[lev][0] + SD(shf::DY + p) * Sm[lev][1]);
+    }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if (sim[k * 64 + tid] != 0) continue;
@@ -1574,6 +1607,7 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
                      qn, f);
       }
       const double je = -(0.5 * SD(shf::EL + k));
+      if (WT) lat_add(aw, k, f, je);
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
         double n4[4], ti[2][2], te[2][2], x[2][2];
@@ -1656,6 +1690,19 @@ __global__ void __launch_bounds__(64, MINB) k_hrhs_s(DMesh m, HArgs a, Cols cs, 
         for (int n = 0; n < 6; ++n) o[n] = a.dt * acc[cc][n];
         st6(a.outc[cc], l, c, L, nt, o);
       }
+    }
+    if constexpr (WT) {   // w_b = s + g_b - g_t, w_t = s + g_b + g_t, s = w_t (columns.py:125-151)
+      const double f6 = SD(shf::F6);
+      double gt[3], gb[3], wo[6];
+      mh_inv3f(aw, f6, gt);
+      mh_inv3f(aw + 3, f6, gb);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        wo[3 + p] = ws[p] + gb[p] - gt[p];
+        wo[p] = ws[p] + gb[p] + gt[p];
+        ws[p] = wo[p];
+      }
+      st6(a.wt, l, c, L, nt, wo);
     }
   }
   if (MODE == 1) {
@@ -2487,11 +2534,12 @@ int pdg_step_rhs(pdg_ctx* ctx, int ncomp, const double* eta_u, const double* eta
 
 // momentum AND tracer stage right-hand sides in one pass (they share q~, the flux factor and the
 // masses): rhs_u = M0 u0 + dt (F_h(u, q~) + stress + M1 F2D/H1), rhs_T = M0 T0 + dt F_T(T, q~)
-int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, const double* u,
-                    const double* T, const double* u0, const double* T0, const double* q, const double* mis,
-                    const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
-                    double cd, double dt, double* out_u, double* out_T, void* stream) {
+static int step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, const double* u,
+                       const double* T, const double* u0, const double* T0, const double* q, const double* mis,
+                       const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
+                       double cd, double dt, double* out_u, double* out_T, double* w, void* stream) {
   HArgs a{};
+  a.wt = w;
   a.eta_u = eta_u;
   a.eta0 = eta0;
   a.eta1 = eta1;
@@ -2520,7 +2568,20 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
   const dim3 grid(nblocks(cs.n, 128)), blk(128);
   cudaStream_t strm = (cudaStream_t)stream;
 #define LAUNCH_ARGS ctx->view(), a, cs, out_u
-  if (const int tw = tune_get(TUNE_TILE_STAGE); tw == 64 || tw == 128) {
+  const int tw = tune_get(TUNE_TILE_STAGE), hv = tune_get(TUNE_HRHS2);
+  const bool same = a.u0c[0] == a.uc[0] && a.u0c[1] == a.uc[1] && a.u0c[2] == a.uc[2];
+  if (w && tw != 64 && tw != 128 && hv == 8) {   // w~ inside the stage RHS (k_hrhs_s<..., WT>)
+    if (same)
+      k_hrhs_s<3, 2, 1, true, true><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    else
+      k_hrhs_s<3, 2, 1, false, true><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
+    return check_launch(ctx);
+  }
+  if (w) {   // other stage-RHS variants: the separate w~ kernel first
+    const int rc = pdg_compute_wtilde(ctx, eta_u, q, nullptr, mis, g, nullptr, 0, w, stream);
+    if (rc) return rc;
+  }
+  if (tw == 64 || tw == 128) {
     if ((tw == 64 ? launch_tile<3, 2, 64>(ctx, a, out_u, strm) : launch_tile<3, 2, 128>(ctx, a, out_u, strm)))
       return PDG_ERR_CUDA;
   } else if (tune_get(TUNE_HRHS2) >= 8) {
@@ -2529,7 +2590,7 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
       k_hrhs_s<3, 2, 6><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
     else if (t == 10)
       k_hrhs_s<3, 2, 8><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
-    else if (a.u0c[0] == a.uc[0] && a.u0c[1] == a.uc[1] && a.u0c[2] == a.uc[2])
+    else if (same)
       k_hrhs_s<3, 2, 1, true><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
     else
       k_hrhs_s<3, 2, 1><<<nblocks(cs.n, 64), 64, 0, strm>>>(LAUNCH_ARGS);
@@ -2538,6 +2599,26 @@ int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const
   }
 #undef LAUNCH_ARGS
   return check_launch(ctx);
+}
+
+int pdg_step_rhs_ut(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, const double* u,
+                    const double* T, const double* u0, const double* T0, const double* q, const double* mis,
+                    const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
+                    double cd, double dt, double* out_u, double* out_T, void* stream) {
+  return step_rhs_ut(ctx, eta_u, eta0, eta1, u, T, u0, T0, q, mis, r, f2d, g, f, rho0, tsx, tsy, cd, dt, out_u, out_T,
+                     nullptr, stream);
+}
+
+// the same, and w~ of the stage (compute_wtilde with q~ = q + Jz mis, as pdg_compute_wtilde) into w
+// [6][L][nt]: formed inside the stage-RHS layer loop (bottom-up), which already forms q~ and its
+// lateral flux factor
+int pdg_step_rhs_ut_w(pdg_ctx* ctx, const double* eta_u, const double* eta0, const double* eta1, const double* u,
+                      const double* T, const double* u0, const double* T0, const double* q, const double* mis,
+                      const double* r, const double* f2d, double g, double f, double rho0, double tsx, double tsy,
+                      double cd, double dt, double* out_u, double* out_T, double* w, void* stream) {
+  if (!w) return PDG_ERR_SHAPE;
+  return step_rhs_ut(ctx, eta_u, eta0, eta1, u, T, u0, T0, q, mis, r, f2d, g, f, rho0, tsx, tsy, cd, dt, out_u, out_T,
+                     w, stream);
 }
 
 }  // extern "C"

@@ -96,6 +96,7 @@ class ImexStepper:
         self.phase_trace = None      # list -> per-phase CUDA events of eager steps (phase_csv)
         self.nvtx = os.environ.get("PDG_NVTX", "0") == "1"   # NVTX range per library launch
         self.concurrent_vertical = os.environ.get("PDG_CONC_VERT", "0") == "1"
+        self.fuse_wt = os.environ.get("PDG_NO_FUSEWT", "0") != "1"   # w~ inside the stage RHS
 
     def _c(self, name, rc):
         _lib.check(rc, name)
@@ -319,13 +320,19 @@ class ImexStepper:
         tm("mismatch", lb.pdg_mismatch, h, ptr(self.qbar), ptr(self.qsum), ptr(self.htot), ptr(self.mis), s)
         if part:
             yield ("all", [self.mis], "mis")
-        tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
-           ptr(self.wt), s)
-        if self.fuse_rhs:
+        if self.fuse_rhs and self.fuse_wt:   # w~ formed in the stage-RHS layer loop (pdg_step_rhs_ut_w)
+            tm("rhs_uT_s1" if u is u0 else "rhs_uT_s2", lb.pdg_step_rhs_ut_w, h, ptr(eta_u), ptr(eta0), ptr(eta1),
+               ptr(u), ptr(T), ptr(u0), ptr(T0), ptr(self.q), ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f,
+               p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), ptr(out_T), ptr(self.wt), s)
+        elif self.fuse_rhs:
+            tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
+               ptr(self.wt), s)
             tm("rhs_uT_s1" if u is u0 else "rhs_uT_s2", lb.pdg_step_rhs_ut, h, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(T), ptr(u0), ptr(T0),
                ptr(self.q), ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s,
                ptr(out_u), ptr(out_T), s)
         else:
+            tm("wtilde", lb.pdg_compute_wtilde, h, ptr(eta_u), ptr(self.q), None, ptr(self.mis), p.g, None, 0,
+               ptr(self.wt), s)
             tm("rhs_u", lb.pdg_step_rhs, h, 2, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(u), ptr(u0), ptr(self.q),
                ptr(self.mis), ptr(self.r), ptr(self.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, dt_s, ptr(out_u), s)
             tm("rhs_T", lb.pdg_step_rhs, h, 1, ptr(eta_u), ptr(eta0), ptr(eta1), ptr(T), ptr(T0), ptr(self.q),

@@ -183,19 +183,27 @@ def test_c4_wtilde_tiled(c4, r_q, mis_wt):
     assert rel(_rows(h, rows_p6(mis_wt.wt, h.ids), L), _rows(h, ref, L)) <= TOL
 
 
+@pytest.mark.parametrize("with_w", [False, True], ids=["rhs", "rhs+wtilde"])
 @pytest.mark.parametrize("same", [False, True], ids=["stage2", "stage1"])
-def test_c4_stage_rhs(c4, r_q, mis_wt, same):
+def test_c4_stage_rhs(c4, r_q, mis_wt, same, with_w):
     """Fused momentum + tracer stage RHS (k_hrhs_s<3, 2>; stage 1: u = u0, T = T0 on G0):
-    rhs_u = M0 u0 + dt (F_h(u, q~) + stress + M1 F2D/H1), rhs_T = M0 T0 + dt F_T(T, q~)."""
+    rhs_u = M0 u0 + dt (F_h(u, q~) + stress + M1 F2D/H1), rhs_T = M0 T0 + dt F_T(T, q~);
+    with_w: pdg_step_rhs_ut_w, the stepper's entry, which also forms w~ (compute_wtilde of q~) in
+    the same bottom-up layer loop (k_hrhs_s<3, 2, .., WT>)."""
     import torch
     lb, check = _lib()
     h, p, L, f = c4.h, c4.p, c4.L, c4.f
     out_u, out_T = torch.empty_like(f.u), torch.empty_like(f.T)
+    w = c4.z(6, L, c4.nt)
     tsx, tsy = p.wind(0.0)
     eta_u, u, T = (f.eta0, f.u0, f.T0) if same else (f.eta_u, f.u, f.T)
-    check(lb.pdg_step_rhs_ut(c4.dm.h, _ptr(eta_u), _ptr(f.eta0), _ptr(f.eta1), _ptr(u), _ptr(T), _ptr(f.u0),
-                             _ptr(f.T0), _ptr(r_q.q), _ptr(mis_wt.mis), _ptr(r_q.r), _ptr(f.f2d), p.g, p.f, p.rho0,
-                             tsx, tsy, p.cd, c4.case.dt, _ptr(out_u), _ptr(out_T), _s()), "rhs_ut")
+    args = (c4.dm.h, _ptr(eta_u), _ptr(f.eta0), _ptr(f.eta1), _ptr(u), _ptr(T), _ptr(f.u0), _ptr(f.T0), _ptr(r_q.q),
+            _ptr(mis_wt.mis), _ptr(r_q.r), _ptr(f.f2d), p.g, p.f, p.rho0, tsx, tsy, p.cd, c4.case.dt, _ptr(out_u),
+            _ptr(out_T))
+    if with_w:
+        check(lb.pdg_step_rhs_ut_w(*args, _ptr(w), _s()), "rhs_ut_w")
+    else:
+        check(lb.pdg_step_rhs_ut(*args, _s()), "rhs_ut")
     c4.dm.raise_errors("rhs_ut")
     Gu, uh, Th = (h.G0, h.u0, h.T0) if same else (h.Gu, h.u, h.T)
     q, r = rows_pv(r_q.q, h.ids), rows_pv(r_q.r, h.ids)          # the kernel's own inputs
@@ -212,6 +220,9 @@ def test_c4_stage_rhs(c4, r_q, mis_wt, same):
     ref_t = OI.mass_apply(M0, h.T0) + dt * OI.tracer_horizontal_rhs(Gu, Th, qb, facb, p)
     assert rel(_rows(h, rows_pv(out_u, h.ids), L), _rows(h, ref_u, L)) <= TOL
     assert rel(_rows(h, rows_p6(out_T, h.ids), L), _rows(h, ref_t, L)) <= TOL
+    if with_w:
+        ref_w = OI.compute_wtilde(Gu, qb, facb)
+        assert rel(_rows(h, rows_p6(w, h.ids), L), _rows(h, ref_w, L)) <= TOL
 
 
 @pytest.mark.parametrize("implicit", [True, False], ids=["implicit", "explicit"])

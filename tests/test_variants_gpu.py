@@ -138,3 +138,42 @@ def test_r_layer_sum(case):
         jm = 0.5 * (fr[l + 1] - fr[l])
         want = want + jm * (rn[:, 0:3, l, :] + rn[:, 3:6, l, :])
     assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+
+
+def test_wtilde_inside_the_stage_rhs(case):
+    """pdg_step_rhs_ut_w forms w~ in the stage-RHS layer loop (bottom-up, k_hrhs_s<.., WT>): the
+    same w~ as pdg_compute_wtilde on the stage's q and mismatch, and the same step."""
+    import torch
+    pdg, c, lib, defaults = case
+    for k, v in defaults.items():
+        lib.pdg_tune(k, v)
+    st = pdg.stepper.ImexStepper(c.mesh, c.L, c.params, c.dt, c.m, c.kv, c.nu_v)
+    st.use_graph = False
+    st.set_state(**c.state)
+    st.step(1)
+    from paper_2605_16082_b200.device import ptr, stream_ptr
+    h, p = st.dm.h, c.params
+    g = torch.Generator(device="cpu").manual_seed(5)
+    mis = (1e-3 * torch.randn(st.mis.shape, generator=g, dtype=torch.float64)).to(st.mis.device)
+    u, T = st.U[st.cur], st.T[st.cur]
+    eta = st.S[0]
+    eta1 = eta + 1e-3
+    st.q.zero_()
+    lib.pdg_project_transport(h, ptr(eta), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(st.q), ptr(st.qsum), ptr(st.htot),
+                              stream_ptr())
+    w_ref, w_got = torch.zeros_like(st.wt), torch.zeros_like(st.wt)
+    ou, oT = torch.zeros_like(u), torch.zeros_like(T)
+    ou2, oT2 = torch.zeros_like(u), torch.zeros_like(T)
+    assert lib.pdg_compute_wtilde(h, ptr(eta), ptr(st.q), None, ptr(mis), p.g, None, 0, ptr(w_ref), stream_ptr()) == 0
+    args = (h, ptr(eta), ptr(eta), ptr(eta1), ptr(u), ptr(T), ptr(u), ptr(T), ptr(st.q), ptr(mis), ptr(st.r),
+            ptr(st.f2d), p.g, p.f, p.rho0, 0.01, -0.02, p.cd, 30.0)
+    assert lib.pdg_step_rhs_ut(*args, ptr(ou), ptr(oT), stream_ptr()) == 0
+    assert lib.pdg_step_rhs_ut_w(*args, ptr(ou2), ptr(oT2), ptr(w_got), stream_ptr()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(ou, ou2) and torch.equal(oT, oT2)
+    err = float((w_got - w_ref).abs().max() / w_ref.abs().max())
+    assert err <= 1e-14, err
+    ref = run(pdg, c, lib, defaults, {}, fuse_wt=False)
+    got = run(pdg, c, lib, defaults, {}, fuse_wt=True)
+    for k in ("eta", "qx", "qy", "ux", "uy", "T"):
+        assert rel(got[k], ref[k]) <= 1e-13, (k, rel(got[k], ref[k]))
