@@ -6,16 +6,16 @@ one defined in DESIGN.md section 3 and restated by the oracle
 implicit vertical solve, stage 2 over dt with m substeps, explicit, from the
 stage-1 midpoint.  Per stage the device work is
 
-  1  compute_r with the EOS inline                    (k_compute_r<FROM_T>)
-  2  q = project(u) + column sum of q + total depth   (k_project<Kronecker>)
-  3  F3D->2D = column sum of (F_h(u, q, fac(q)) + stresses)     (k_hrhs<2, PRED>)
+  1  compute_r with the EOS inline, + its layer sum   (k_compute_r_t<FROM_T>, tile-staged)
+  2  q = project(u) + column sum of q + total depth   (k_project)
+  3  F3D->2D = column sum of (F_h(u, q, fac(q)) + stresses)     (k_hrhs_t<2, PRED, RS>)
   4  m_s SSP-RK3 substeps, one fused kernel per RK stage, + Qbar, F2D
   5  mismatch (Qbar - sum q) / H                      (k_mismatch)
-  6  w~ with qbar = q + Jz mis and its factor on the fly         (k_compute_wtilde<FUSED>)
-  7  rhs_u = M0 u0 + dt (F_h(u, qbar) + stress + M1 F2D/H1)      (k_hrhs<2, STAGE>)
-     rhs_T = M0 T0 + dt F_T(T, qbar)                             (k_hrhs<1, STAGE>)
-  8  vertical: (M1 - dt A) x = rhs (block Thomas) or x = M1^-1 (rhs + dt A x)
-     with A assembled per layer in registers          (k_vstep<NC, IMPLICIT>)
+  6  rhs_u = M0 u0 + dt (F_h(u, qbar) + stress + M1 F2D/H1), rhs_T = M0 T0 + dt F_T(T, qbar),
+     and w~ (qbar = q + Jz mis and its factor on the fly; bottom-up layer loop carrying the
+     w~ sweep)                                        (k_hrhs_s<3, STAGE, .., WT>)
+  7  vertical: (M1 - dt A) x = rhs (block Thomas: k_vimpl_fwd + k_vimpl_bwd_r) or
+     x = M1^-1 (rhs + dt A x) (k_vexpl3), A assembled per layer in registers
 
 The flux factors, qbar, prism masses, mesh velocity and the banded matrices
 are never materialised.  The whole step is one CUDA graph.
