@@ -6,15 +6,16 @@
 // .so has no link-time NCCL dependency.  A halo plan holds, per peer rank, the device index lists
 // of the owned columns to send and of the ghost slots to fill, and message buffers sized for the
 // largest exchange.  An exchange is
-//     start:  pack (one kernel per field and peer) on the caller's stream -> event ->
-//             grouped ncclSend/ncclRecv to every peer on the plan's communication stream
-//     finish: the caller's stream waits for the communication -> unpack
+//     start:  pack (one kernel for every field and peer, grid.y = peer) on the caller's stream ->
+//             event -> grouped ncclSend/ncclRecv to every peer on the plan's communication stream
+//     finish: the caller's stream waits for the communication -> unpack (one kernel)
 // everything stream ordered, so the caller launches interior work between start and finish and
 // the whole partitioned step can be captured in one CUDA graph (NCCL point-to-point operations
 // are capturable; the event fork/join becomes graph edges).
 #include <dlfcn.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 
 #include <vector>
@@ -62,15 +63,69 @@ struct pdg_comm {
   cudaStream_t cs = nullptr;  // communication stream (high priority)
 };
 
+namespace pdg {
+struct HaloFields {
+  const double* f[8];
+  long long np[8];
+};
+struct HaloPeerDev {                    // per peer: index lists and message buffers (device)
+  const int* sidx;
+  const int* ridx;
+  int nsend, nrecv;
+  double* sbuf;
+  double* rbuf;
+};
+// every field's boundary values for every peer (blockIdx.y = peer) into its [planes][nsend] buffer
+__global__ void k_halo_pack_all(HaloFields F, int nt, const HaloPeerDev* __restrict__ pd, long long tot) {
+  const HaloPeerDev q = pd[blockIdx.y];
+  const int n = q.nsend;
+  const long long total = tot * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long p = t / n;
+    const int c = (int)(t - p * n);
+    int f = 0;
+    while (p >= F.np[f]) p -= F.np[f++];
+    q.sbuf[t] = F.f[f][p * nt + q.sidx[c]];
+  }
+}
+__global__ void k_halo_unpack_all(HaloFields F, int nt, const HaloPeerDev* __restrict__ pd, long long tot) {
+  const HaloPeerDev q = pd[blockIdx.y];
+  const int n = q.nrecv;
+  const long long total = tot * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long p = t / n;
+    const int c = (int)(t - p * n);
+    int f = 0;
+    while (p >= F.np[f]) p -= F.np[f++];
+    const_cast<double*>(F.f[f])[p * nt + q.ridx[c]] = q.rbuf[t];
+  }
+}
+}  // namespace pdg
+
 struct pdg_halo_plan {
   pdg_comm* c = nullptr;
   int nt = 0, max_planes = 0;
   std::vector<int> peers, nsend, nrecv;
   std::vector<int*> sidx, ridx;         // device index lists (copies owned by the plan)
   std::vector<double*> sbuf, rbuf;      // [max_planes][n] per peer
+  pdg::HaloPeerDev* pdev = nullptr;     // the same, per peer, for the all-peer kernels (device)
+  int max_send = 0, max_recv = 0;
   cudaEvent_t packed = nullptr, done = nullptr;
   long long planes = 0;                 // planes of the exchange in flight
 };
+
+static bool halo_fields(int nf, double* const* fields, const long long* nplanes, pdg::HaloFields& F, long long& tot) {
+  if (nf < 1 || nf > 8) return false;
+  tot = 0;
+  for (int f = 0; f < 8; ++f) {
+    F.f[f] = f < nf ? fields[f] : nullptr;
+    F.np[f] = f < nf ? nplanes[f] : (1LL << 62);
+    if (f < nf) tot += nplanes[f];
+  }
+  return true;
+}
 
 using namespace pdg;
 extern "C" {
@@ -146,6 +201,7 @@ int pdg_halo_plan_destroy(pdg_halo_plan* p) {
   for (auto* q : p->ridx) cudaFree(q);
   for (auto* q : p->sbuf) cudaFree(q);
   for (auto* q : p->rbuf) cudaFree(q);
+  cudaFree(p->pdev);
   if (p->packed) cudaEventDestroy(p->packed);
   if (p->done) cudaEventDestroy(p->done);
   delete p;
@@ -182,6 +238,17 @@ int pdg_halo_plan_create(pdg_comm* c, int nt, int npeers, const int* peers, cons
     if (ok && nsend[i]) ok = cudaMemcpy(si, send_idx[i], sizeof(int) * nsend[i], cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok && nrecv[i]) ok = cudaMemcpy(ri, recv_idx[i], sizeof(int) * nrecv[i], cudaMemcpyHostToDevice) == cudaSuccess;
   }
+  if (ok) {
+    std::vector<HaloPeerDev> d;
+    for (int i = 0; i < npeers; ++i) {
+      d.push_back({p->sidx[i], p->ridx[i], p->nsend[i], p->nrecv[i], p->sbuf[i], p->rbuf[i]});
+      p->max_send = std::max(p->max_send, p->nsend[i]);
+      p->max_recv = std::max(p->max_recv, p->nrecv[i]);
+    }
+    ok = cudaMalloc(&p->pdev, sizeof(HaloPeerDev) * (npeers + 1)) == cudaSuccess &&
+         (npeers == 0 ||
+          cudaMemcpy(p->pdev, d.data(), sizeof(HaloPeerDev) * npeers, cudaMemcpyHostToDevice) == cudaSuccess);
+  }
   if (!ok) {
     pdg_halo_plan_destroy(p);
     return PDG_ERR_CUDA;
@@ -195,17 +262,15 @@ int pdg_halo_plan_create(pdg_comm* c, int nt, int npeers, const int* peers, cons
 // planes of nt doubles each.
 int pdg_halo_start(pdg_halo_plan* p, int nf, double* const* fields, const long long* nplanes, void* stream) {
   if (!p) return PDG_ERR_SHAPE;
+  HaloFields F;
   long long tot = 0;
-  for (int f = 0; f < nf; ++f) tot += nplanes[f];
-  if (tot > p->max_planes) return PDG_ERR_SHAPE;
+  if (!halo_fields(nf, fields, nplanes, F, tot) || tot > p->max_planes) return PDG_ERR_SHAPE;
   const cudaStream_t s = (cudaStream_t)stream;
-  for (size_t i = 0; i < p->peers.size(); ++i) {
-    long long off = 0;
-    for (int f = 0; f < nf; ++f) {
-      if (pdg_halo_pack(fields[f], nplanes[f], p->nt, p->sidx[i], p->nsend[i], p->sbuf[i] + off * p->nsend[i], s))
-        return PDG_ERR_CUDA;
-      off += nplanes[f];
-    }
+  const int np = (int)p->peers.size();
+  if (np > 0 && p->max_send > 0) {
+    const int nb = (int)std::min<long long>((tot * p->max_send + 255) / 256, std::max(1, 4 * 148 / np));
+    k_halo_pack_all<<<dim3(nb, np), 256, 0, s>>>(F, p->nt, p->pdev, tot);
+    if (cudaGetLastError() != cudaSuccess) return PDG_ERR_CUDA;
   }
   p->planes = tot;
   if (cudaEventRecord(p->packed, s) != cudaSuccess) return PDG_ERR_CUDA;
@@ -231,16 +296,14 @@ int pdg_halo_finish(pdg_halo_plan* p, int nf, double* const* fields, const long 
   if (!p) return PDG_ERR_SHAPE;
   const cudaStream_t s = (cudaStream_t)stream;
   if (cudaStreamWaitEvent(s, p->done, 0) != cudaSuccess) return PDG_ERR_CUDA;
+  HaloFields F;
   long long tot = 0;
-  for (int f = 0; f < nf; ++f) tot += nplanes[f];
-  if (tot != p->planes) return PDG_ERR_SHAPE;
-  for (size_t i = 0; i < p->peers.size(); ++i) {
-    long long off = 0;
-    for (int f = 0; f < nf; ++f) {
-      if (pdg_halo_unpack(p->rbuf[i] + off * p->nrecv[i], nplanes[f], p->nt, p->ridx[i], p->nrecv[i], fields[f], s))
-        return PDG_ERR_CUDA;
-      off += nplanes[f];
-    }
+  if (!halo_fields(nf, fields, nplanes, F, tot) || tot != p->planes) return PDG_ERR_SHAPE;
+  const int np = (int)p->peers.size();
+  if (np > 0 && p->max_recv > 0) {
+    const int nb = (int)std::min<long long>((tot * p->max_recv + 255) / 256, std::max(1, 4 * 148 / np));
+    k_halo_unpack_all<<<dim3(nb, np), 256, 0, s>>>(F, p->nt, p->pdev, tot);
+    if (cudaGetLastError() != cudaSuccess) return PDG_ERR_CUDA;
   }
   return PDG_OK;
 }

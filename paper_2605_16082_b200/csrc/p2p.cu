@@ -4,12 +4,14 @@
 // Every rank owns one device buffer ("inbox") holding, per peer it receives from, an epoch flag
 // and a double-buffered receive window [2][max_planes][nrecv].  The buffer is mapped by the peers
 // (CUDA IPC between processes; the raw pointer for ranks that share a process).  An exchange is
-//     start:  per peer, one kernel packs the boundary columns of every field and STORES them
-//             straight into the peer's window (parity = epoch & 1) through the peer pointer, then
-//             the last block to finish publishes the new epoch in the peer's flag (release,
-//             system scope) -- pack, transfer and signal are one launch;
-//     finish: per peer, one kernel waits (acquire, system scope) until the flag reaches the
-//             expected epoch and scatters its own window into the ghost slots.
+// two launches whatever the number of peers (grid.y = peer):
+//     start:  the blocks of peer i pack the boundary columns of every field and STORE them
+//             straight into peer i's window (parity = epoch & 1) through the peer pointer; the
+//             last of them to finish publishes the new epoch in peer i's flag (release, system
+//             scope) -- pack, transfer and signal in one launch;
+//     finish: the blocks of peer i wait (acquire, system scope) until its flag reaches the
+//             expected epoch and scatter the window into the ghost slots; the last of them
+//             advances the expected epoch.
 // The epochs live in device memory (sent / expected counters advanced by the kernels), so the
 // launches carry no per-exchange host values and a captured CUDA graph can be replayed.
 // Two windows suffice: ghost rings are symmetric (a rank that sends to a peer also receives from
@@ -35,13 +37,28 @@ struct Peer {
 };
 }  // namespace
 
+namespace pdg {
+// what the all-peer kernels need per peer (device array, refreshed by pdg_p2p_connect)
+struct PeerDev {
+  const int* sidx;
+  const int* ridx;
+  int nsend, nrecv;
+  double* rwin;          // my window in the peer's inbox
+  unsigned* rflag;       // my flag in the peer's inbox
+  const double* win;     // the peer's window in my inbox
+  const unsigned* flag;  // the peer's flag in my inbox
+};
+}  // namespace pdg
+
 struct pdg_p2p {
   int nt = 0, max_planes = 0, device = 0;
   std::vector<Peer> peers;
   char* inbox = nullptr;
   size_t inbox_bytes = 0;
   unsigned* counters = nullptr;   // [2][npeers] sent / expected epochs (device)
-  unsigned* done = nullptr;       // [npeers] blocks finished packing for the current epoch (device)
+  unsigned* done = nullptr;       // [2][npeers] blocks finished pushing / pulling the current epoch
+  pdg::PeerDev* pdev = nullptr;   // [npeers] (device)
+  int max_send = 0, max_recv = 0;
   long long planes = 0;           // planes of the exchange in flight (host check)
 };
 
@@ -62,61 +79,71 @@ struct P2PFields {
   int nf;
 };
 
-// pack every field's send columns straight into the peer's window (parity of the next epoch),
-// then the last block publishes the epoch
-__global__ void k_p2p_push(P2PFields F, int nt, const int* __restrict__ idx, int n, double* remote_win, long long wstride,
-                           unsigned* sent, unsigned* done, unsigned* remote_flag, long long total) {
-  const unsigned epoch = *sent + 1;   // read before any block can advance it (advanced by the last block)
-  double* win = remote_win + (epoch & 1u) * wstride;
+// every peer in one launch: blockIdx.y = peer, blockIdx.x strides over its (plane, column) words
+__global__ void k_p2p_push_all(P2PFields F, int nt, const PeerDev* __restrict__ pd, long long wplanes,
+                               long long tot, unsigned* sent, unsigned* done) {
+  const int i = blockIdx.y;
+  const PeerDev q = pd[i];
+  const unsigned epoch = sent[i] + 1;   // advanced only by the last block of this peer
+  const int n = q.nsend > 0 ? q.nsend : 1;
+  double* win = q.rwin + (epoch & 1u) * (wplanes * q.nsend);
+  const long long total = tot * q.nsend;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     long long p = t / n;
-    const int i = (int)(t - p * n);
+    const int c = (int)(t - p * n);
     int f = 0;
     while (p >= F.np[f]) p -= F.np[f++];
-    win[t] = F.f[f][p * nt + idx[i]];
+    win[t] = F.f[f][p * nt + q.sidx[c]];
   }
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(done, 1u);
-    if (prev == gridDim.x - 1) {       // every block's stores are fenced: publish, reset for reuse
-      *done = 0u;
-      *sent = epoch;
+    const unsigned prev = atomicAdd(done + i, 1u);
+    if (prev == gridDim.x - 1) {   // every block of this peer has stored and fenced: publish
+      done[i] = 0u;
+      sent[i] = epoch;
       __threadfence_system();
-      st_release_sys(remote_flag, epoch);
+      st_release_sys(q.rflag, epoch);
     }
   }
 }
 
-// wait for the peer's epoch, then fill the ghost slots from my window
-__global__ void k_p2p_pull(P2PFields F, int nt, const int* __restrict__ idx, int n, const double* my_win,
-                           long long wstride, const unsigned* flag, const unsigned* expected, long long total) {
-  const unsigned want = *expected + 1;
+__global__ void k_p2p_pull_all(P2PFields F, int nt, const PeerDev* __restrict__ pd, long long wplanes,
+                               long long tot, unsigned* expected, unsigned* done) {
+  const int i = blockIdx.y;
+  const PeerDev q = pd[i];
+  const unsigned want = expected[i] + 1;   // advanced only by the last block of this peer
   if (threadIdx.x == 0) {
-    // bounded wait: a peer that never publishes (broken schedule, dead rank) aborts the kernel
-    // with an error after kP2PTimeoutNs instead of hanging the device
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (ld_acquire_sys(flag) < want) {
+    while (ld_acquire_sys(q.flag) < want) {
       __nanosleep(200);
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > kP2PTimeoutNs) __trap();
     }
   }
   __syncthreads();
-  const double* win = my_win + (want & 1u) * wstride;
+  const int n = q.nrecv > 0 ? q.nrecv : 1;
+  const double* win = q.win + (want & 1u) * (wplanes * q.nrecv);
+  const long long total = tot * q.nrecv;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     long long p = t / n;
-    const int i = (int)(t - p * n);
+    const int c = (int)(t - p * n);
     int f = 0;
     while (p >= F.np[f]) p -= F.np[f++];
-    const_cast<double*>(F.f[f])[p * nt + idx[i]] = __ldcg(win + t);   // written by the peer: bypass L1
+    const_cast<double*>(F.f[f])[p * nt + q.ridx[c]] = __ldcg(win + t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(done + i, 1u);
+    if (prev == gridDim.x - 1) {   // every block of this peer has read `want`: advance it
+      done[i] = 0u;
+      expected[i] = want;
+    }
   }
 }
-// advance the expected epoch once every block of the pull has read it
-__global__ void k_p2p_advance(unsigned* expected) { *expected += 1u; }
 }  // namespace pdg
 
 using namespace pdg;
@@ -150,6 +177,7 @@ int pdg_p2p_destroy(pdg_p2p* p) {
   cudaFree(p->inbox);
   cudaFree(p->counters);
   cudaFree(p->done);
+  cudaFree(p->pdev);
   delete p;
   return PDG_OK;
 }
@@ -184,8 +212,13 @@ int pdg_p2p_create(int nt, int npeers, const int* peers, const int* nsend, const
        cudaMemset(p->inbox, 0, (size_t)npeers * kFlagBytes + 256) == cudaSuccess &&
        cudaMalloc(&p->counters, sizeof(unsigned) * (2 * npeers + 1)) == cudaSuccess &&
        cudaMemset(p->counters, 0, sizeof(unsigned) * (2 * npeers + 1)) == cudaSuccess &&
-       cudaMalloc(&p->done, sizeof(unsigned) * (npeers + 1)) == cudaSuccess &&
-       cudaMemset(p->done, 0, sizeof(unsigned) * (npeers + 1)) == cudaSuccess;
+       cudaMalloc(&p->done, sizeof(unsigned) * (2 * npeers + 1)) == cudaSuccess &&
+       cudaMemset(p->done, 0, sizeof(unsigned) * (2 * npeers + 1)) == cudaSuccess &&
+       cudaMalloc(&p->pdev, sizeof(PeerDev) * (npeers + 1)) == cudaSuccess;
+  for (const auto& q : p->peers) {
+    p->max_send = std::max(p->max_send, q.nsend);
+    p->max_recv = std::max(p->max_recv, q.nrecv);
+  }
   if (!ok) {
     pdg_p2p_destroy(p);
     return PDG_ERR_CUDA;
@@ -229,6 +262,9 @@ int pdg_p2p_connect(pdg_p2p* p, int slot, const void* ipc_handle, void* raw, lon
   }
   q.rwin_off = win_off;
   q.rflag_off = flag_off;
+  PeerDev d{q.sidx, q.ridx, q.nsend, q.nrecv, (double*)(q.remote + win_off), (unsigned*)(q.remote + flag_off),
+            (const double*)(p->inbox + q.win_off), (const unsigned*)(p->inbox + q.flag_off)};
+  if (cudaMemcpy(p->pdev + slot, &d, sizeof(d), cudaMemcpyHostToDevice) != cudaSuccess) return PDG_ERR_CUDA;
   return PDG_OK;
 }
 
@@ -239,15 +275,12 @@ int pdg_p2p_start(pdg_p2p* p, int nf, double* const* fields, const long long* np
   if (!fields_of(nf, fields, nplanes, F, tot) || tot > p->max_planes) return PDG_ERR_SHAPE;
   const cudaStream_t s = (cudaStream_t)stream;
   const int np = (int)p->peers.size();
-  for (int i = 0; i < np; ++i) {
-    const Peer& q = p->peers[i];
+  for (const auto& q : p->peers)
     if (!q.remote) return PDG_ERR_SHAPE;
-    const long long total = tot * q.nsend;
-    const int nb = (int)std::min<long long>(std::max<long long>(1, (total + 255) / 256), 4 * 148);
-    double* rwin = (double*)(q.remote + q.rwin_off);
-    unsigned* rflag = (unsigned*)(q.remote + q.rflag_off);
-    k_p2p_push<<<nb, 256, 0, s>>>(F, p->nt, q.sidx, q.nsend > 0 ? q.nsend : 1, rwin,
-                                   (long long)p->max_planes * q.nsend, p->counters + i, p->done + i, rflag, total);
+  if (np > 0) {
+    const int nb = (int)std::min<long long>(std::max<long long>(1, (tot * p->max_send + 255) / 256),
+                                            std::max(1, 4 * 148 / np));
+    k_p2p_push_all<<<dim3(nb, np), 256, 0, s>>>(F, p->nt, p->pdev, p->max_planes, tot, p->counters, p->done);
   }
   p->planes = tot;
   return check_launch_noctx();
@@ -260,16 +293,11 @@ int pdg_p2p_finish(pdg_p2p* p, int nf, double* const* fields, const long long* n
   if (!fields_of(nf, fields, nplanes, F, tot) || tot != p->planes) return PDG_ERR_SHAPE;
   const cudaStream_t s = (cudaStream_t)stream;
   const int np = (int)p->peers.size();
-  for (int i = 0; i < np; ++i) {
-    const Peer& q = p->peers[i];
-    const long long total = tot * q.nrecv;
-    const int nb = (int)std::min<long long>(std::max<long long>(1, (total + 255) / 256), 4 * 148);
-    const double* win = (const double*)(p->inbox + q.win_off);
-    const unsigned* flag = (const unsigned*)(p->inbox + q.flag_off);
-    unsigned* expected = p->counters + np + i;
-    k_p2p_pull<<<nb, 256, 0, s>>>(F, p->nt, q.ridx, q.nrecv > 0 ? q.nrecv : 1, win,
-                                   (long long)p->max_planes * q.nrecv, flag, expected, total);
-    k_p2p_advance<<<1, 1, 0, s>>>(expected);
+  if (np > 0) {
+    const int nb = (int)std::min<long long>(std::max<long long>(1, (tot * p->max_recv + 255) / 256),
+                                            std::max(1, 4 * 148 / np));
+    k_p2p_pull_all<<<dim3(nb, np), 256, 0, s>>>(F, p->nt, p->pdev, p->max_planes, tot, p->counters + np,
+                                                 p->done + np);
   }
   return check_launch_noctx();
 }
