@@ -2,7 +2,8 @@
 the reference's algorithm beyond point comparisons): r vanishes for a uniform density, the
 consistent transport integrates to the external-mode transport, the lateral flux factor is
 antisymmetric across every interior face, uniform flow over a flat bed gives w = 0 in columns
-without walls, and `els` subsets return exactly the rows of the full evaluation."""
+without walls, `els` subsets return exactly the rows of the full evaluation, and the column sum
+of the w~ right-hand side is the free-surface residual of the external transport (criterion 6b)."""
 import numpy as np
 import pytest
 
@@ -103,3 +104,59 @@ def test_els_subsets_return_the_full_rows(pdg):
     q = full_q
     full_f, sub_f = I.lateral_flux_factor(G, q, p), I.lateral_flux_factor(G, q, p, els=els)
     assert np.array_equal(sub_f[els] if sub_f.shape[0] == m.nt else sub_f, full_f[els])
+
+
+def _wtilde_rhs_column_sum(pdg, G, w, L):
+    """Rebuild the w~ right-hand side from w~ (the bed-anchored sweep inverted, columns.py:125-151:
+    g_t = (w_t - w_b)/2, g_b = (w_t + w_b)/2 - w_t(below), rhs = Mh g) and sum it over the column."""
+    nt = G.mesh.nt
+    w = np.asarray(w).reshape(nt, L, 6)
+    j2d = np.asarray(G.mesh.j2d)
+    mh = lambda v: pdg.columns.apply_mh(v, j2d)   # noqa: E731
+    out = np.zeros((nt, 3))
+    s = np.zeros((nt, 3))
+    for l in range(L - 1, -1, -1):
+        wt, wb = w[:, l, 0:3], w[:, l, 3:6]
+        out += np.asarray(mh(0.5 * (wt - wb))) + np.asarray(mh(0.5 * (wt + wb) - s))
+        s = wt
+    return out
+
+
+def test_wtilde_rhs_column_sum_is_the_free_surface_residual(pdg):
+    """SPEC criterion 6b: the column sum of the w~ right-hand side equals
+    rhs_free_surface with the external-mode transport Qbar -- for the API w~ (compute_wtilde) and
+    for the w~ the stepper forms inside the stage RHS (pdg_step_rhs_ut_w, q~ = q + Jz mis)."""
+    import torch
+
+    from paper_2605_16082_b200 import _lib
+    from paper_2605_16082_b200.device import ptr, stream_ptr
+    m, G, rng, L = _case(pdg, _wavy)
+    P = m.nt * L
+    I = pdg.internal3d
+    p = pdg.PhysParams()
+    ux, uy = 0.3 * rng.standard_normal((P, 6)), 0.3 * rng.standard_normal((P, 6))
+    q = I.project_transport(G, ux, uy)
+    qbx, qby = rng.standard_normal((m.nt, 3)), rng.standard_normal((m.nt, 3))
+    qb = I.consistent_transport(G, q, qbx, qby)
+    fs = np.asarray(pdg.external2d.rhs_free_surface(pdg.State2D(np.asarray(G.eta), qbx, qby, 0.0), m, p))
+    scale = np.abs(fs).max()
+    w_api = I.compute_wtilde(G, qb, I.lateral_flux_factor(G, qb, p))
+    assert np.abs(_wtilde_rhs_column_sum(pdg, G, w_api, L) - fs).max() <= 1e-13 * scale
+    # the stepper's w~: the stage RHS with its mismatch, on the same grid (eta0 = eta1 = eta)
+    st = pdg.stepper.ImexStepper(m, L, p, 30.0, 2, 1e-3, 1e-4)
+    st.set_state(np.asarray(G.eta), qbx, qby, ux, uy, np.full((P, 6), 10.0))
+    lib, h = _lib.lib(), st.dm.h
+    eta = st.S[0]
+    u, T = st.U[st.cur], st.T[st.cur]
+    assert lib.pdg_project_transport(h, ptr(eta), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(st.q), ptr(st.qsum),
+                                     ptr(st.htot), stream_ptr()) == 0
+    qbar2d = torch.as_tensor(np.stack([qbx.T, qby.T]).copy(), device=st.dev)     # [2][3][nt]
+    assert lib.pdg_mismatch(h, ptr(qbar2d), ptr(st.qsum), ptr(st.htot), ptr(st.mis), stream_ptr()) == 0
+    w = torch.zeros_like(st.wt)
+    ou, oT = torch.zeros_like(u), torch.zeros_like(T)
+    assert lib.pdg_step_rhs_ut_w(h, ptr(eta), ptr(eta), ptr(eta), ptr(u), ptr(T), ptr(u), ptr(T), ptr(st.q),
+                                 ptr(st.mis), ptr(st.r), ptr(st.f2d), p.g, p.f, p.rho0, 0.0, 0.0, 0.0, 30.0,
+                                 ptr(ou), ptr(oT), ptr(w), stream_ptr()) == 0
+    torch.cuda.synchronize()
+    w_rows = np.asarray(w.cpu()).reshape(6, L, m.nt).transpose(2, 1, 0).reshape(P, 6)
+    assert np.abs(_wtilde_rhs_column_sum(pdg, G, w_rows, L) - fs).max() <= 1e-13 * scale
