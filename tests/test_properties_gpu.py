@@ -160,3 +160,46 @@ def test_wtilde_rhs_column_sum_is_the_free_surface_residual(pdg):
     torch.cuda.synchronize()
     w_rows = np.asarray(w.cpu()).reshape(6, L, m.nt).transpose(2, 1, 0).reshape(P, 6)
     assert np.abs(_wtilde_rhs_column_sum(pdg, G, w_rows, L) - fs).max() <= 1e-13 * scale
+
+
+def test_linear_flow_flat_bed_analytic_vertical_velocity(pdg):
+    """SURVEY.md section 4 known answer: u = (x / Lx, 0) over a flat bed gives w = -(z - b) div u =
+    -(z - b) / Lx at every node of the columns without walls (P1 represents u exactly)."""
+    def flat(x, y):
+        return np.full_like(x, -25.0)
+    lx = 2e4
+    m = pdg.mesh.hilbert_reorder(pdg.mesh.generate_basin_mesh(14, 9, lx, 1e4, flat))
+    L = 5
+    G = pdg.mesh.extrude(m, pdg.LayerPolicy(count=L), np.zeros((m.nt, 3)))
+    P = m.nt * L
+    I = pdg.internal3d
+    p = pdg.PhysParams()
+    xs = np.asarray(m.x) / lx                                        # (nt, 3) corners
+    ux = np.repeat(np.concatenate([xs, xs], axis=1), L, axis=0)      # (P, 6): p = c L + l
+    uy = np.zeros((P, 6))
+    q = I.project_transport(G, ux, uy)
+    w = np.asarray(I.compute_w(G, q, ux, uy, p, I.lateral_flux_factor(G, q, p))).reshape(m.nt, L, 6)
+    f = np.arange(L + 1) / L                                         # uniform sigma fractions
+    H = 25.0
+    z_minus_b = np.empty((L, 6))
+    for lev, fr in ((0, f[:-1]), (1, f[1:])):
+        z_minus_b[:, 3 * lev:3 * lev + 3] = (H - fr * H)[:, None]
+    ref = -z_minus_b / lx
+    inner = np.flatnonzero((m.nbr >= 0).all(axis=1))
+    assert inner.size > 0
+    assert np.abs(w[inner] - ref[None]).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_projection_reproduces_constant_transport(pdg):
+    """SURVEY.md section 4 known answer: on a flat surface over a flat bed (constant Jz) a constant
+    velocity projects to q = Jz u exactly (to rounding)."""
+    def flat(x, y):
+        return np.full_like(x, -20.0)
+    m = pdg.mesh.hilbert_reorder(pdg.mesh.generate_basin_mesh(10, 7, 1e4, 1e4, flat))
+    L = 4
+    G = pdg.mesh.extrude(m, pdg.LayerPolicy(count=L), np.zeros((m.nt, 3)))
+    P = m.nt * L
+    q = np.asarray(pdg.internal3d.project_transport(G, np.full((P, 6), 0.7), np.full((P, 6), -0.2)))
+    jz = 0.5 * 20.0 / L
+    assert np.abs(q[..., 0] - 0.7 * jz).max() <= 1e-14 * 0.7 * jz
+    assert np.abs(q[..., 1] + 0.2 * jz).max() <= 1e-14 * 0.7 * jz
