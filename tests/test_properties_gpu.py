@@ -29,13 +29,17 @@ def _wavy(x, y):
     return -30.0 + 8.0 * np.sin(np.pi * x / 2e4) * np.cos(2 * np.pi * y / 1e4) - 5e-4 * x
 
 
-def test_r_vanishes_for_uniform_density_under_a_flat_surface(pdg):
+@pytest.mark.parametrize("surface", ["flat", "elementwise_jumps"])
+def test_r_vanishes_for_uniform_density(pdg, surface):
+    """SPEC criterion 11: constant rho' gives r = 0 -- also with a free surface that is constant on
+    each element and jumps between elements (every term is a gradient or a jump of rho', or the
+    surface fold rho'_s grad eta, which vanishes inside each element)."""
     m, G, rng, L = _case(pdg, _wavy)
-    G = pdg.mesh.extrude(m, pdg.LayerPolicy(count=L), np.zeros((m.nt, 3)))
+    eta = np.zeros((m.nt, 3)) if surface == "flat" else np.repeat(0.3 * rng.standard_normal((m.nt, 1)), 3, axis=1)
+    G = pdg.mesh.extrude(m, pdg.LayerPolicy(count=L), eta)
     p = pdg.PhysParams()
     rho = np.full((m.nt * L, 6), 0.37)
     r = pdg.internal3d.compute_r(G, rho, p)
-    # every term is a gradient or a jump of rho', or the surface fold rho'_s grad eta (flat here):
     # zero up to the rounding of sum_p grad phi_p = 0 and of the sigma-layer metric terms
     assert np.abs(r).max() <= 1e-12 * p.g * 0.37 * 40.0
 
