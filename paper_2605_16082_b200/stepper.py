@@ -96,6 +96,7 @@ class ImexStepper:
         self.phase_trace = None      # list -> per-phase CUDA events of eager steps (phase_csv)
         self.nvtx = os.environ.get("PDG_NVTX", "0") == "1"   # NVTX range per library launch
         self.concurrent_vertical = os.environ.get("PDG_CONC_VERT", "0") == "1"
+        self.concurrent_rp = os.environ.get("PDG_CONC_RP", "0") == "1"   # r || projection (A/B)
         self.fuse_wt = os.environ.get("PDG_NO_FUSEWT", "0") != "1"   # w~ inside the stage RHS
 
     def _c(self, name, rc):
@@ -277,10 +278,21 @@ class ImexStepper:
         if part:   # debug: ghosts of the fields this stage produces stay NaN until their exchange lands
             self._poison([self.q, self.mis, out_u, out_T], False)
             self._poison([self.f3d2d], True)
-        tm("r", lb.pdg_step_r, h, ptr(eta_u), ptr(T), p.alpha, p.t_ref, p.g, ptr(self.r),
-           ptr(self.rsum) if self.use_rsum else None, ctypes.byref(self._rs_ok), s)
+        r_args = (h, ptr(eta_u), ptr(T), p.alpha, p.t_ref, p.g, ptr(self.r),
+                  ptr(self.rsum) if self.use_rsum else None, ctypes.byref(self._rs_ok))
+        conc_rp = self.concurrent_rp and self.prof is None
+        if conc_rp:   # r (FP64-bound) on a second stream, overlapping the HBM-bound projection
+            main = torch.cuda.current_stream(self.dev)
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                _lib.check(lb.pdg_step_r(*r_args, stream_ptr()), "r")
+        else:
+            tm("r", lb.pdg_step_r, *r_args, s)
         tm("project", lb.pdg_project_transport, h, ptr(eta_u), ptr(u[0]), ptr(u[1]), None, None, 0, ptr(self.q),
            ptr(self.qsum), ptr(self.htot), s)
+        if conc_rp:
+            main.wait_stream(side)
         # the 3D ring-1 exchanges block the stream: a boundary-first split (boundary columns, post,
         # interior) was measured slower -- the extra launch of the 50-layer column loops costs a
         # latency-bound partial wave (~0.3-0.6 ms per call at 8 ranks) against ~30 us of transfer
