@@ -42,6 +42,10 @@ def main():
     from paper_2605_16082_b200.partition import PartitionedRun, exchanges_per_step
     from paper_2605_16082_b200.scenarios import device_state_c4, make_case
     from rank_overhead import NullHalo
+    from paper_2605_16082_b200 import _lib
+    for kv in filter(None, os.environ.get("PDG_TUNE", "").split(",")):   # A/B: pdg_tune key=value[,..]
+        k, v = kv.split("=")
+        _lib.lib().pdg_tune(int(k), int(v))
     Ps = [int(a) for a in sys.argv[1:]] or [2, 4, 8]
     case = make_case("c4", with_state=False)
     for P in Ps:
