@@ -77,6 +77,21 @@ def test_variant_matches_default(case, setting, tol):
 
 
 
+@pytest.mark.parametrize("attrs", [
+    {"concurrent_rp": True}, {"concurrent_vertical": True},
+    {"concurrent_rp": True, "concurrent_vertical": True, "use_graph": True},
+])
+def test_second_stream_variants_bitwise(case, attrs):
+    """The step-graph variants with a second stream (r beside the projection, PDG_CONC_RP; the tracer
+    vertical solve beside the momentum one, PDG_CONC_VERT; both measured without gain, DESIGN.md
+    section 5) run the same kernels on independent data: bitwise equal to the single-stream step."""
+    pdg, c, lib, defaults = case
+    ref = run(pdg, c, lib, defaults, {})
+    got = run(pdg, c, lib, defaults, {}, **attrs)
+    for k in ("eta", "qx", "qy", "ux", "uy", "T"):
+        assert np.array_equal(got[k], ref[k]), (attrs, k)
+
+
 @pytest.mark.parametrize("implicit", [1, 0])
 def test_vertical_column_lists_bitwise(case, implicit):
     """pdg_step_vertical_cols over two complementary column lists == one launch over all columns
